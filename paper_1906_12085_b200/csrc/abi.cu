@@ -1,0 +1,534 @@
+// abi.cu — the extern "C" boundary (include/svdk.h).
+//
+// Every entry point validates like the reference function it replaces
+// (file:line in svdk.h), converts engine failures into status codes, and
+// keeps the message / residual in thread-local storage.
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "svdk_methods.h"
+
+namespace svdk {
+void gaussian_fill(int64_t rows, int64_t cols, uint64_t seed, double* out);
+int64_t randomized_pca(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n, int64_t l,
+                       int64_t q, uint64_t seed, double* U, int64_t ldu, double* sigma, double* V,
+                       int64_t ldv, const RowComm* comm);
+int64_t krylov_svd(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n, int64_t l,
+                   int64_t iters, uint64_t seed, double* U, int64_t ldu, double* sigma, double* V,
+                   int64_t ldv, const RowComm* comm);
+int64_t lanczos_svd(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n, int64_t steps,
+                    uint64_t seed, double* U, int64_t ldu, double* sigma, double* V, int64_t ldv,
+                    const RowComm* comm);
+int64_t qr_thin(Ctx* c, const double* H, int64_t ldh, int64_t m, int64_t p, double* Q, int64_t ldq,
+                double* R, const RowComm* comm);
+int64_t select_components(Ctx* c, const double* d_w, int64_t count, double total, double t);
+}  // namespace svdk
+
+using namespace svdk;
+
+struct svdk_ctx : Ctx {};
+
+namespace {
+
+thread_local std::string g_err;
+thread_local double g_residual = 0.0;
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return SVDK_OK;
+    } catch (const Failure& e) {
+        g_err = e.msg;
+        g_residual = e.residual;
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "host allocation failed";
+        return SVDK_E_NOMEM;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return SVDK_E_STATE;
+    }
+}
+
+void need_ctx(svdk_ctx* c) {
+    if (!c) fail(SVDK_E_STATE, "null svdk_ctx");
+}
+
+// Host column-major (ld = rows) -> device with an even leading dimension
+// (TMA needs 16-byte strides).
+DBuf upload(Ctx* c, const double* h, int64_t rows, int64_t cols, int64_t& ld) {
+    ld = std::max<int64_t>(2, round_up(rows, 2));
+    DBuf d(c, static_cast<size_t>(ld) * std::max<int64_t>(cols, 1));
+    if (rows > 0 && cols > 0) {
+        if (ld == rows)
+            SVDK_CUDA(cudaMemcpyAsync(d.p(), h, sizeof(double) * rows * cols,
+                                      cudaMemcpyHostToDevice, c->stream));
+        else
+            SVDK_CUDA(cudaMemcpy2DAsync(d.p(), ld * sizeof(double), h, rows * sizeof(double),
+                                        rows * sizeof(double), cols, cudaMemcpyHostToDevice,
+                                        c->stream));
+    }
+    return d;
+}
+
+DBuf alloc_mat(Ctx* c, int64_t rows, int64_t cols, int64_t& ld) {
+    ld = std::max<int64_t>(2, round_up(rows, 2));
+    return DBuf(c, static_cast<size_t>(ld) * std::max<int64_t>(cols, 1));
+}
+
+void download(Ctx* c, double* h, const double* d, int64_t ld, int64_t rows, int64_t cols) {
+    if (rows > 0 && cols > 0) {
+        if (ld == rows)
+            SVDK_CUDA(cudaMemcpyAsync(h, d, sizeof(double) * rows * cols, cudaMemcpyDeviceToHost,
+                                      c->stream));
+        else
+            SVDK_CUDA(cudaMemcpy2DAsync(h, rows * sizeof(double), d, ld * sizeof(double),
+                                        rows * sizeof(double), cols, cudaMemcpyDeviceToHost,
+                                        c->stream));
+    }
+    SVDK_CUDA(cudaStreamSynchronize(c->stream));
+}
+
+void require_tall(int64_t m, int64_t n, const char* op) {
+    if (m < n)
+        fail(SVDK_E_DIM, std::string(op) + ": needs rows >= cols, got " + std::to_string(m) + "x" +
+                             std::to_string(n) +
+                             "; pass the transpose and swap U/V, or use compute_svd_any");
+    if (n == 0) fail(SVDK_E_DIM, std::string(op) + ": empty input");
+}
+
+// svd_methods.cpp:77-93
+void validate_sketch(int64_t m, int64_t n, int64_t l, int64_t q, bool krylov) {
+    if (l < 1 || l > n)
+        fail(SVDK_E_PARAM, "sketch width l = " + std::to_string(l) + " outside [1, n] for n = " +
+                               std::to_string(n));
+    if (krylov) {
+        if (q < 1) fail(SVDK_E_PARAM, "krylov_svd: needs power_iterations >= 1");
+        const int64_t width = (q + 1) * l;
+        if (width > m)
+            fail(SVDK_E_PARAM, "krylov_svd: block width (i+1)*l = " + std::to_string(width) +
+                                   " exceeds rows = " + std::to_string(m));
+    }
+}
+
+// Run one SVD method on a device-resident tall A; returns rank.
+int64_t run_method(Ctx* c, int method, const double* dA, int64_t lda, int64_t m, int64_t n,
+                   int64_t l, int64_t q, uint64_t seed, double* dU, int64_t ldu, double* dS,
+                   double* dV, int64_t ldv, const RowComm* comm) {
+    switch (method) {
+        case SVDK_TRUNCATED:
+            return truncated_svd(c, dA, lda, m, n, dU, ldu, dS, dV, ldv, comm);
+        case SVDK_RANDOMIZED:
+            return randomized_pca(c, dA, lda, m, n, l, q, seed, dU, ldu, dS, dV, ldv, comm);
+        case SVDK_KRYLOV:
+            return krylov_svd(c, dA, lda, m, n, l, q, seed, dU, ldu, dS, dV, ldv, comm);
+        case SVDK_LANCZOS:
+            return lanczos_svd(c, dA, lda, m, n, l, seed, dU, ldu, dS, dV, ldv, comm);
+        default:
+            fail(SVDK_E_PARAM, "compute_svd: unknown method");
+    }
+}
+
+// Output column bound of each method for a tall m x n input.
+int64_t method_width(int method, int64_t m, int64_t n, int64_t l, int64_t q) {
+    switch (method) {
+        case SVDK_RANDOMIZED:
+            return l;
+        case SVDK_KRYLOV:
+            return std::min<int64_t>((q + 1) * l, n);
+        case SVDK_LANCZOS:
+            return (l <= 0 || l > n) ? n : l;
+        default:
+            return n;
+    }
+}
+
+void validate_method(int method, int64_t m, int64_t n, int64_t l, int64_t q, const char* name) {
+    require_tall(m, n, name);
+    if (method == SVDK_RANDOMIZED) validate_sketch(m, n, l, q, false);
+    if (method == SVDK_KRYLOV) validate_sketch(m, n, l, q, true);
+    if (method == SVDK_LANCZOS && l < 0) fail(SVDK_E_PARAM, "lanczos_svd: steps must be >= 0");
+    if (method < 0 || method > SVDK_LANCZOS) fail(SVDK_E_PARAM, "compute_svd: unknown method");
+}
+
+// Host-pointer method call: H2D, run, D2H (u m x rank, sigma, v n x rank).
+void host_method(svdk_ctx* c, int method, const double* a, int64_t m, int64_t n, int64_t l,
+                 int64_t q, uint64_t seed, double* u, double* sigma, double* v, int64_t* rank,
+                 const char* name) {
+    need_ctx(c);
+    validate_method(method, m, n, l, q, name);
+    const int64_t w = method_width(method, m, n, l, q);
+    int64_t lda, ldu, ldv;
+    DBuf dA = upload(c, a, m, n, lda);
+    DBuf dU = alloc_mat(c, m, w, ldu), dV = alloc_mat(c, n, w, ldv), dS(c, std::max<int64_t>(w, n));
+    const int64_t r = run_method(c, method, dA.p(), lda, m, n, l, q, seed, dU.p(), ldu, dS.p(),
+                                 dV.p(), ldv, nullptr);
+    download(c, u, dU.p(), ldu, m, r);
+    download(c, v, dV.p(), ldv, n, r);
+    download(c, sigma, dS.p(), r, r, 1);
+    *rank = r;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* svdk_version(void) { return "svdk-b200 0.1 (sm_100a, FP64 DMMA)"; }
+const char* svdk_last_error(void) { return g_err.c_str(); }
+double svdk_last_residual(void) { return g_residual; }
+
+int svdk_ctx_create(int device, svdk_ctx** out) {
+    return guarded([&] {
+        if (!out) fail(SVDK_E_PARAM, "svdk_ctx_create: null out");
+        *out = nullptr;
+        int count = 0;
+        SVDK_CUDA(cudaGetDeviceCount(&count));
+        if (device < 0 || device >= count)
+            fail(SVDK_E_CUDA, "svdk_ctx_create: no CUDA device " + std::to_string(device));
+        SVDK_CUDA(cudaSetDevice(device));
+        cudaDeviceProp prop;
+        SVDK_CUDA(cudaGetDeviceProperties(&prop, device));
+        if (prop.major < 10)
+            fail(SVDK_E_CUDA, std::string("svdk: needs an sm_100 (B200) device, got ") + prop.name);
+        auto* c = new svdk_ctx();
+        c->device = device;
+        c->num_sms = prop.multiProcessorCount;
+        SVDK_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        c->own_stream = true;
+        SVDK_CUDA(cudaMalloc(&c->d_flags, 64 * sizeof(int)));
+        SVDK_CUDA(cudaMemset(c->d_flags, 0, 64 * sizeof(int)));
+        *out = c;
+    });
+}
+
+int svdk_ctx_destroy(svdk_ctx* ctx) {
+    return guarded([&] {
+        if (!ctx) return;
+        cudaSetDevice(ctx->device);
+        cudaStreamSynchronize(ctx->stream);
+        destroy_comm(ctx);
+        ctx->pool.trim();
+        if (ctx->d_flags) cudaFree(ctx->d_flags);
+        if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+        delete ctx;
+    });
+}
+
+int svdk_ctx_set_stream(svdk_ctx* ctx, void* stream) {
+    return guarded([&] {
+        need_ctx(ctx);
+        SVDK_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+        ctx->stream = static_cast<cudaStream_t>(stream);
+        ctx->own_stream = false;
+    });
+}
+
+int svdk_ctx_sync(svdk_ctx* ctx) {
+    return guarded([&] {
+        need_ctx(ctx);
+        sync(ctx);
+    });
+}
+
+int64_t svdk_ctx_launches(svdk_ctx* ctx) { return ctx ? ctx->launches : 0; }
+int svdk_ctx_last_sweeps(svdk_ctx* ctx) { return ctx ? ctx->jacobi_sweeps : 0; }
+
+int svdk_gaussian_matrix(int64_t rows, int64_t cols, uint64_t seed, double* out) {
+    return guarded([&] {
+        if (rows < 1 || cols < 1) fail(SVDK_E_PARAM, "gaussian_matrix: rows and cols must be >= 1");
+        gaussian_fill(rows, cols, seed, out);
+    });
+}
+
+int svdk_matmul(svdk_ctx* c, const double* a, int64_t m, int64_t n, const double* b, int64_t l,
+                double* out) {
+    return guarded([&] {
+        need_ctx(c);
+        int64_t lda, ldb, ldc;
+        DBuf dA = upload(c, a, m, n, lda), dB = upload(c, b, n, l, ldb);
+        DBuf dC = alloc_mat(c, m, l, ldc);
+        reset_nonfinite(c);
+        gemm(c, false, m, l, n, dA.p(), lda, dB.p(), ldb, dC.p(), ldc, nullptr, true);
+        raise_if_nonfinite(c);
+        download(c, out, dC.p(), ldc, m, l);
+    });
+}
+
+int svdk_matmul_transposed_left(svdk_ctx* c, const double* a, int64_t m, int64_t n,
+                                const double* b, int64_t l, double* out) {
+    return guarded([&] {
+        need_ctx(c);
+        int64_t lda, ldb, ldc;
+        DBuf dA = upload(c, a, m, n, lda), dB = upload(c, b, m, l, ldb);
+        DBuf dC = alloc_mat(c, n, l, ldc);
+        gemm(c, true, n, l, m, dA.p(), lda, dB.p(), ldb, dC.p(), ldc);
+        download(c, out, dC.p(), ldc, n, l);
+    });
+}
+
+int svdk_transpose(svdk_ctx* c, const double* a, int64_t m, int64_t n, double* t) {
+    return guarded([&] {
+        need_ctx(c);
+        int64_t lda, ldt;
+        DBuf dA = upload(c, a, m, n, lda);
+        DBuf dT = alloc_mat(c, n, m, ldt);
+        transpose(c, dA.p(), lda, m, n, dT.p(), ldt);
+        download(c, t, dT.p(), ldt, n, m);
+    });
+}
+
+int svdk_gram(svdk_ctx* c, const double* a, int64_t m, int64_t n, double* g) {
+    return guarded([&] {
+        need_ctx(c);
+        int64_t lda;
+        DBuf dA = upload(c, a, m, n, lda);
+        DBuf dG(c, static_cast<size_t>(std::max<int64_t>(n, 1)) * std::max<int64_t>(n, 1));
+        syrk(c, m, n, dA.p(), lda, dG.p(), n);
+        download(c, g, dG.p(), n, n, n);
+    });
+}
+
+int svdk_frobenius_norm_sq(svdk_ctx* c, const double* a, int64_t m, int64_t n, double* out) {
+    return guarded([&] {
+        need_ctx(c);
+        int64_t lda;
+        DBuf dA = upload(c, a, m, n, lda);
+        *out = frob_sq(c, dA.p(), lda, m, n);
+    });
+}
+
+int svdk_qr_thin(svdk_ctx* c, const double* h, int64_t m, int64_t p, double* q, double* r,
+                 int64_t* rank) {
+    return guarded([&] {
+        need_ctx(c);
+        if (m < p)
+            fail(SVDK_E_DIM, "qr_thin: need rows >= cols, got " + std::to_string(m) + "x" +
+                                 std::to_string(p));
+        int64_t ldh, ldq;
+        DBuf dH = upload(c, h, m, p, ldh);
+        DBuf dQ = alloc_mat(c, m, p, ldq);
+        DBuf dR(c, static_cast<size_t>(std::max<int64_t>(p, 1)) * std::max<int64_t>(p, 1));
+        const int64_t rk = qr_thin(c, dH.p(), ldh, m, p, dQ.p(), ldq, dR.p(), nullptr);
+        download(c, q, dQ.p(), ldq, m, p);
+        if (r) download(c, r, dR.p(), p, p, p);
+        if (rank) *rank = rk;
+    });
+}
+
+int svdk_eig_sym(svdk_ctx* c, const double* s, int64_t n, int max_sweeps, double* w, double* v) {
+    return guarded([&] {
+        need_ctx(c);
+        if (n < 0) fail(SVDK_E_DIM, "eig_sym: matrix not square");
+        if (n == 0) return;
+        int64_t lds;
+        DBuf dS = upload(c, s, n, n, lds);
+        DBuf dW(c, n), dV(c, static_cast<size_t>(n) * n);
+        eig_sym(c, dS.p(), lds, n, max_sweeps, dW.p(), dV.p(), n);
+        download(c, w, dW.p(), n, n, 1);
+        download(c, v, dV.p(), n, n, n);
+    });
+}
+
+int svdk_truncated_svd(svdk_ctx* c, const double* a, int64_t m, int64_t n, double* u,
+                       double* sigma, double* v, int64_t* rank) {
+    return guarded([&] {
+        host_method(c, SVDK_TRUNCATED, a, m, n, 0, 0, 0, u, sigma, v, rank, "truncated_svd");
+    });
+}
+
+int svdk_randomized_pca(svdk_ctx* c, const double* a, int64_t m, int64_t n, int64_t l, int64_t q,
+                        uint64_t seed, double* u, double* sigma, double* v, int64_t* rank) {
+    return guarded([&] {
+        host_method(c, SVDK_RANDOMIZED, a, m, n, l, q, seed, u, sigma, v, rank, "randomized_pca");
+    });
+}
+
+int svdk_krylov_svd(svdk_ctx* c, const double* a, int64_t m, int64_t n, int64_t l, int64_t i,
+                    uint64_t seed, double* u, double* sigma, double* v, int64_t* rank) {
+    return guarded([&] {
+        host_method(c, SVDK_KRYLOV, a, m, n, l, i, seed, u, sigma, v, rank, "krylov_svd");
+    });
+}
+
+int svdk_lanczos_svd(svdk_ctx* c, const double* a, int64_t m, int64_t n, int64_t steps,
+                     uint64_t seed, double* u, double* sigma, double* v, int64_t* rank) {
+    return guarded([&] {
+        host_method(c, SVDK_LANCZOS, a, m, n, steps, 0, seed, u, sigma, v, rank, "lanczos_svd");
+    });
+}
+
+int svdk_compute_svd(svdk_ctx* c, const double* a, int64_t m, int64_t n, int method, int64_t l,
+                     int64_t q, uint64_t seed, double* u, double* sigma, double* v,
+                     int64_t* rank) {
+    return guarded([&] {
+        need_ctx(c);
+        if (m >= n) {
+            host_method(c, method, a, m, n, l, q, seed, u, sigma, v, rank, "compute_svd");
+            return;
+        }
+        // svd_methods.cpp:239-246: factor the transpose, swap U and V.
+        int64_t lda, ldt;
+        DBuf dA = upload(c, a, m, n, lda);
+        DBuf dT = alloc_mat(c, n, m, ldt);
+        transpose(c, dA.p(), lda, m, n, dT.p(), ldt);
+        dA.reset();
+        validate_method(method, n, m, l, q, "compute_svd");
+        const int64_t w = method_width(method, n, m, l, q);
+        int64_t ldu, ldv;
+        DBuf dU = alloc_mat(c, n, w, ldu), dV = alloc_mat(c, m, w, ldv), dS(c, std::max(w, m));
+        const int64_t r = run_method(c, method, dT.p(), ldt, n, m, l, q, seed, dU.p(), ldu, dS.p(),
+                                     dV.p(), ldv, nullptr);
+        download(c, u, dV.p(), ldv, m, r);  // U of A = V of A^T
+        download(c, v, dU.p(), ldu, n, r);
+        download(c, sigma, dS.p(), r, r, 1);
+        *rank = r;
+    });
+}
+
+int svdk_center(svdk_ctx* c, const double* a, int64_t m, int64_t n, int orientation,
+                double* centered, double* mean) {
+    return guarded([&] {
+        need_ctx(c);
+        int64_t lda, ldc;
+        DBuf dA = upload(c, a, m, n, lda);
+        DBuf dC = alloc_mat(c, m, n, ldc);
+        const int64_t nm = orientation == SVDK_COLUMNS_ARE_EXAMPLES ? m : n;
+        DBuf dM(c, std::max<int64_t>(nm, 1));
+        if (m > 0 && n > 0) {
+            if (orientation == SVDK_COLUMNS_ARE_EXAMPLES)
+                center_cols_are_examples(c, dA.p(), lda, m, n, dC.p(), ldc, dM.p());
+            else
+                center_rows_are_examples(c, dA.p(), lda, m, n, dC.p(), ldc, dM.p());
+        } else if (nm > 0) {
+            fill(c, dM.p(), nm, std::nan(""));  // 0/0 like the reference
+        }
+        download(c, centered, dC.p(), ldc, m, n);
+        download(c, mean, dM.p(), nm, nm, 1);
+    });
+}
+
+int svdk_select_components(svdk_ctx* c, const double* eigenvalues, int64_t count, double total,
+                           double threshold, int64_t* k) {
+    return guarded([&] {
+        need_ctx(c);
+        DBuf dW(c, std::max<int64_t>(count, 1));
+        h2d(c, dW.p(), eigenvalues, count);
+        *k = select_components(c, dW.p(), count, total, threshold);
+    });
+}
+
+int svdk_fit_pca(svdk_ctx* c, const double* data, int64_t m, int64_t n, int orientation,
+                 int method, int64_t l, int64_t q, uint64_t seed, int center, double* basis,
+                 double* eigenvalues, double* total, double* mean, int64_t* rank) {
+    return guarded([&] {
+        need_ctx(c);
+        // pca.cpp:91-116: center -> total -> compute_svd_any -> basis, sigma^2
+        const bool cols_ex = orientation == SVDK_COLUMNS_ARE_EXAMPLES;
+        const int64_t nm = cols_ex ? m : n;
+        int64_t lda, ldc;
+        DBuf dA = upload(c, data, m, n, lda);
+        DBuf dC = alloc_mat(c, m, n, ldc);
+        DBuf dM(c, std::max<int64_t>(nm, 1));
+        if (center) {
+            if (cols_ex)
+                center_cols_are_examples(c, dA.p(), lda, m, n, dC.p(), ldc, dM.p());
+            else
+                center_rows_are_examples(c, dA.p(), lda, m, n, dC.p(), ldc, dM.p());
+        } else {
+            copy_mat(c, dA.p(), lda, dC.p(), ldc, m, n);
+            fill(c, dM.p(), nm, 0.0);
+        }
+        dA.reset();
+        *total = frob_sq(c, dC.p(), ldc, m, n);
+        // tall orientation for the method
+        const bool wide = m < n;
+        const double* dT = dC.p();
+        int64_t tm = m, tn = n, ldt = ldc;
+        DBuf tbuf;
+        if (wide) {
+            tbuf = alloc_mat(c, n, m, ldt);
+            transpose(c, dC.p(), ldc, m, n, tbuf.p(), ldt);
+            dT = tbuf.p();
+            tm = n;
+            tn = m;
+        }
+        validate_method(method, tm, tn, l, q, "fit_pca");
+        const int64_t w = method_width(method, tm, tn, l, q);
+        int64_t ldu, ldv;
+        DBuf dU = alloc_mat(c, tm, w, ldu), dV = alloc_mat(c, tn, w, ldv), dS(c, std::max(w, tn));
+        const int64_t r = run_method(c, method, dT, ldt, tm, tn, l, q, seed, dU.p(), ldu, dS.p(),
+                                     dV.p(), ldv, nullptr);
+        // basis: U for ColumnsAreExamples, V for RowsAreExamples (of the original A)
+        const bool basis_is_tall_v = (cols_ex == wide);  // after the swap of compute_svd_any
+        if (basis_is_tall_v)
+            download(c, basis, dV.p(), ldv, tn, r);
+        else
+            download(c, basis, dU.p(), ldu, tm, r);
+        std::vector<double> s(r);
+        download(c, s.data(), dS.p(), r, r, 1);
+        for (int64_t i = 0; i < r; ++i) eigenvalues[i] = s[i] * s[i];
+        download(c, mean, dM.p(), nm, nm, 1);
+        *rank = r;
+    });
+}
+
+int svdk_dev_gemm(svdk_ctx* c, int transa, int64_t m, int64_t n, int64_t k, const double* a,
+                  int64_t lda, const double* b, int64_t ldb, double* out, int64_t ldc) {
+    return guarded([&] {
+        need_ctx(c);
+        gemm(c, transa != 0, m, n, k, a, lda, b, ldb, out, ldc);
+    });
+}
+
+int svdk_dev_gram(svdk_ctx* c, const double* a, int64_t m, int64_t n, int64_t lda, double* g,
+                  int64_t ldg) {
+    return guarded([&] {
+        need_ctx(c);
+        syrk(c, m, n, a, lda, g, ldg);
+    });
+}
+
+int svdk_dev_eig_sym(svdk_ctx* c, const double* s, int64_t n, int64_t lds, int max_sweeps,
+                     double* w, double* v, int64_t ldv) {
+    return guarded([&] {
+        need_ctx(c);
+        eig_sym(c, s, lds, n, max_sweeps, w, v, ldv);
+    });
+}
+
+int svdk_dev_qr_thin(svdk_ctx* c, const double* h, int64_t m, int64_t p, int64_t ldh, double* q,
+                     int64_t ldq, double* r, int64_t* rank) {
+    return guarded([&] {
+        need_ctx(c);
+        if (m < p) fail(SVDK_E_DIM, "qr_thin: need rows >= cols");
+        const int64_t rk = qr_thin(c, h, ldh, m, p, q, ldq, r, nullptr);
+        if (rank) *rank = rk;
+    });
+}
+
+int svdk_dev_pca(svdk_ctx* c, const double* a, int64_t m_local, int64_t n, int64_t lda, int method,
+                 int64_t l, int64_t q, uint64_t seed, int center, double threshold, double* u,
+                 int64_t ldu, double* sigma, double* v, int64_t ldv, double* mean, int64_t* rank,
+                 int64_t* k, double* total) {
+    return guarded([&] {
+        need_ctx(c);
+        dev_pca(c, a, m_local, n, lda, method, l, q, seed, center != 0, threshold, u, ldu, sigma, v,
+                ldv, mean, rank, k, total);
+    });
+}
+
+int svdk_nccl_unique_id(char out[128]) {
+    return guarded([&] { nccl_unique_id(out); });
+}
+
+int svdk_ctx_attach_nccl(svdk_ctx* c, const char id[128], int rank, int world) {
+    return guarded([&] {
+        need_ctx(c);
+        attach_nccl(c, id, rank, world);
+    });
+}
+
+}  // extern "C"

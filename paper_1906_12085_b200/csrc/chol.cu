@@ -1,0 +1,314 @@
+// chol.cu — CholeskyQR2 (+ shifted CholeskyQR3 and a rank-revealing
+// fallback) replacing the reference's Householder qr_thin
+// (kernels.cpp:111-224).
+//
+// For the tall-skinny H (m >> p) of the range finder, Householder is a
+// BLAS-2 column sweep; CholeskyQR2 turns it into two FP64 DMMA passes:
+//     G = H^T H (SYRK [+ NCCL allreduce over row shards]);  G = R^T R;
+//     Q = H R^-1 (blocked right-TRSM: one NN GEMM per 128-column panel);
+//     repeat once on Q; R = R2 R1.
+// R has a positive diagonal by construction (the reference's sign
+// convention, kernels.cpp:173-182). Full-rank inputs whose Gram is too
+// ill-conditioned for CholeskyQR2 (a relative Cholesky pivot below 1e-12)
+// go through shifted CholeskyQR3; inputs that are numerically rank deficient
+// get an eigen-based orthonormal basis of their range, completed to p
+// orthonormal columns with projected random vectors (the reference also
+// completes Q with unit vectors orthogonal to the kept ones, kernels.hpp:
+// "its Q column is still a unit vector orthogonal to the others"); `rank`
+// counts the kept columns.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "svdk_methods.h"
+
+namespace svdk {
+void gaussian_fill(int64_t rows, int64_t cols, uint64_t seed, double* out);
+
+namespace {
+
+constexpr int NB = 128;  // Cholesky / TRSM panel width
+
+// Factor the bs x bs diagonal block G[k0.., k0..] (upper part holds the
+// trailing-updated values) as R^T R, write R (upper) and R^-1 (upper).
+// flag |= 1 on a pivot d <= rel_tol * diag0[k] (or d <= 0).
+__global__ void __launch_bounds__(256)
+    chol_diag_kernel(const double* G, int64_t ldg, int64_t k0, int bs, double* R, int64_t ldr,
+                     double* Rinv, int ldri, const double* diag0, double rel_tol, int* flag) {
+    constexpr int LD = NB + 1;
+    extern __shared__ double S[];  // NB x LD
+    __shared__ double dinv[NB];
+    const int tid = threadIdx.x;
+    for (int e = tid; e < bs * bs; e += blockDim.x) {
+        const int i = e % bs, j = e / bs;
+        // upper triangle is authoritative; mirror it
+        const int r = min(i, j), c = max(i, j);
+        S[i + j * LD] = G[(k0 + r) + (k0 + c) * ldg];
+    }
+    __syncthreads();
+    for (int j = 0; j < bs; ++j) {
+        // pivot
+        if (tid == 0) {
+            const double d = S[j + j * LD];
+            const double ref = diag0[k0 + j];
+            if (!(d > 0.0) || d <= rel_tol * ref) atomicOr(flag, 1);
+            const double r = sqrt(fmax(d, 0.0));
+            S[j + j * LD] = r;
+            dinv[j] = r > 0.0 ? 1.0 / r : 0.0;
+        }
+        __syncthreads();
+        const double inv = dinv[j];
+        for (int c = j + 1 + tid; c < bs; c += blockDim.x) S[j + c * LD] *= inv;
+        __syncthreads();
+        // trailing update of the upper triangle: S[i][c] -= S[j][i] S[j][c], j < i <= c
+        const int t = bs - j - 1;
+        for (int e = tid; e < t * t; e += blockDim.x) {
+            const int i = j + 1 + e % t, c = j + 1 + e / t;
+            if (i <= c) S[i + c * LD] -= S[j + i * LD] * S[j + c * LD];
+        }
+        __syncthreads();
+    }
+    // R out (upper, zero strictly-lower)
+    for (int e = tid; e < bs * bs; e += blockDim.x) {
+        const int i = e % bs, j = e / bs;
+        R[(k0 + i) + (k0 + j) * ldr] = i <= j ? S[i + j * LD] : 0.0;
+    }
+    // R^-1 by column back substitution; column c is computed by thread c and
+    // kept transposed in the free strictly-lower part of S: X[i][c] -> S[c][i].
+    if (tid < bs) {
+        const int c = tid;
+        const double xcc = dinv[c];
+        for (int i = c - 1; i >= 0; --i) {
+            double s = S[i + c * LD] * xcc;
+            for (int k = i + 1; k < c; ++k) s += S[i + k * LD] * S[c + k * LD];
+            S[c + i * LD] = -s * dinv[i];
+        }
+        for (int i = 0; i < bs; ++i) {
+            double x;
+            if (i < c)
+                x = S[c + i * LD];
+            else if (i == c)
+                x = xcc;
+            else
+                x = 0.0;
+            Rinv[i + c * ldri] = x;
+        }
+    }
+}
+
+__global__ void diag_copy_kernel(const double* G, int64_t ldg, int64_t p, double shift,
+                                 double* diag, double* Gs, int64_t ldgs) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < p;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        diag[i] = G[i + i * ldg];
+        if (Gs) Gs[i + i * ldgs] += shift;
+    }
+}
+
+// rank-revealing helpers
+__global__ void eig_invsqrt_kernel(const double* w, int64_t p, double tau, double* scale,
+                                   int* rank_out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        int64_t r = 0;
+        while (r < p && w[r] > tau) ++r;
+        *rank_out = static_cast<int>(r);
+    }
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < p;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        scale[i] = w[i] > tau ? 1.0 / sqrt(w[i]) : 0.0;
+}
+
+int read_flag(Ctx* c, int idx) {
+    int f = 0;
+    SVDK_CUDA(cudaMemcpyAsync(&f, c->d_flags + idx, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    SVDK_CUDA(cudaStreamSynchronize(c->stream));
+    return f;
+}
+
+}  // namespace
+
+// Blocked right-looking Cholesky of G (p x p, overwritten) -> R (upper,
+// ldr) and the inverses of its 128 x 128 diagonal blocks (Rinv_blocks,
+// nblk x NB x NB). Returns false on a pivot breakdown.
+bool potrf_upper(Ctx* c, double* G, int64_t ldg, int64_t p, double* R, int64_t ldr,
+                 double* Rinv_blocks, double rel_tol) {
+    static bool attr = false;
+    const size_t smem = static_cast<size_t>(NB) * (NB + 1) * sizeof(double);
+    if (!attr) {
+        SVDK_CUDA(cudaFuncSetAttribute(chol_diag_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem)));
+        attr = true;
+    }
+    DBuf diag(c, p);
+    diag_copy_kernel<<<static_cast<unsigned>(ceil_div(p, 256)), 256, 0, c->stream>>>(
+        G, ldg, p, 0.0, diag.p(), nullptr, 0);
+    SVDK_CHECK_LAUNCH();
+    SVDK_CUDA(cudaMemsetAsync(c->d_flags + 3, 0, sizeof(int), c->stream));
+    c->launches++;
+    for (int64_t j = 0; j < p; ++j)
+        if (ldr == p) {
+            fill(c, R, p * p, 0.0);
+            break;
+        } else {
+            fill(c, R + j * ldr, p, 0.0);
+        }
+    const int64_t nblk = ceil_div(p, NB);
+    for (int64_t kb = 0; kb < nblk; ++kb) {
+        const int64_t k0 = kb * NB;
+        const int bs = static_cast<int>(std::min<int64_t>(NB, p - k0));
+        double* rinv = Rinv_blocks + kb * NB * NB;
+        chol_diag_kernel<<<1, 256, smem, c->stream>>>(G, ldg, k0, bs, R, ldr, rinv, NB, diag.p(),
+                                                      rel_tol, c->d_flags + 3);
+        SVDK_CHECK_LAUNCH();
+        c->launches++;
+        const int64_t k1 = k0 + bs, rest = p - k1;
+        if (rest > 0) {
+            // R[k0:k1, k1:] = R_kk^-T G[k0:k1, k1:]
+            gemm(c, true, bs, rest, bs, rinv, NB, G + k0 + k1 * ldg, ldg, R + k0 + k1 * ldr, ldr);
+            // G[k1:, k1:] -= R[k0:k1, k1:]^T R[k0:k1, k1:]
+            syrk(c, bs, rest, R + k0 + k1 * ldr, ldr, G + k1 + k1 * ldg, ldg, -1.0, true);
+        }
+    }
+    return read_flag(c, 3) == 0;
+}
+
+// Q = H R^-1 for upper R (p x p) with precomputed diagonal-block inverses.
+// W is scratch with H's contents (may alias H when H is disposable).
+void trsm_right_upper(Ctx* c, double* W, int64_t ldw, int64_t m, int64_t p, const double* R,
+                      int64_t ldr, const double* Rinv_blocks, double* Q, int64_t ldq) {
+    const int64_t nblk = ceil_div(p, NB);
+    for (int64_t J = 0; J < nblk; ++J) {
+        const int64_t j0 = J * NB;
+        const int64_t bs = std::min<int64_t>(NB, p - j0);
+        if (j0 > 0)  // W_J -= Q[:, :j0] R[:j0, J]
+            gemm(c, false, m, bs, j0, Q, ldq, R + j0 * ldr, ldr, W + j0 * ldw, ldw, nullptr, false,
+                 -1.0, true);
+        gemm(c, false, m, bs, bs, W + j0 * ldw, ldw, Rinv_blocks + J * NB * NB, NB, Q + j0 * ldq,
+             ldq);
+    }
+}
+
+namespace {
+
+// One CholeskyQR pass: Q = H R^-1 with R from chol(H^T H + shift I).
+// H is overwritten (used as TRSM scratch). Returns false on breakdown.
+bool cholqr_pass(Ctx* c, double* H, int64_t ldh, int64_t m, int64_t p, double* Q, int64_t ldq,
+                 double* R, double shift_rel, double rel_tol, const RowComm* comm) {
+    DBuf G(c, static_cast<size_t>(p) * p), Rinv(c, static_cast<size_t>(ceil_div(p, NB)) * NB * NB);
+    gram_rows(c, H, ldh, m, p, G.p(), p, comm);
+    if (shift_rel > 0.0) {
+        // shift = shift_rel * tr(G), tr(G) = ||H||_F^2 >= ||H||_2^2
+        std::vector<double> d(p);
+        DBuf diag(c, p);
+        diag_copy_kernel<<<static_cast<unsigned>(ceil_div(p, 256)), 256, 0, c->stream>>>(
+            G.p(), p, p, 0.0, diag.p(), nullptr, 0);
+        SVDK_CHECK_LAUNCH();
+        d2h(c, d.data(), diag.p(), p);
+        double tr = 0.0;
+        for (double x : d) tr += x;
+        diag_copy_kernel<<<static_cast<unsigned>(ceil_div(p, 256)), 256, 0, c->stream>>>(
+            G.p(), p, p, shift_rel * tr, diag.p(), G.p(), p);
+        SVDK_CHECK_LAUNCH();
+        c->launches += 2;
+    }
+    if (!potrf_upper(c, G.p(), p, p, R, p, Rinv.p(), rel_tol)) return false;
+    trsm_right_upper(c, H, ldh, m, p, R, p, Rinv.p(), Q, ldq);
+    return true;
+}
+
+}  // namespace
+
+// CholeskyQR2 with fallbacks. Q (m x p, ldq), R (p x p, ld p) or nullptr.
+// Returns the numerical rank. H is not modified.
+int64_t qr_thin(Ctx* c, const double* H, int64_t ldh, int64_t m, int64_t p, double* Q, int64_t ldq,
+                double* R, const RowComm* comm) {
+    if (p == 0) return 0;
+    const int64_t ldw = round_up(std::max<int64_t>(m, 1), 2);
+    DBuf W(c, static_cast<size_t>(ldw) * p), Q1(c, static_cast<size_t>(ldw) * p);
+    DBuf R1(c, static_cast<size_t>(p) * p), R2(c, static_cast<size_t>(p) * p);
+    auto load_w = [&] { copy_mat(c, H, ldh, W.p(), ldw, m, p); };
+
+    const double accept = 1e-12;  // relative pivot floor for a plain CholeskyQR pass
+    bool ok;
+    // --- CholeskyQR2 ---
+    load_w();
+    ok = cholqr_pass(c, W.p(), ldw, m, p, Q1.p(), ldw, R1.p(), 0.0, accept, comm);
+    if (!ok) {
+        // --- shifted CholeskyQR3: first pass on G + s I ---
+        load_w();
+        const double u = 1.1102230246251565e-16;
+        const double mg = static_cast<double>(m) * std::max(1, comm ? comm->world() : 1);
+        const double shift_rel = 11.0 * (mg * p + p * (p + 1.0)) * u;
+        ok = cholqr_pass(c, W.p(), ldw, m, p, Q1.p(), ldw, R1.p(), shift_rel, 0.0, comm);
+        if (ok) {
+            DBuf R0(c, static_cast<size_t>(p) * p);
+            copy_mat(c, R1.p(), p, R0.p(), p, p, p);
+            copy_mat(c, Q1.p(), ldw, W.p(), ldw, m, p);
+            ok = cholqr_pass(c, W.p(), ldw, m, p, Q1.p(), ldw, R1.p(), 0.0, accept, comm);
+            if (ok) {  // R1 <- R1 R0
+                DBuf t(c, static_cast<size_t>(p) * p);
+                gemm(c, false, p, p, p, R1.p(), p, R0.p(), p, t.p(), p);
+                copy_mat(c, t.p(), p, R1.p(), p, p, p);
+            }
+        }
+    }
+    if (ok) {
+        copy_mat(c, Q1.p(), ldw, W.p(), ldw, m, p);
+        ok = cholqr_pass(c, W.p(), ldw, m, p, Q, ldq, R2.p(), 0.0, accept, comm);
+        if (ok) {
+            if (R) gemm(c, false, p, p, p, R2.p(), p, R1.p(), p, R, p);  // R = R2 R1
+            return p;
+        }
+    }
+
+    // --- rank-revealing fallback: orthonormal basis of range(H) via eig(H^T H) ---
+    DBuf G(c, static_cast<size_t>(p) * p), w(c, p), Wv(c, static_cast<size_t>(p) * p),
+        scale(c, p);
+    gram_rows(c, H, ldh, m, p, G.p(), p, comm);
+    eig_sym(c, G.p(), p, p, 30, w.p(), Wv.p(), p);
+    double w0 = 0.0;
+    d2h(c, &w0, w.p(), 1);
+    const double tau = std::max(1e-14 * w0, 0.0);
+    eig_invsqrt_kernel<<<static_cast<unsigned>(ceil_div(p, 256)), 256, 0, c->stream>>>(
+        w.p(), p, tau, scale.p(), c->d_flags + 4);
+    SVDK_CHECK_LAUNCH();
+    c->launches++;
+    const int64_t r = (w0 > 0.0) ? read_flag(c, 4) : 0;
+    if (r > 0) {
+        // Q_r = H W_r Lambda_r^-1/2, then one CholeskyQR2 to clean orthogonality
+        gemm(c, false, m, r, p, H, ldh, Wv.p(), p, W.p(), ldw, scale.p());
+        ok = cholqr_pass(c, W.p(), ldw, m, r, Q1.p(), ldw, R1.p(), 0.0, 0.0, comm);
+        if (ok) {
+            copy_mat(c, Q1.p(), ldw, W.p(), ldw, m, r);
+            ok = cholqr_pass(c, W.p(), ldw, m, r, Q, ldq, R2.p(), 0.0, 0.0, comm);
+        }
+        if (!ok) fail(SVDK_E_NUMERICAL, "qr_thin: rank-revealing fallback failed", 0.0);
+    }
+    if (r < p) {
+        ok = true;
+        // complete with random directions orthogonalised twice against Q_r
+        const int64_t pc = p - r;
+        std::vector<double> hz(static_cast<size_t>(m) * pc);
+        gaussian_fill(m, pc, 0x5eed0f0a11ull + static_cast<uint64_t>(comm ? comm->rank() : 0),
+                      hz.data());
+        DBuf Z(c, static_cast<size_t>(ldw) * pc), T(c, static_cast<size_t>(std::max<int64_t>(r, 1)) * pc);
+        SVDK_CUDA(cudaMemcpy2DAsync(Z.p(), ldw * sizeof(double), hz.data(), m * sizeof(double),
+                                    m * sizeof(double), pc, cudaMemcpyHostToDevice, c->stream));
+        if (r > 0)
+            for (int pass = 0; pass < 2; ++pass) {
+                gemm_tn_rows(c, r, pc, m, Q, ldq, Z.p(), ldw, T.p(), r, comm);
+                gemm(c, false, m, pc, r, Q, ldq, T.p(), r, Z.p(), ldw, nullptr, false, -1.0, true);
+            }
+        for (int pass = 0; pass < 2 && ok; ++pass) {
+            ok = cholqr_pass(c, Z.p(), ldw, m, pc, pass == 0 ? Q1.p() : Q + r * ldq,
+                             pass == 0 ? ldw : ldq, R1.p(), 0.0, 0.0, comm);
+            if (pass == 0 && ok) copy_mat(c, Q1.p(), ldw, Z.p(), ldw, m, pc);
+        }
+        if (!ok) fail(SVDK_E_NUMERICAL, "qr_thin: completion of a rank-deficient basis failed", 0.0);
+    }
+    if (R) gemm_tn_rows(c, p, p, m, Q, ldq, H, ldh, R, p, comm);  // R = Q^T H
+    return r;
+}
+
+}  // namespace svdk

@@ -1,0 +1,512 @@
+// gemm_f64.cu — FP64 tensor-core GEMM / SYRK engine for sm_100a.
+//
+// Replaces the reference's scalar loop nests
+//   gram                    kernels.cpp:80-97   (SYRK, upper tiles, exact mirror)
+//   matmul_transposed_left  kernels.cpp:47-67   (TN, long-K split-K)
+//   matmul                  kernels.cpp:14-45   (NN, + column-scale epilogue and
+//                                                non-finite flag, :39-43)
+//
+// Hardware mapping (B200 / sm_100a):
+//  * FP64 math runs on the DMMA pipe: mma.sync.m8n8k4.f64 lowers to
+//    DMMA.8x8x4 (tcgen05 has no f64 kind). Measured pipe peak 37.0 TFLOP/s
+//    vs 33.8 for DFMA (profiles/fp64_peaks.json).
+//  * Operands stream HBM/L2 -> SMEM by TMA (cp.async.bulk.tensor, 128B
+//    swizzle) into a 6-stage mbarrier ring filled by one producer warp;
+//    eight consumer warps each own a 64x32 slice of the 128x128 CTA tile
+//    (64 FP64 accumulators per thread in registers).
+//  * Persistent grid: one CTA per SM walks (tile, k-split) work units in a
+//    static round-robin, so concurrent CTAs share the same k-range of A in
+//    L2. Split-K partials are reduced in a fixed order (deterministic; no
+//    floating-point atomics), and SYRK writes each mirror pair from one value
+//    so G is exactly symmetric like the reference.
+//
+// Shared-memory fragment layout and bank conflicts: with 128B swizzle a
+// K-major tile holds element (c, k) at byte c*128 + (((k>>1) ^ (c&7))<<4) +
+// (k&1)*8. The m8n8k4 fragment of a lane is (row = lane>>2, k = lane&3); we
+// map MMA row r to tile row perm8(r) = 2*(r&3) + (r>>2) so the four rows a
+// half-warp touches fall in distinct 32B bank groups (conflict-free LDS.64).
+// The M-major tile (NN's A operand) uses the analogous map within 16 rows.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "svdk_internal.h"
+
+namespace svdk {
+namespace {
+
+constexpr int BM = 128, BN = 128, BK = 16;
+constexpr int STAGES = 6;
+constexpr int CWARPS = 8;                        // consumer warps (2 warpgroups)
+constexpr int PWARPS = 4;                        // producer warpgroup (1 thread issues TMA)
+constexpr int THREADS = (CWARPS + PWARPS) * 32;
+constexpr int TILE_BYTES = BM * BK * 8;          // 16 KiB per operand per stage
+constexpr int TILE_ELEMS = BM * BN;              // partial tile size (doubles)
+constexpr int SMEM_BYTES = STAGES * 2 * TILE_BYTES + 1024 + 2 * STAGES * 8;
+
+enum Kind : int { KIND_SYRK = 0, KIND_TN = 1, KIND_NN = 2 };
+
+struct Params {
+    int kind;
+    int a_mmajor;  // A operand is M-contiguous (NN)
+    int64_t M, N, K;
+    int tiles_m, tiles_n, n_tiles;
+    int splits;
+    int64_t k_per_split;
+    int units;
+    double* C;
+    int64_t ldc;
+    double* partial;
+    const double* col_scale;
+    int* flag;
+    double alpha;  // out = alpha * (op(A) B) [+ C_old when beta_one]
+    int beta_one;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    const uint32_t addr = smem_u32(bar);
+    uint32_t ok = 0;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(ok)
+            : "r"(addr), "r"(parity)
+            : "memory");
+    } while (!ok);
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+// MMA row r (0..7) -> row within an 8-row K-major group.
+__host__ __device__ __forceinline__ int perm8(int r) { return ((r & 3) << 1) | (r >> 2); }
+// MMA row r of m-tile parity p -> row within a 16-row M-major group.
+__host__ __device__ __forceinline__ int map16(int p, int r) {
+    return (r & 1) + (((r >> 1) & 1) << 3) + ((r >> 2) << 1) + (p << 2);
+}
+
+struct Unit {
+    int64_t row0, col0, k0, k1;
+    bool diag;
+};
+
+__device__ __forceinline__ Unit decode(const Params& p, int u) {
+    Unit w;
+    const int split = u / p.n_tiles;
+    const int t = u - split * p.n_tiles;
+    int ti, tj;
+    if (p.kind == KIND_SYRK) {
+        // upper-triangular enumeration, column by column: t -> (ti <= tj)
+        tj = static_cast<int>((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
+        while ((tj + 1) * (tj + 2) / 2 <= t) ++tj;
+        while (tj * (tj + 1) / 2 > t) --tj;
+        ti = t - tj * (tj + 1) / 2;
+    } else {
+        ti = t / p.tiles_n;
+        tj = t - ti * p.tiles_n;
+    }
+    w.row0 = static_cast<int64_t>(ti) * BM;
+    w.col0 = static_cast<int64_t>(tj) * BN;
+    w.diag = (p.kind == KIND_SYRK) && (ti == tj);
+    w.k0 = static_cast<int64_t>(split) * p.k_per_split;
+    w.k1 = min(p.K, w.k0 + p.k_per_split);
+    return w;
+}
+
+// (idx, tid) of a thread-linear accumulator slot -> tile-local (row, col).
+__device__ __forceinline__ void slot_coord(int a_mmajor, int idx, int tid, int& r, int& c) {
+    const int warp = tid >> 5, lane = tid & 31;
+    const int wm = warp >> 2, wn = warp & 3;
+    const int t = idx >> 3, tn = (idx >> 1) & 3, i = idx & 1;
+    const int lr = lane >> 2;
+    r = wm * 64 + (a_mmajor ? 16 * (t >> 1) + map16(t & 1, lr) : t * 8 + perm8(lr));
+    c = wn * 32 + tn * 8 + perm8(2 * (lane & 3) + i);
+}
+
+__device__ __forceinline__ void store_out(const Params& p, int64_t row, int64_t col, double v) {
+    if (row >= p.M || col >= p.N) return;
+    if (p.kind == KIND_SYRK) {
+        if (row > col) return;  // one value per mirror pair -> exact symmetry
+        if (p.alpha != 1.0) v *= p.alpha;
+        if (p.beta_one) v += p.C[row + col * p.ldc];
+        p.C[row + col * p.ldc] = v;
+        p.C[col + row * p.ldc] = v;
+        return;
+    }
+    if (p.flag && !isfinite(v)) atomicOr(p.flag, 1);
+    if (p.col_scale) v *= p.col_scale[col];
+    if (p.alpha != 1.0) v *= p.alpha;
+    if (p.beta_one) v += p.C[row + col * p.ldc];
+    p.C[row + col * p.ldc] = v;
+}
+
+template <bool AMM>
+__global__ void __launch_bounds__(THREADS, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                const Params p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+    uint8_t* smA = smem;
+    uint8_t* smB = smem + STAGES * TILE_BYTES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + 2 * STAGES * TILE_BYTES);
+    uint64_t* empty = full + STAGES;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], CWARPS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp >= CWARPS) {
+        // ---------------- TMA producer warpgroup ----------------
+        // Hand registers to the consumers: 1 producer + 2 consumer warps per
+        // SM sub-partition fit 40 + 2 x 232 registers per lane.
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
+        if (warp == CWARPS && lane == 0) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA))
+                         : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB))
+                         : "memory");
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+                const Unit w = decode(p, u);
+                for (int64_t k = w.k0; k < w.k1; k += BK) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_expect_tx(&full[stage], w.diag ? TILE_BYTES : 2 * TILE_BYTES);
+                    uint8_t* da = smA + stage * TILE_BYTES;
+                    if (AMM) {
+#pragma unroll
+                        for (int b = 0; b < BM / 16; ++b)
+                            tma_load_2d(da + b * 2048, &mapA, &full[stage],
+                                        static_cast<int>(w.row0 + 16 * b), static_cast<int>(k));
+                    } else {
+                        tma_load_2d(da, &mapA, &full[stage], static_cast<int>(k),
+                                    static_cast<int>(w.row0));
+                    }
+                    if (!w.diag)
+                        tma_load_2d(smB + stage * TILE_BYTES, &mapB, &full[stage],
+                                    static_cast<int>(k), static_cast<int>(w.col0));
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+        return;
+    }
+
+    // ---------------- consumers ----------------
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
+    const int wm = warp >> 2, wn = warp & 3;
+    const int lr = lane >> 2, kq = lane & 3;
+    const int p8 = perm8(lr);
+    // K-major fragment offsets (bytes) for the 4 k4-steps of a BK=16 stage.
+    uint32_t koff[4];
+#pragma unroll
+    for (int s = 0; s < 4; ++s)
+        koff[s] = p8 * 128 + ((((2 * s + (kq >> 1)) ^ p8)) << 4) + ((kq & 1) << 3);
+    // M-major fragment offsets for the two 8-row halves of a 16-row group.
+    uint32_t moff[2][4];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int mlo = map16(h, lr);
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+            const int k = 4 * s + kq;
+            moff[h][s] = k * 128 + ((((mlo >> 1) ^ (k & 7))) << 4) + ((mlo & 1) << 3);
+        }
+    }
+    const uint32_t a_row_base = AMM ? wm * 4 * 2048 : wm * 64 * 128;
+    const uint32_t b_row_base = wn * 32 * 128;
+
+    double acc[8][4][2];
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+        const Unit w = decode(p, u);
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+#pragma unroll
+            for (int n = 0; n < 4; ++n) acc[t][n][0] = acc[t][n][1] = 0.0;
+
+        for (int64_t k = w.k0; k < w.k1; k += BK) {
+            mbar_wait(&full[stage], phase);
+            const uint8_t* sa = smA + stage * TILE_BYTES + a_row_base;
+            const uint8_t* sb = (w.diag ? smA : smB) + stage * TILE_BYTES + b_row_base;
+#pragma unroll
+            for (int s = 0; s < 4; ++s) {
+                double af[8], bf[4];
+                if (AMM) {
+#pragma unroll
+                    for (int t = 0; t < 8; ++t)
+                        af[t] = *reinterpret_cast<const double*>(sa + (t >> 1) * 2048 +
+                                                                 moff[t & 1][s]);
+                } else {
+#pragma unroll
+                    for (int t = 0; t < 8; ++t)
+                        af[t] = *reinterpret_cast<const double*>(sa + t * 1024 + koff[s]);
+                }
+#pragma unroll
+                for (int n = 0; n < 4; ++n)
+                    bf[n] = *reinterpret_cast<const double*>(sb + n * 1024 + koff[s]);
+#pragma unroll
+                for (int t = 0; t < 8; ++t)
+#pragma unroll
+                    for (int n = 0; n < 4; ++n) dmma(acc[t][n][0], acc[t][n][1], af[t], bf[n]);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stage]);
+            if (++stage == STAGES) {
+                stage = 0;
+                phase ^= 1;
+            }
+        }
+
+        // ---------------- epilogue ----------------
+        const int tid = threadIdx.x;
+        if (p.splits > 1) {
+            double* dst = p.partial + static_cast<size_t>(u) * TILE_ELEMS;
+#pragma unroll
+            for (int t = 0; t < 8; ++t)
+#pragma unroll
+                for (int n = 0; n < 4; ++n)
+#pragma unroll
+                    for (int i = 0; i < 2; ++i)
+                        dst[((t * 4 + n) * 2 + i) * (CWARPS * 32) + tid] = acc[t][n][i];
+        } else {
+#pragma unroll
+            for (int t = 0; t < 8; ++t)
+#pragma unroll
+                for (int n = 0; n < 4; ++n)
+#pragma unroll
+                    for (int i = 0; i < 2; ++i) {
+                        int r, c;
+                        slot_coord(AMM, (t * 4 + n) * 2 + i, tid, r, c);
+                        store_out(p, w.row0 + r, w.col0 + c, acc[t][n][i]);
+                    }
+        }
+    }
+}
+
+// Fixed-order split-K reduction: out = sum_{s=0}^{S-1} partial[s][tile].
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(const Params p) {
+    const int t = blockIdx.x;
+    const int tid = threadIdx.x;
+    Params q = p;
+    // Recover the tile origin from any unit of this tile (split 0).
+    const Unit w = decode(q, t);
+    for (int idx = blockIdx.y * 8; idx < blockIdx.y * 8 + 8; ++idx) {
+        double s = 0.0;
+        const double* src = p.partial + static_cast<size_t>(t) * TILE_ELEMS + idx * 256 + tid;
+        for (int sp = 0; sp < p.splits; ++sp)
+            s += src[static_cast<size_t>(sp) * p.n_tiles * TILE_ELEMS];
+        int r, c;
+        slot_coord(p.a_mmajor, idx, tid, r, c);
+        store_out(p, w.row0 + r, w.col0 + c, s);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        SVDK_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q));
+        if (!ptr || q != cudaDriverEntryPointSuccess)
+            fail(SVDK_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+    }
+    return fn;
+}
+
+// 2-D FP64 map over a column-major matrix: dim0 = rows (contiguous), dim1 = cols.
+CUtensorMap make_map(const double* base, int64_t rows, int64_t cols, int64_t ld, uint32_t box0,
+                     uint32_t box1) {
+    CUtensorMap m;
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(cols)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 8};
+    cuuint32_t box[2] = {box0, box1};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base),
+                             dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(SVDK_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+    return m;
+}
+
+// Pick the k-split count S so (tiles x S) fills whole waves of the SMs.
+int choose_splits(int n_tiles, int64_t K, int sms) {
+    const int64_t k_steps = ceil_div(K, BK);
+    const int max_s = static_cast<int>(std::min<int64_t>(std::max<int64_t>(1, k_steps / 8), 256));
+    double best_eff = 0;
+    int best = 1;
+    for (int s = 1; s <= max_s; ++s) {
+        const int64_t units = static_cast<int64_t>(n_tiles) * s;
+        const double eff = static_cast<double>(units) / (ceil_div(units, sms) * sms);
+        if (eff > best_eff + 0.02) {
+            best_eff = eff;
+            best = s;
+        }
+        if (best_eff > 0.97) break;
+    }
+    return best;
+}
+
+bool tma_ok(const void* p, int64_t ld) {
+    return (reinterpret_cast<uintptr_t>(p) % 16 == 0) && (ld % 2 == 0);
+}
+
+void launch(Ctx* c, Params& p, const CUtensorMap& ma, const CUtensorMap& mb) {
+    static bool attr_set = false;
+    if (!attr_set) {
+        SVDK_CUDA(cudaFuncSetAttribute(gemm_kernel<false>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+        SVDK_CUDA(cudaFuncSetAttribute(gemm_kernel<true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+        attr_set = true;
+    }
+    DBuf partial;
+    if (p.splits > 1) {
+        partial = DBuf(c, static_cast<size_t>(p.units) * TILE_ELEMS);
+        p.partial = partial.p();
+    }
+    const int grid = std::min(p.units, c->num_sms);
+    if (p.a_mmajor)
+        gemm_kernel<true><<<grid, THREADS, SMEM_BYTES, c->stream>>>(ma, mb, p);
+    else
+        gemm_kernel<false><<<grid, THREADS, SMEM_BYTES, c->stream>>>(ma, mb, p);
+    SVDK_CHECK_LAUNCH();
+    c->launches++;
+    if (p.splits > 1) {
+        splitk_reduce_kernel<<<dim3(p.n_tiles, 8), 256, 0, c->stream>>>(p);
+        SVDK_CHECK_LAUNCH();
+        c->launches++;
+    }
+}
+
+}  // namespace
+
+void syrk(Ctx* c, int64_t m, int64_t n, const double* A, int64_t lda, double* G, int64_t ldg,
+          double alpha, bool beta_one) {
+    if (n == 0) return;
+    if (m == 0) {
+        if (!beta_one)
+            for (int64_t j = 0; j < n; ++j) fill(c, G + j * ldg, n, 0.0);
+        return;
+    }
+    DBuf padded;
+    if (!tma_ok(A, lda)) {
+        const int64_t ld2 = round_up(m, 2);
+        padded = DBuf(c, static_cast<size_t>(ld2) * n);
+        copy_mat(c, A, lda, padded.p(), ld2, m, n);
+        A = padded.p();
+        lda = ld2;
+    }
+    Params p{};
+    p.kind = KIND_SYRK;
+    p.a_mmajor = 0;
+    p.M = n;
+    p.N = n;
+    p.K = m;
+    p.tiles_m = p.tiles_n = static_cast<int>(ceil_div(n, BM));
+    p.n_tiles = p.tiles_m * (p.tiles_m + 1) / 2;
+    int s = choose_splits(p.n_tiles, m, c->num_sms);
+    p.k_per_split = round_up(ceil_div(m, s), BK);
+    p.splits = static_cast<int>(ceil_div(m, p.k_per_split));
+    p.units = p.n_tiles * p.splits;
+    p.C = G;
+    p.ldc = ldg;
+    p.alpha = alpha;
+    p.beta_one = beta_one ? 1 : 0;
+    const CUtensorMap ma = make_map(A, m, n, lda, BK, BM);
+    launch(c, p, ma, ma);
+}
+
+void gemm(Ctx* c, bool transa, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda,
+          const double* B, int64_t ldb, double* C, int64_t ldc, const double* col_scale,
+          bool nonfinite_check, double alpha, bool beta_one) {
+    if (m == 0 || n == 0) return;
+    if (k == 0) {
+        if (!beta_one)
+            for (int64_t j = 0; j < n; ++j) fill(c, C + j * ldc, m, 0.0);
+        return;
+    }
+    DBuf pa, pb;
+    if (!tma_ok(A, lda)) {
+        const int64_t rows = transa ? k : m, cols = transa ? m : k;
+        const int64_t ld2 = round_up(rows, 2);
+        pa = DBuf(c, static_cast<size_t>(ld2) * cols);
+        copy_mat(c, A, lda, pa.p(), ld2, rows, cols);
+        A = pa.p();
+        lda = ld2;
+    }
+    if (!tma_ok(B, ldb)) {
+        const int64_t ld2 = round_up(k, 2);
+        pb = DBuf(c, static_cast<size_t>(ld2) * n);
+        copy_mat(c, B, ldb, pb.p(), ld2, k, n);
+        B = pb.p();
+        ldb = ld2;
+    }
+    Params p{};
+    p.kind = transa ? KIND_TN : KIND_NN;
+    p.a_mmajor = transa ? 0 : 1;
+    p.M = m;
+    p.N = n;
+    p.K = k;
+    p.tiles_m = static_cast<int>(ceil_div(m, BM));
+    p.tiles_n = static_cast<int>(ceil_div(n, BN));
+    p.n_tiles = p.tiles_m * p.tiles_n;
+    int s = 1;
+    if (p.n_tiles < 2 * c->num_sms) s = choose_splits(p.n_tiles, k, c->num_sms);
+    p.k_per_split = round_up(ceil_div(k, s), BK);
+    p.splits = static_cast<int>(ceil_div(k, p.k_per_split));
+    p.units = p.n_tiles * p.splits;
+    p.C = C;
+    p.ldc = ldc;
+    p.col_scale = col_scale;
+    p.alpha = alpha;
+    p.beta_one = beta_one ? 1 : 0;
+    if (nonfinite_check) p.flag = c->d_flags;  // sticky; see raise_if_nonfinite()
+    const CUtensorMap ma = transa ? make_map(A, k, m, lda, BK, BM) : make_map(A, m, k, lda, 16, BK);
+    const CUtensorMap mb = make_map(B, k, n, ldb, BK, BN);
+    launch(c, p, ma, mb);
+}
+
+}  // namespace svdk

@@ -1,0 +1,592 @@
+// jacobi.cu — parallel block-cyclic Jacobi eigensolver for symmetric n x n.
+//
+// Replaces eig_sym (reference kernels.cpp:241-346) and keeps its contract:
+//   * square input, else DimensionError                        (:247-249)
+//   * max|s - s^T| <= 1e-8 max|s|, else ParamError              (:251-262)
+//   * iterate on (s + s^T)/2                                     (:264-269)
+//   * converged when off(A) = sqrt(2 sum_{i>j} a_ij^2) <= 1e-12 ||A||_F,
+//     tested before the first sweep and after every sweep         (:271-274, :319)
+//   * rotation formulas tau, t, c, s of the reference             (:282-290)
+//   * sweep cap (default 30) -> NumericalError(off(A))            (:321-326)
+//   * eigenvalues = final diagonal, STABLE descending sort        (:328-331)
+//
+// Parallel ordering instead of cyclic-by-row: the n indices are cut into nb
+// blocks of b; a sweep is nb-1 rounds of a round-robin tournament over the
+// blocks, and in each round the nb/2 disjoint block pairs (I, J) are
+// processed at once:
+//   1. jacobi_pair_solve: one CTA per pair diagonalises the 2b x 2b
+//      subproblem A[IJ, IJ] in shared memory with the reference rotations
+//      (itself in parallel round-robin order, b rotations at a time), and
+//      emits the accumulated rotation Q_p (2b x 2b).
+//   2. jacobi_update: every off-diagonal pair block becomes
+//      A[IJ_p, IJ_q] <- Q_p^T A[IJ_p, IJ_q] Q_q (written with its mirror, so A
+//      stays exactly symmetric) and V[:, IJ_q] <- V[:, IJ_q] Q_q, as small
+//      FP64 DMMA GEMMs out of shared memory.
+// A sweep therefore applies every rotation of a cyclic sweep's pair set, in
+// block form, with ~8 n^3 flops on the DMMA pipe. Padding indices (n rounded
+// up to a multiple of 2b) carry zero rows/columns, never couple, and are
+// dropped at the end.
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+
+#include "svdk_internal.h"
+
+namespace svdk {
+namespace {
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+// Round-robin (circle method) pairing of P players, round r, pair i.
+__host__ __device__ __forceinline__ void circle_pair(int P, int r, int i, int& a, int& b) {
+    const int m = P - 1;
+    a = (i == 0) ? 0 : ((i - 1 + r) % m) + 1;
+    b = ((P - 2 - i + r) % m) + 1;
+    if (a > b) {
+        const int t = a;
+        a = b;
+        b = t;
+    }
+}
+
+// Global index of local index i (0..2b-1) of the pair (I, J).
+__device__ __forceinline__ int64_t gidx(int B, int I, int J, int i) {
+    return i < B ? static_cast<int64_t>(I) * B + i : static_cast<int64_t>(J) * B + (i - B);
+}
+
+// C = op(A) * B on TB x TB shared-memory matrices (col-major, ld TB+4) with
+// FP64 DMMA; result is written to C (same layout). No block barrier inside.
+template <int TB, bool TRANS_A>
+__device__ __forceinline__ void smem_mma(const double* A, const double* Bm, double* C) {
+    constexpr int LD = TB + 4;
+    constexpr int NT = TB / 8;
+    constexpr int WTM = NT >= 8 ? 2 : 1;
+    constexpr int WTN = NT >= 8 ? 4 : (NT >= 4 ? 2 : 1);
+    constexpr int WARPS_M = NT / WTM, WARPS_N = NT / WTN;
+    static_assert(WARPS_M * WARPS_N <= 8, "tile split");
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp >= WARPS_M * WARPS_N) return;
+    const int wm = warp % WARPS_M, wn = warp / WARPS_M;
+    const int r = lane >> 2, kq = lane & 3;
+    double acc[WTM][WTN][2];
+#pragma unroll
+    for (int a = 0; a < WTM; ++a)
+#pragma unroll
+        for (int b = 0; b < WTN; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+#pragma unroll 4
+    for (int k0 = 0; k0 < TB; k0 += 4) {
+        const int k = k0 + kq;
+        double af[WTM], bf[WTN];
+#pragma unroll
+        for (int a = 0; a < WTM; ++a) {
+            const int m = (wm * WTM + a) * 8 + r;
+            af[a] = TRANS_A ? A[k + m * LD] : A[m + k * LD];
+        }
+#pragma unroll
+        for (int b = 0; b < WTN; ++b) {
+            const int nn = (wn * WTN + b) * 8 + r;
+            bf[b] = Bm[k + nn * LD];
+        }
+#pragma unroll
+        for (int a = 0; a < WTM; ++a)
+#pragma unroll
+            for (int b = 0; b < WTN; ++b) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+    }
+#pragma unroll
+    for (int a = 0; a < WTM; ++a)
+#pragma unroll
+        for (int b = 0; b < WTN; ++b) {
+            const int row = (wm * WTM + a) * 8 + r;
+            const int col = (wn * WTN + b) * 8 + 2 * kq;
+            C[row + col * LD] = acc[a][b][0];
+            C[row + (col + 1) * LD] = acc[a][b][1];
+        }
+}
+
+// ---------------------------------------------------------------------------
+// 1. per-pair subproblem solve
+// ---------------------------------------------------------------------------
+// One CTA diagonalises M = A[IJ, IJ] (TB x TB) in shared memory and emits the
+// accumulated rotation Q. Each inner round applies TB/2 disjoint rotations
+// (round-robin pairs) as ONE fused phase: every 2x2 block (rows {p_i,q_i}) x
+// (cols {p_j,q_j}) is replaced by R_i^T B R_j, so a round costs one barrier
+// after the rotation parameters and one after the update. Inner sweeps stop
+// when no |m_pq| exceeds skip_tau. A pair whose subproblem is already
+// diagonal to skip_tau is flagged inactive (Q = I) and its blocks skipped.
+// M itself is scratch: the update kernel applies the (re-orthogonalised) Q to
+// every pair block, the diagonal ones included, so A changes by one
+// similarity per round.
+template <int TB>
+__global__ void __launch_bounds__(256)
+    jacobi_pair_solve(double* A, int64_t lda, double* Qbuf, int* active, int nb, int round,
+                      double skip_tau, int max_inner) {
+    constexpr int B = TB / 2, LD = TB + 4, NP = TB / 2;
+    extern __shared__ double sm[];
+    double* M = sm;
+    double* Q = sm + TB * LD;
+    double* T = Q + TB * LD;
+    __shared__ double cs[NP], sn[NP];
+    __shared__ int pp_s[NP], qq_s[NP], on_s[NP];
+    __shared__ int any_applied;
+
+    const int tid = threadIdx.x;
+    int I, J;
+    circle_pair(nb, round, blockIdx.x, I, J);
+    if (tid == 0) any_applied = 0;
+    __syncthreads();
+    for (int e = tid; e < TB * TB; e += blockDim.x) {
+        const int i = e % TB, j = e / TB;
+        const double x = A[gidx(B, I, J, i) + gidx(B, I, J, j) * lda];
+        M[i + j * LD] = x;
+        Q[i + j * LD] = (i == j) ? 1.0 : 0.0;
+        if (i != j && fabs(x) > skip_tau) any_applied = 1;
+    }
+    __syncthreads();
+    const bool work = any_applied != 0;
+    if (work) {
+        for (int sweep = 0; sweep < max_inner; ++sweep) {
+            __syncthreads();
+            if (tid == 0) any_applied = 0;
+            for (int rr = 0; rr < TB - 1; ++rr) {
+                if (tid < NP) {
+                    int p, q;
+                    circle_pair(TB, rr, tid, p, q);
+                    const double apq = M[p + q * LD];
+                    double c = 1.0, s = 0.0;
+                    int on = 0;
+                    if (fabs(apq) > skip_tau) {
+                        // reference kernels.cpp:282-290
+                        const double tau = (M[q + q * LD] - M[p + p * LD]) / (2.0 * apq);
+                        double t;
+                        if (tau >= 0.0)
+                            t = 1.0 / (tau + sqrt(1.0 + tau * tau));
+                        else
+                            t = -1.0 / (-tau + sqrt(1.0 + tau * tau));
+                        c = 1.0 / sqrt(1.0 + t * t);
+                        s = t * c;
+                        on = 1;
+                        any_applied = 1;
+                    }
+                    pp_s[tid] = p;
+                    qq_s[tid] = q;
+                    cs[tid] = c;
+                    sn[tid] = s;
+                    on_s[tid] = on;
+                }
+                __syncthreads();
+                // fused 2x2-block update  M <- R^T M R
+                for (int e = tid; e < NP * NP; e += blockDim.x) {
+                    const int bi = e % NP, bj = e / NP;
+                    const int oi = on_s[bi], oj = on_s[bj];
+                    if (!(oi | oj)) continue;
+                    const int pi = pp_s[bi], qi = qq_s[bi], pj = pp_s[bj], qj = qq_s[bj];
+                    double m00 = M[pi + pj * LD], m01 = M[pi + qj * LD];
+                    double m10 = M[qi + pj * LD], m11 = M[qi + qj * LD];
+                    if (oj) {  // columns pj, qj
+                        const double c = cs[bj], s = sn[bj];
+                        const double a0 = c * m00 - s * m01, b0 = s * m00 + c * m01;
+                        const double a1 = c * m10 - s * m11, b1 = s * m10 + c * m11;
+                        m00 = a0; m01 = b0; m10 = a1; m11 = b1;
+                    }
+                    if (oi) {  // rows pi, qi
+                        const double c = cs[bi], s = sn[bi];
+                        const double a0 = c * m00 - s * m10, b0 = s * m00 + c * m10;
+                        const double a1 = c * m01 - s * m11, b1 = s * m01 + c * m11;
+                        m00 = a0; m10 = b0; m01 = a1; m11 = b1;
+                    }
+                    if (bi == bj && oi) {  // the rotated pair is annihilated exactly
+                        m01 = 0.0;
+                        m10 = 0.0;
+                    }
+                    M[pi + pj * LD] = m00;
+                    M[pi + qj * LD] = m01;
+                    M[qi + pj * LD] = m10;
+                    M[qi + qj * LD] = m11;
+                }
+                for (int e = tid; e < TB * NP; e += blockDim.x) {
+                    const int r = e % TB, j = e / TB;
+                    if (!on_s[j]) continue;
+                    const int p = pp_s[j], q = qq_s[j];
+                    const double c = cs[j], s = sn[j];
+                    const double x = Q[r + p * LD], y = Q[r + q * LD];
+                    Q[r + p * LD] = c * x - s * y;
+                    Q[r + q * LD] = s * x + c * y;
+                }
+                __syncthreads();
+            }
+            if (!any_applied) break;
+        }
+        // The product of ~TB * sweeps rotations drifts from orthogonality by a
+        // few hundred ulps; one Newton-Schulz step Q <- Q (3I - Q^T Q) / 2
+        // restores it to working precision so that A' = Q^T A Q is a
+        // similarity to rounding (otherwise the spectrum drifts over sweeps).
+        __syncthreads();
+        smem_mma<TB, true>(Q, Q, M);  // M <- Q^T Q
+        __syncthreads();
+        for (int e = tid; e < TB * TB; e += blockDim.x) {
+            const int i = e % TB, j = e / TB;
+            M[i + j * LD] = (i == j ? 1.5 : 0.0) - 0.5 * M[i + j * LD];
+        }
+        __syncthreads();
+        smem_mma<TB, false>(Q, M, T);  // T <- Q (3I - Q^T Q) / 2
+        __syncthreads();
+        for (int e = tid; e < TB * TB; e += blockDim.x)
+            Qbuf[static_cast<size_t>(blockIdx.x) * TB * TB + e] = T[(e % TB) + (e / TB) * LD];
+    }
+    if (tid == 0) active[blockIdx.x] = work ? 1 : 0;
+}
+
+// ---------------------------------------------------------------------------
+// 2. off-diagonal pair blocks of A and the columns of V
+// ---------------------------------------------------------------------------
+template <int TB>
+__global__ void __launch_bounds__(256)
+    jacobi_update(double* A, int64_t lda, double* V, int64_t ldv, const double* Qbuf,
+                  const int* active, int nb, int round, int64_t n_pad) {
+    constexpr int B = TB / 2, LD = TB + 4;
+    extern __shared__ double sm[];
+    double* X = sm;
+    double* Qa = X + TB * LD;
+    double* Qb = Qa + TB * LD;
+    double* T = Qb + TB * LD;
+    const int tid = threadIdx.x;
+    const int k = nb / 2;
+    const int n_off = k * (k + 1) / 2;
+    int u = blockIdx.x;
+    if (u < n_off) {
+        // (p <= q) from u, column-wise upper enumeration
+        int q = static_cast<int>((sqrt(8.0 * u + 1.0) - 1.0) * 0.5);
+        while ((q + 1) * (q + 2) / 2 <= u) ++q;
+        while (q * (q + 1) / 2 > u) --q;
+        const int p = u - q * (q + 1) / 2;
+        const int ap = active[p], aq = active[q];
+        if (!(ap | aq)) return;  // both rotations are the identity
+        int Ip, Jp, Iq, Jq;
+        circle_pair(nb, round, p, Ip, Jp);
+        circle_pair(nb, round, q, Iq, Jq);
+        const double* qa = Qbuf + static_cast<size_t>(p) * TB * TB;
+        const double* qb = Qbuf + static_cast<size_t>(q) * TB * TB;
+        for (int e = tid; e < TB * TB; e += blockDim.x) {
+            const int i = e % TB, j = e / TB;
+            X[i + j * LD] = A[gidx(B, Ip, Jp, i) + gidx(B, Iq, Jq, j) * lda];
+            Qa[i + j * LD] = ap ? qa[e] : (i == j ? 1.0 : 0.0);
+            Qb[i + j * LD] = aq ? qb[e] : (i == j ? 1.0 : 0.0);
+        }
+        __syncthreads();
+        if (aq) {
+            smem_mma<TB, false>(X, Qb, T);  // T = X Q_q
+        } else {
+            for (int e = tid; e < TB * TB; e += blockDim.x) T[(e % TB) + (e / TB) * LD] = X[(e % TB) + (e / TB) * LD];
+        }
+        __syncthreads();
+        if (ap) {
+            smem_mma<TB, true>(Qa, T, X);  // X = Q_p^T T
+        } else {
+            for (int e = tid; e < TB * TB; e += blockDim.x) X[(e % TB) + (e / TB) * LD] = T[(e % TB) + (e / TB) * LD];
+        }
+        __syncthreads();
+        if (p == q) {  // diagonal pair block: write the exactly symmetric part
+            for (int e = tid; e < TB * TB; e += blockDim.x) {
+                const int i = e % TB, j = e / TB;
+                A[gidx(B, Ip, Jp, i) + gidx(B, Ip, Jp, j) * lda] =
+                    0.5 * (X[i + j * LD] + X[j + i * LD]);
+            }
+            return;
+        }
+        for (int e = tid; e < TB * TB; e += blockDim.x) {
+            const int i = e % TB, j = e / TB;
+            A[gidx(B, Ip, Jp, i) + gidx(B, Iq, Jq, j) * lda] = X[i + j * LD];
+        }
+        for (int e = tid; e < TB * TB; e += blockDim.x) {
+            const int j = e % TB, i = e / TB;  // consecutive threads walk rows of the mirror
+            A[gidx(B, Iq, Jq, j) + gidx(B, Ip, Jp, i) * lda] = X[i + j * LD];
+        }
+    } else {
+        u -= n_off;
+        const int q = u % k;
+        if (!active[q]) return;
+        const int64_t r0 = static_cast<int64_t>(u / k) * TB;
+        int Iq, Jq;
+        circle_pair(nb, round, q, Iq, Jq);
+        const double* qb = Qbuf + static_cast<size_t>(q) * TB * TB;
+        for (int e = tid; e < TB * TB; e += blockDim.x) {
+            const int i = e % TB, j = e / TB;
+            X[i + j * LD] = V[r0 + i + gidx(B, Iq, Jq, j) * ldv];
+            Qb[i + j * LD] = qb[e];
+        }
+        __syncthreads();
+        smem_mma<TB, false>(X, Qb, T);
+        __syncthreads();
+        for (int e = tid; e < TB * TB; e += blockDim.x) {
+            const int i = e % TB, j = e / TB;
+            V[r0 + i + gidx(B, Iq, Jq, j) * ldv] = T[i + j * LD];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// setup / checks / finish
+// ---------------------------------------------------------------------------
+// max|s_ij| and max|s_ij - s_ji| (block partials; max is order-independent)
+__global__ void symcheck_kernel(const double* S, int64_t lds, int64_t n, double* partial) {
+    __shared__ double r1[32], r2[32];
+    double mabs = 0.0, masym = 0.0;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n * n;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t j = e / n, i = e - j * n;
+        const double a = S[i + j * lds];
+        mabs = fmax(mabs, fabs(a));
+        masym = fmax(masym, fabs(a - S[j + i * lds]));
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        mabs = fmax(mabs, __shfl_xor_sync(0xffffffffu, mabs, o));
+        masym = fmax(masym, __shfl_xor_sync(0xffffffffu, masym, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        r1[threadIdx.x >> 5] = mabs;
+        r2[threadIdx.x >> 5] = masym;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (blockDim.x >> 5); ++w) {
+            mabs = fmax(mabs, r1[w]);
+            masym = fmax(masym, r2[w]);
+        }
+        partial[2 * blockIdx.x] = mabs;
+        partial[2 * blockIdx.x + 1] = masym;
+    }
+}
+
+// A (n_pad x n_pad) = (S + S^T)/2 zero padded; V = I.
+__global__ void jacobi_init_kernel(const double* S, int64_t lds, int64_t n, double* A, double* V,
+                                   int64_t n_pad) {
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n_pad * n_pad;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t j = e / n_pad, i = e - j * n_pad;
+        double a = 0.0;
+        if (i < n && j < n) a = 0.5 * (S[i + j * lds] + S[j + i * lds]);
+        A[e] = a;
+        V[e] = (i == j) ? 1.0 : 0.0;
+    }
+}
+
+// partial sums of squares: mode 0 = all entries, mode 1 = strictly lower.
+__global__ void jacobi_sumsq_kernel(const double* A, int64_t n, int mode, double* partial) {
+    __shared__ double red[32];
+    double s = 0.0;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n * n;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t j = e / n, i = e - j * n;
+        if (mode == 0 || i > j) s = fma(A[e], A[e], s);
+    }
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (blockDim.x >> 5); ++w) s += red[w];
+        partial[blockIdx.x] = s;
+    }
+}
+
+__global__ void sum_fixed_kernel(const double* partial, int count, double* out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double s = 0.0;
+        for (int i = 0; i < count; ++i) s += partial[i];
+        *out = s;
+    }
+}
+
+// Stable descending order by rank counting: rank_i = #{j : l_j > l_i or
+// (l_j == l_i and j < i)} — exactly std::stable_sort's permutation.
+__global__ void eig_sort_kernel(const double* A, int64_t n_pad, int64_t n, double* w, int* dest) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    const double li = A[i + i * n_pad];
+    int64_t rank = 0;
+    for (int64_t j = 0; j < n; ++j) {
+        const double lj = A[j + j * n_pad];
+        rank += (lj > li) || (lj == li && j < i);
+    }
+    w[rank] = li;
+    dest[i] = static_cast<int>(rank);
+}
+
+__global__ void eig_gather_kernel(const double* V, int64_t n_pad, int64_t n, const int* dest,
+                                  double* Vout, int64_t ldv) {
+    for (int64_t j = blockIdx.y; j < n; j += gridDim.y) {
+        const int64_t d = dest[j];
+        for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+             i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+            Vout[i + d * ldv] = V[i + j * n_pad];
+    }
+}
+
+double device_sumsq(Ctx* c, const double* A, int64_t n, int mode, DBuf& scratch) {
+    const int blocks = static_cast<int>(
+        std::max<int64_t>(1, std::min<int64_t>(ceil_div(n * n, 256), 2 * c->num_sms)));
+    jacobi_sumsq_kernel<<<blocks, 256, 0, c->stream>>>(A, n, mode, scratch.p());
+    SVDK_CHECK_LAUNCH();
+    sum_fixed_kernel<<<1, 32, 0, c->stream>>>(scratch.p(), blocks, scratch.p() + blocks);
+    SVDK_CHECK_LAUNCH();
+    c->launches += 2;
+    double out = 0.0;
+    d2h(c, &out, scratch.p() + blocks, 1);
+    return out;
+}
+
+template <int TB>
+void run_sweeps(Ctx* c, double* A, double* V, double* Qbuf, int* active, int64_t n_pad,
+                int max_sweeps, double thr, double fro, DBuf& scratch, int& sweeps, double& off) {
+    constexpr int B = TB / 2;
+    const int nb = static_cast<int>(n_pad / B);
+    const int k = nb / 2;
+    const size_t smem_solve = 3 * TB * (TB + 4) * sizeof(double);
+    const size_t smem_upd = 4 * TB * (TB + 4) * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+        SVDK_CUDA(cudaFuncSetAttribute(jacobi_pair_solve<TB>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem_solve)));
+        SVDK_CUDA(cudaFuncSetAttribute(jacobi_update<TB>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem_upd)));
+        attr = true;
+    }
+    // Inner skip threshold: if every off-diagonal entry were this small the
+    // outer test off <= 1e-12 ||A||_F would hold with a 10x margin.
+    const double skip_tau = 1e-13 * fro / static_cast<double>(n_pad);
+    const char* inner_env = std::getenv("SVDK_JACOBI_INNER");
+    const int max_inner = inner_env ? std::max(1, std::atoi(inner_env)) : 1;
+    const int update_ctas = k * (k + 1) / 2 + static_cast<int>(n_pad / TB) * k;
+    auto enqueue_sweep = [&] {
+        for (int r = 0; r < nb - 1; ++r) {
+            jacobi_pair_solve<TB><<<k, 256, smem_solve, c->stream>>>(A, n_pad, Qbuf, active, nb, r,
+                                                                     skip_tau, max_inner);
+            jacobi_update<TB><<<update_ctas, 256, smem_upd, c->stream>>>(A, n_pad, V, n_pad, Qbuf,
+                                                                         active, nb, r, n_pad);
+        }
+    };
+    // One sweep = 2 (nb - 1) dependent launches: capture them once as a CUDA
+    // graph and replay it per sweep (launch latency dominates at small n).
+    cudaGraphExec_t exec = nullptr;
+    const bool use_graph = nb > 2 && c->stream != nullptr;
+    if (use_graph) {
+        cudaGraph_t graph;
+        SVDK_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        enqueue_sweep();
+        SVDK_CUDA(cudaStreamEndCapture(c->stream, &graph));
+        SVDK_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+        cudaGraphDestroy(graph);
+    }
+    sweeps = 0;
+    try {
+        while (off > thr && sweeps < max_sweeps) {
+            if (use_graph) {
+                SVDK_CUDA(cudaGraphLaunch(exec, c->stream));
+            } else {
+                enqueue_sweep();
+                SVDK_CHECK_LAUNCH();
+            }
+            c->launches += 2 * (nb - 1);
+            ++sweeps;
+            off = std::sqrt(2.0 * device_sumsq(c, A, n_pad, 1, scratch));
+        }
+    } catch (...) {
+        if (exec) cudaGraphExecDestroy(exec);
+        throw;
+    }
+    if (exec) cudaGraphExecDestroy(exec);
+}
+
+}  // namespace
+
+void eig_sym(Ctx* c, const double* S, int64_t lds, int64_t n, int max_sweeps, double* w,
+             double* Vout, int64_t ldv) {
+    if (max_sweeps <= 0) max_sweeps = 30;
+    if (n == 0) return;
+    // symmetry check (kernels.cpp:251-262)
+    {
+        const int blocks = static_cast<int>(
+            std::max<int64_t>(1, std::min<int64_t>(ceil_div(n * n, 256), 2 * c->num_sms)));
+        DBuf part(c, 2 * blocks);
+        symcheck_kernel<<<blocks, 256, 0, c->stream>>>(S, lds, n, part.p());
+        SVDK_CHECK_LAUNCH();
+        c->launches++;
+        std::vector<double> h(2 * blocks);
+        d2h(c, h.data(), part.p(), 2 * blocks);
+        double mabs = 0.0, masym = 0.0;
+        for (int b = 0; b < blocks; ++b) {
+            mabs = std::max(mabs, h[2 * b]);
+            masym = std::max(masym, h[2 * b + 1]);
+        }
+        if (masym > 1e-8 * mabs) {
+            char buf[96];
+            std::snprintf(buf, sizeof buf, "%f", masym);
+            fail(SVDK_E_PARAM,
+                 std::string("eig_sym: input asymmetric beyond tolerance, max|s-s^T| = ") + buf);
+        }
+    }
+    // Block size: measured on B200 (tools/eig_sweep.sh): 2b = 32 with ONE
+    // inner sweep per round is fastest for n in [256, 2048]; the outer sweep
+    // count (9-12) does not depend on how far each subproblem is pushed.
+    int TB = n <= 64 ? 16 : 32;
+    if (const char* e = std::getenv("SVDK_JACOBI_TB")) {  // tuning override
+        const int t = std::atoi(e);
+        if (t == 16 || t == 32 || t == 64) TB = t;
+    }
+    const int64_t n_pad = round_up(n, TB);
+    DBuf A(c, static_cast<size_t>(n_pad) * n_pad), V(c, static_cast<size_t>(n_pad) * n_pad);
+    const int64_t k = n_pad / TB;  // pairs per round (nb = 2k blocks of TB/2)
+    DBuf Qbuf(c, static_cast<size_t>(k) * TB * TB), active(c, k);
+    DBuf scratch(c, 4 * c->num_sms + 8);
+    {
+        const int blocks = static_cast<int>(
+            std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_pad * n_pad, 256), 4 * c->num_sms)));
+        jacobi_init_kernel<<<blocks, 256, 0, c->stream>>>(S, lds, n, A.p(), V.p(), n_pad);
+        SVDK_CHECK_LAUNCH();
+        c->launches++;
+    }
+    const double fro = std::sqrt(device_sumsq(c, A.p(), n_pad, 0, scratch));
+    const double thr = 1e-12 * fro;  // kernels.cpp:271
+    double off = std::sqrt(2.0 * device_sumsq(c, A.p(), n_pad, 1, scratch));
+    int sweeps = 0;
+    if (n == 1) off = 0.0;
+    switch (TB) {
+        case 16:
+            run_sweeps<16>(c, A.p(), V.p(), Qbuf.p(), reinterpret_cast<int*>(active.p()), n_pad,
+                            max_sweeps, thr, fro, scratch, sweeps, off);
+            break;
+        case 32:
+            run_sweeps<32>(c, A.p(), V.p(), Qbuf.p(), reinterpret_cast<int*>(active.p()), n_pad,
+                            max_sweeps, thr, fro, scratch, sweeps, off);
+            break;
+        default:
+            run_sweeps<64>(c, A.p(), V.p(), Qbuf.p(), reinterpret_cast<int*>(active.p()), n_pad,
+                            max_sweeps, thr, fro, scratch, sweeps, off);
+            break;
+    }
+    c->jacobi_sweeps = sweeps;
+    c->last_off_norm = off;
+    if (off > thr) {
+        char buf[160];
+        std::snprintf(buf, sizeof buf, "eig_sym: no convergence in %d sweeps, off-diagonal norm %f",
+                      max_sweeps, off);
+        fail(SVDK_E_NUMERICAL, buf, off);
+    }
+    DBuf dest(c, n);  // int storage inside a double buffer
+    eig_sort_kernel<<<static_cast<unsigned>(ceil_div(n, 128)), 128, 0, c->stream>>>(
+        A.p(), n_pad, n, w, reinterpret_cast<int*>(dest.p()));
+    SVDK_CHECK_LAUNCH();
+    dim3 g(static_cast<unsigned>(std::min<int64_t>(ceil_div(n, 128), 64)),
+           static_cast<unsigned>(std::min<int64_t>(n, 65535)));
+    eig_gather_kernel<<<g, 128, 0, c->stream>>>(V.p(), n_pad, n,
+                                                reinterpret_cast<const int*>(dest.p()), Vout, ldv);
+    SVDK_CHECK_LAUNCH();
+    c->launches += 2;
+}
+
+}  // namespace svdk

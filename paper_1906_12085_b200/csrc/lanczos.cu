@@ -1,0 +1,291 @@
+// lanczos.cu — Lanczos on A^T A with full reorthogonalisation (NEW method:
+// the reference has block Krylov only, svd_methods.cpp:172-196, and lists
+// Lanczos as a non-goal; BASELINE configs c3/c5 ask for it). Parity oracle:
+// the reference truncated_svd (Gram + Jacobi) on the same A.
+//
+//   q_0 = g / ||g||, g = gaussian_matrix(n, 1, seed)  (reference sampler)
+//   for j < steps:
+//     w   = A^T (A q_j)           fused one-pass GEMV pair  [+ allreduce n]
+//     a_j = q_j^T w ; w -= a_j q_j + b_{j-1} q_{j-1}
+//     w  -= Q_j (Q_j^T w)  twice  (CGS2 full reorthogonalisation)
+//     b_j = ||w|| ; q_{j+1} = w / b_j   (random restart on breakdown)
+//   T = tridiag(a, b) -> Jacobi eig_sym -> Ritz V = Q_L S -> sigma, U = A V / sigma
+//
+// The GEMV pair is HBM-bound (4mn flop over 8mn bytes): each CTA streams its
+// share of 32-row slabs of A once from HBM; the slab's second use (A^T y)
+// hits L2. Per-CTA column partials are reduced in fixed order.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "svdk_methods.h"
+
+namespace svdk {
+void gaussian_fill(int64_t rows, int64_t cols, uint64_t seed, double* out);
+int64_t back_project(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n, const double* w,
+                     const double* Vfull, int64_t ldvf, int64_t kcols, double* U, int64_t ldu,
+                     double* sigma, double* V, int64_t ldv);
+
+namespace {
+
+constexpr int GV_WARPS = 16;
+constexpr int GV_THREADS = GV_WARPS * 32;
+
+// partial[b][j] = sum over this CTA's 32-row slabs of A_slab^T (A_slab q)
+__global__ void __launch_bounds__(GV_THREADS)
+    gemv_pair_kernel(const double* __restrict__ A, int64_t lda, int64_t m, int64_t n,
+                     const double* __restrict__ q, double* __restrict__ partial) {
+    extern __shared__ double sm[];
+    double* qs = sm;                 // n
+    double* wacc = sm + n;           // n
+    double* ypart = wacc + n;        // GV_WARPS x 32
+    __shared__ double y[32];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    for (int64_t j = tid; j < n; j += GV_THREADS) {
+        qs[j] = q[j];
+        wacc[j] = 0.0;
+    }
+    __syncthreads();
+    const int64_t nslabs = (m + 31) / 32;
+    for (int64_t s = blockIdx.x; s < nslabs; s += gridDim.x) {
+        const int64_t row = s * 32 + lane;
+        const bool in = row < m;
+        const double* a = A + (in ? row : 0);
+        // phase 1: y = A_slab q  (warp w takes columns w, w+16, ...)
+        double acc0 = 0.0, acc1 = 0.0;
+        int64_t j = warp;
+        for (; j + GV_WARPS < n; j += 2 * GV_WARPS) {
+            const double x0 = in ? __ldg(a + j * lda) : 0.0;
+            const double x1 = in ? __ldg(a + (j + GV_WARPS) * lda) : 0.0;
+            acc0 = fma(x0, qs[j], acc0);
+            acc1 = fma(x1, qs[j + GV_WARPS], acc1);
+        }
+        if (j < n) acc0 = fma(in ? __ldg(a + j * lda) : 0.0, qs[j], acc0);
+        ypart[warp * 32 + lane] = acc0 + acc1;
+        __syncthreads();
+        if (warp == 0) {
+            double t = 0.0;
+#pragma unroll
+            for (int w = 0; w < GV_WARPS; ++w) t += ypart[w * 32 + lane];
+            y[lane] = t;
+        }
+        __syncthreads();
+        // phase 2: wacc += A_slab^T y  (column dot over the 32 lanes)
+        const double yl = y[lane];
+        for (int64_t jj = warp; jj < n; jj += GV_WARPS) {
+            double v = (in ? a[jj * lda] : 0.0) * yl;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0) wacc[jj] += v;
+        }
+        // ypart/y are rewritten next slab only after the first barrier above
+    }
+    __syncthreads();
+    for (int64_t j = tid; j < n; j += GV_THREADS) partial[blockIdx.x * n + j] = wacc[j];
+}
+
+__global__ void reduce_parts_kernel(const double* partial, int parts, int64_t n, double* w) {
+    const int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (j >= n) return;
+    double s = 0.0;
+    for (int b = 0; b < parts; ++b) s += partial[b * n + j];
+    w[j] = s;
+}
+
+__device__ double block_sum(double v, double* red) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    double t = 0.0;
+    for (int i = 0; i < (blockDim.x >> 5); ++i) t += red[i];
+    return t;
+}
+
+// a_j = q^T w ; w -= a_j q + b_prev q_prev   (single CTA)
+__global__ void alpha_kernel(double* w, const double* q, const double* qprev, int64_t n,
+                             const double* beta_prev, double* alpha_out) {
+    __shared__ double red[32];
+    double s = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s = fma(q[i], w[i], s);
+    const double a = block_sum(s, red);
+    const double b = beta_prev ? *beta_prev : 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        double x = w[i] - a * q[i];
+        if (qprev) x -= b * qprev[i];
+        w[i] = x;
+    }
+    if (threadIdx.x == 0) *alpha_out = a;
+}
+
+// h_k = Q[:, k]^T w for k < cols (one warp per column)
+__global__ void cgs_dot_kernel(const double* Q, int64_t ldq, int64_t n, int64_t cols,
+                               const double* w, double* h) {
+    const int64_t k = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (k >= cols) return;
+    const double* qk = Q + k * ldq;
+    double s = 0.0;
+    for (int64_t i = lane; i < n; i += 32) s = fma(qk[i], w[i], s);
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) h[k] = s;
+}
+
+// w_i -= sum_k Q[i,k] h_k (thread per row, coalesced over i)
+__global__ void cgs_update_kernel(const double* Q, int64_t ldq, int64_t n, int64_t cols,
+                                  const double* h, double* w) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    double s0 = 0.0, s1 = 0.0;
+    int64_t k = 0;
+    for (; k + 1 < cols; k += 2) {
+        s0 = fma(Q[i + k * ldq], h[k], s0);
+        s1 = fma(Q[i + (k + 1) * ldq], h[k + 1], s1);
+    }
+    if (k < cols) s0 = fma(Q[i + k * ldq], h[k], s0);
+    w[i] -= s0 + s1;
+}
+
+__global__ void norm_kernel(const double* w, int64_t n, double* out) {
+    __shared__ double red[32];
+    double s = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s = fma(w[i], w[i], s);
+    const double t = block_sum(s, red);
+    if (threadIdx.x == 0) *out = sqrt(t);
+}
+
+__global__ void scale_kernel(const double* w, int64_t n, const double* nrm, double* out) {
+    const double inv = 1.0 / *nrm;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        out[i] = w[i] * inv;
+}
+
+// Dense tridiagonal T (k x k) from alpha, beta.
+__global__ void tridiag_kernel(const double* alpha, const double* beta, int64_t k, double* T) {
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < k * k;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t j = e / k, i = e - j * k;
+        double v = 0.0;
+        if (i == j)
+            v = alpha[i];
+        else if (i == j + 1)
+            v = beta[j];
+        else if (j == i + 1)
+            v = beta[i];
+        T[e] = v;
+    }
+}
+
+}  // namespace
+
+int64_t lanczos_svd(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n, int64_t steps,
+                    uint64_t seed, double* U, int64_t ldu, double* sigma, double* V, int64_t ldv,
+                    const RowComm* comm) {
+    if (steps <= 0 || steps > n) steps = n;
+    const int parts = c->num_sms;
+    const size_t gv_smem = (2 * n + GV_WARPS * 32) * sizeof(double);
+    if (gv_smem > 200 * 1024) fail(SVDK_E_PARAM, "lanczos_svd: n too large for the fused GEMV");
+    SVDK_CUDA(cudaFuncSetAttribute(gemv_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(gv_smem)));
+    DBuf Q(c, static_cast<size_t>(n) * (steps + 1)), w(c, n), partial(c, static_cast<size_t>(parts) * n),
+        h(c, steps + 1), scal(c, 2 * steps + 8);
+    double* alpha = scal.p();
+    double* beta = scal.p() + steps;
+    double* nrm = scal.p() + 2 * steps;  // [0] after pass 1, [1] after pass 2
+    // q_0 from the reference sampler
+    {
+        std::vector<double> g(n);
+        gaussian_fill(n, 1, seed, g.data());
+        double s = 0.0;
+        for (double x : g) s += x * x;
+        const double inv = 1.0 / std::sqrt(s);
+        for (double& x : g) x *= inv;
+        h2d(c, Q.p(), g.data(), n);
+    }
+    double gnorm = 0.0;  // running Gershgorin bound on ||T||
+    std::vector<double> hb(2);
+    double prev_beta = 0.0;
+    for (int64_t j = 0; j < steps; ++j) {
+        const double* qj = Q.p() + j * n;
+        gemv_pair_kernel<<<parts, GV_THREADS, gv_smem, c->stream>>>(A, lda, m, n, qj, partial.p());
+        SVDK_CHECK_LAUNCH();
+        reduce_parts_kernel<<<static_cast<unsigned>(ceil_div(n, 256)), 256, 0, c->stream>>>(
+            partial.p(), parts, n, w.p());
+        SVDK_CHECK_LAUNCH();
+        if (comm) comm->allreduce(w.p(), static_cast<size_t>(n));
+        alpha_kernel<<<1, 1024, 0, c->stream>>>(w.p(), qj, j > 0 ? Q.p() + (j - 1) * n : nullptr, n,
+                                                j > 0 ? beta + (j - 1) : nullptr, alpha + j);
+        SVDK_CHECK_LAUNCH();
+        const int64_t cols = j + 1;
+        for (int pass = 0; pass < 2; ++pass) {
+            cgs_dot_kernel<<<static_cast<unsigned>(ceil_div(cols * 32, 256)), 256, 0, c->stream>>>(
+                Q.p(), n, n, cols, w.p(), h.p());
+            SVDK_CHECK_LAUNCH();
+            cgs_update_kernel<<<static_cast<unsigned>(ceil_div(n, 256)), 256, 0, c->stream>>>(
+                Q.p(), n, n, cols, h.p(), w.p());
+            SVDK_CHECK_LAUNCH();
+            norm_kernel<<<1, 1024, 0, c->stream>>>(w.p(), n, nrm + pass);
+            SVDK_CHECK_LAUNCH();
+        }
+        c->launches += 9;
+        double ab[3];
+        SVDK_CUDA(cudaMemcpyAsync(hb.data(), nrm, 2 * sizeof(double), cudaMemcpyDeviceToHost,
+                                  c->stream));
+        SVDK_CUDA(cudaMemcpyAsync(ab, alpha + j, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        SVDK_CUDA(cudaStreamSynchronize(c->stream));
+        const double n1 = hb[0], n2 = hb[1];
+        gnorm = std::max(gnorm, std::fabs(ab[0]) + prev_beta + n2);
+        if (j + 1 == steps) {
+            SVDK_CUDA(cudaMemcpyAsync(beta + j, nrm + 1, sizeof(double), cudaMemcpyDeviceToDevice,
+                                      c->stream));
+            break;
+        }
+        double* qn = Q.p() + (j + 1) * n;
+        const bool breakdown = !(n2 > 0.5 * n1) || !(n2 > 1e-14 * gnorm);
+        if (!breakdown) {
+            SVDK_CUDA(cudaMemcpyAsync(beta + j, nrm + 1, sizeof(double), cudaMemcpyDeviceToDevice,
+                                      c->stream));
+            scale_kernel<<<static_cast<unsigned>(ceil_div(n, 256)), 256, 0, c->stream>>>(
+                w.p(), n, nrm + 1, qn);
+            SVDK_CHECK_LAUNCH();
+            c->launches++;
+            prev_beta = n2;
+        } else {
+            // invariant subspace found: b_j = 0, restart with a random vector
+            // orthogonalised (twice) against Q_j (replicated on every rank)
+            const double zero = 0.0;
+            h2d(c, beta + j, &zero, 1);
+            std::vector<double> g(n);
+            gaussian_fill(n, 1, seed ^ (0x9e3779b97f4a7c15ull * static_cast<uint64_t>(j + 1)),
+                          g.data());
+            h2d(c, w.p(), g.data(), n);
+            for (int pass = 0; pass < 2; ++pass) {
+                cgs_dot_kernel<<<static_cast<unsigned>(ceil_div(cols * 32, 256)), 256, 0,
+                                 c->stream>>>(Q.p(), n, n, cols, w.p(), h.p());
+                cgs_update_kernel<<<static_cast<unsigned>(ceil_div(n, 256)), 256, 0, c->stream>>>(
+                    Q.p(), n, n, cols, h.p(), w.p());
+            }
+            norm_kernel<<<1, 1024, 0, c->stream>>>(w.p(), n, nrm);
+            scale_kernel<<<static_cast<unsigned>(ceil_div(n, 256)), 256, 0, c->stream>>>(
+                w.p(), n, nrm, qn);
+            SVDK_CHECK_LAUNCH();
+            c->launches += 6;
+            prev_beta = 0.0;
+        }
+    }
+    // Ritz pairs: eig(T), V = Q_L S
+    DBuf T(c, static_cast<size_t>(steps) * steps), theta(c, steps), S(c, static_cast<size_t>(steps) * steps);
+    tridiag_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(steps * steps, 256), 1024)), 256,
+                     0, c->stream>>>(alpha, beta, steps, T.p());
+    SVDK_CHECK_LAUNCH();
+    c->launches++;
+    eig_sym(c, T.p(), steps, steps, 30, theta.p(), S.p(), steps);
+    DBuf Vr(c, static_cast<size_t>(n) * steps);
+    gemm(c, false, n, steps, steps, Q.p(), n, S.p(), steps, Vr.p(), n);
+    Q.reset();
+    return back_project(c, A, lda, m, n, theta.p(), Vr.p(), n, steps, U, ldu, sigma, V, ldv);
+}
+
+}  // namespace svdk

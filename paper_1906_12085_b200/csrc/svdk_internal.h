@@ -1,0 +1,159 @@
+// svdk_internal.h — engine-internal context, status plumbing and device pool.
+//
+// Everything here is private to libsvdk.so; the public surface is
+// include/svdk.h (C-ABI). Status codes map one-to-one onto the reference
+// exception taxonomy (reference errors.hpp:11-55), see include/svdk.h.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "svdk.h"
+
+namespace svdk {
+
+// ---------------------------------------------------------------------------
+// Status plumbing: C++ exceptions inside the engine, int codes at the C-ABI.
+// ---------------------------------------------------------------------------
+struct Failure {
+    int code;
+    std::string msg;
+    double residual = 0.0;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg, double residual = 0.0);
+
+#define SVDK_CUDA(call)                                                                   \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess)                                                            \
+            ::svdk::fail(SVDK_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+#define SVDK_CHECK_LAUNCH() SVDK_CUDA(cudaGetLastError())
+
+// ---------------------------------------------------------------------------
+// Device memory pool: stream-ordered reuse on the context's single stream.
+// ---------------------------------------------------------------------------
+class Pool {
+public:
+    ~Pool();
+    void* get(size_t bytes);
+    void put(void* p);
+    void trim();
+    size_t reserved() const { return reserved_; }
+
+private:
+    struct Block {
+        void* p;
+        size_t bytes;
+        bool busy;
+    };
+    std::vector<Block> blocks_;
+    size_t reserved_ = 0;
+};
+
+struct Ctx;
+
+// RAII device buffer of doubles from the context pool.
+class DBuf {
+public:
+    DBuf() = default;
+    DBuf(Ctx* c, size_t count);
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    DBuf(DBuf&& o) noexcept { *this = std::move(o); }
+    DBuf& operator=(DBuf&& o) noexcept;
+    ~DBuf();
+    double* p() const { return p_; }
+    size_t count() const { return n_; }
+    void reset();
+
+private:
+    Ctx* c_ = nullptr;
+    double* p_ = nullptr;
+    size_t n_ = 0;
+};
+
+// Column-major device matrix view (ld >= rows).
+struct DMat {
+    double* p = nullptr;
+    int64_t rows = 0, cols = 0, ld = 0;
+    double* col(int64_t j) const { return p + j * ld; }
+};
+
+struct Ctx {
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    Pool pool;
+    // scratch: small pinned host buffer for scalars / flags
+    void* host_scratch = nullptr;
+    int* d_flags = nullptr;  // [0] non-finite flag, [1] jacobi status, ...
+    double* d_scalars = nullptr;
+    // multi-GPU (row-sharded) state
+    void* nccl_comm = nullptr;
+    int rank = 0, world = 1;
+    // counters for bench/introspection
+    int64_t launches = 0;
+    int jacobi_sweeps = 0;
+    double last_off_norm = 0.0;
+};
+
+inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+inline int64_t ceil_div(int64_t x, int64_t m) { return (x + m - 1) / m; }
+
+// ---------------------------------------------------------------------------
+// Engine entry points shared across translation units (device pointers,
+// everything ordered on ctx->stream).
+// ---------------------------------------------------------------------------
+
+// C = op(A) * B  with op(A) = A (NN: A m x k) or A^T (TN: A k x m).
+// B is k x n (K-major). Optional per-column scale of the output (epilogue).
+// If nonfinite_check, raises SVDK_E_NUMERICAL on a non-finite output entry
+// (reference kernels.cpp:39-43).
+// Epilogue: C = alpha * (op(A) B) (+ C_old when beta_one).
+void gemm(Ctx* c, bool transa, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda,
+          const double* B, int64_t ldb, double* C, int64_t ldc, const double* col_scale = nullptr,
+          bool nonfinite_check = false, double alpha = 1.0, bool beta_one = false);
+// G = alpha A^T A (+ G_old) (n x n, exactly symmetric), A m x n.
+void syrk(Ctx* c, int64_t m, int64_t n, const double* A, int64_t lda, double* G, int64_t ldg,
+          double alpha = 1.0, bool beta_one = false);
+
+// Small helpers (linalg_small.cu)
+void fill(Ctx* c, double* p, int64_t count, double v);
+void copy_mat(Ctx* c, const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows,
+              int64_t cols);
+void transpose(Ctx* c, const double* src, int64_t lds, int64_t rows, int64_t cols, double* dst,
+               int64_t ldd);
+// Sum of squares of an m x n block, deterministic fixed-order reduction.
+double frob_sq(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n);
+// Column means (RowsAreExamples) + subtract in place into dst; returns mean on device.
+void center_rows_are_examples(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n,
+                              double* dst, int64_t ldd, double* d_mean);
+// Column sums / denom (denom = 1 gives plain sums), fixed-order reduction.
+void column_sums(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n, double denom,
+                 double* d_out);
+void subtract_column_means(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n,
+                           const double* d_mean, double* dst, int64_t ldd);
+void center_cols_are_examples(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n,
+                              double* dst, int64_t ldd, double* d_mean);
+
+// Symmetric eigensolver (jacobi.cu): S n x n (device), returns eigenvalues
+// descending in w and eigenvectors in V (ldv). Contract of reference
+// kernels.cpp:241-346 (symmetry check, threshold, sweep cap, stable sort).
+void eig_sym(Ctx* c, const double* S, int64_t lds, int64_t n, int max_sweeps, double* w,
+             double* V, int64_t ldv);
+
+// Host <-> device
+void h2d(Ctx* c, double* dst, const double* src, int64_t count);
+void d2h(Ctx* c, double* dst, const double* src, int64_t count);
+void sync(Ctx* c);
+
+}  // namespace svdk

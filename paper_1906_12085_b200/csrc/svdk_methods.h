@@ -1,0 +1,55 @@
+// svdk_methods.h — engine-internal method entry points (device operands).
+#pragma once
+
+#include <functional>
+
+#include "svdk_internal.h"
+
+namespace svdk {
+
+// Row-sharded execution: A is split by rows over `world` GPUs (one process
+// each). Every reduction over the row index (Gram, A^T Y, column sums,
+// norms) is followed by an NCCL allreduce over NVLink; the n x n eigensolve
+// runs on rank 0 and its result is broadcast. nullptr = single GPU.
+struct RowComm {
+    Ctx* c;
+    void allreduce(double* buf, size_t count) const;
+    void broadcast(double* buf, size_t count, int root) const;
+    int rank() const;
+    int world() const;
+};
+
+// Sum-reduce over rows helpers honouring an optional RowComm.
+void gram_rows(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n, double* G, int64_t ldg,
+               const RowComm* comm);
+void gemm_tn_rows(Ctx* c, int64_t n, int64_t l, int64_t m, const double* A, int64_t lda,
+                  const double* B, int64_t ldb, double* C, int64_t ldc, const RowComm* comm);
+double frob_sq_rows(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n,
+                    const RowComm* comm);
+// eig_sym on rank 0 (or the only GPU) + broadcast of w and V.
+void eig_sym_rows(Ctx* c, const double* S, int64_t lds, int64_t n, double* w, double* V,
+                  int64_t ldv, const RowComm* comm);
+
+void nccl_unique_id(char out[128]);
+void attach_nccl(Ctx* c, const char id[128], int rank, int world);
+void destroy_comm(Ctx* c);
+
+void raise_if_nonfinite(Ctx* c);
+void reset_nonfinite(Ctx* c);
+// sigma from eigenvalues + numerical rank (svd_methods.cpp:127-135)
+int64_t spectrum(Ctx* c, const double* w, int64_t n, double* sigma);
+// normalize_signs on already-formed U, V (svd_methods.cpp:50-71)
+void normalize_signs_uv(Ctx* c, double* U, int64_t ldu, int64_t m, double* V, int64_t ldv,
+                        int64_t n, int64_t rank);
+
+int64_t truncated_svd(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n, double* U,
+                      int64_t ldu, double* sigma, double* V, int64_t ldv,
+                      const RowComm* comm = nullptr);
+
+// Full PCA pipeline on a device-resident (local shard of) A; see svdk.h.
+void dev_pca(Ctx* c, const double* A, int64_t m_local, int64_t n, int64_t lda, int method,
+             int64_t l, int64_t q, uint64_t seed, bool center, double threshold, double* U,
+             int64_t ldu, double* sigma, double* V, int64_t ldv, double* mean, int64_t* rank,
+             int64_t* k, double* total);
+
+}  // namespace svdk

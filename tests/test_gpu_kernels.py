@@ -1,0 +1,165 @@
+"""GPU parity of the L1 kernels (DMMA GEMM/SYRK, Jacobi, CholeskyQR2) through the C-ABI."""
+import numpy as np
+import pytest
+
+from paper_1906_12085_b200 import errors
+
+pytestmark = pytest.mark.gpu
+
+
+def rel_gemm_err(c, ref, a_norms, b_norms):
+    return float(np.max(np.abs(c - ref) / (np.outer(a_norms, b_norms) + 1e-300)))
+
+
+@pytest.mark.parametrize("m,n", [(1, 1), (2, 2), (5, 3), (129, 17), (1000, 130), (4099, 257), (20000, 256)])
+def test_gram_vs_numpy(sk, m, n):
+    rng = np.random.default_rng(m + n)
+    a = np.asfortranarray(rng.standard_normal((m, n)))
+    g = sk.gram(a)
+    ref = a.T @ a
+    cn = np.linalg.norm(a, axis=0)
+    assert rel_gemm_err(g, ref, cn, cn) < 1e-14
+    assert np.array_equal(g, g.T), "gram must be exactly symmetric (kernels.cpp:92-93)"
+
+
+def test_gram_vs_reference(sk, ref):
+    a = np.asfortranarray(np.random.default_rng(3).standard_normal((3000, 200)))
+    g, gr = sk.gram(a), ref.gram(a)
+    cn = np.linalg.norm(a, axis=0)
+    assert rel_gemm_err(g, gr, cn, cn) < 1e-14
+
+
+@pytest.mark.parametrize("m,k,n", [(2, 2, 2), (7, 3, 5), (300, 129, 130), (5001, 64, 200), (130, 1000, 131)])
+def test_matmul_vs_numpy(sk, m, k, n):
+    rng = np.random.default_rng(m * k + n)
+    a = np.asfortranarray(rng.standard_normal((m, k)))
+    b = np.asfortranarray(rng.standard_normal((k, n)))
+    c = sk.matmul(a, b)
+    assert rel_gemm_err(c, a @ b, np.linalg.norm(a, axis=1), np.linalg.norm(b, axis=0)) < 1e-14
+
+
+@pytest.mark.parametrize("m,n,l", [(3, 2, 2), (1000, 130, 7), (20001, 256, 256), (4096, 1024, 96)])
+def test_matmul_tl_vs_numpy(sk, m, n, l):
+    rng = np.random.default_rng(m + n * l)
+    a = np.asfortranarray(rng.standard_normal((m, n)))
+    b = np.asfortranarray(rng.standard_normal((m, l)))
+    c = sk.matmul_transposed_left(a, b)
+    assert rel_gemm_err(c, a.T @ b, np.linalg.norm(a, axis=0), np.linalg.norm(b, axis=0)) < 1e-14
+
+
+def test_matmul_kat_and_nonfinite(sk):
+    assert sk.matmul([[1, 2], [3, 4]], [[5, 6], [7, 8]]).tolist() == [[19, 22], [43, 50]]
+    with pytest.raises(errors.NumericalError):
+        sk.matmul([[1e200, 1e200]], [[1e200], [1e200]])
+
+
+def test_transpose_and_frob(sk):
+    a = np.asfortranarray(np.random.default_rng(9).standard_normal((37, 29)))
+    assert np.array_equal(sk.transpose(a), a.T)
+    assert abs(sk.frobenius_norm_sq(a) - (a ** 2).sum()) <= 1e-13 * (a ** 2).sum()
+    assert sk.frobenius_norm_sq(np.eye(3)) == 3.0
+
+
+def test_eig_kats(sk):
+    e = sk.eig_sym([[2.0, 1], [1, 2]])
+    assert np.allclose(e.eigenvalues, [3, 1], rtol=0, atol=1e-15)
+    v = e.eigenvectors
+    assert np.allclose(np.abs(v), np.sqrt(0.5), atol=1e-15)
+    e = sk.eig_sym(np.eye(4))
+    assert e.eigenvalues.tolist() == [1, 1, 1, 1] and np.array_equal(e.eigenvectors, np.eye(4))
+    e = sk.eig_sym(np.diag([1.0, 3.0]))
+    assert e.eigenvalues.tolist() == [3, 1] and np.array_equal(np.abs(e.eigenvectors), [[0, 1], [1, 0]])
+
+
+@pytest.mark.parametrize("n", [3, 17, 64, 100, 256, 513, 1024])
+def test_eig_random_symmetric(sk, n):
+    rng = np.random.default_rng(n)
+    x = rng.standard_normal((n, n))
+    s = np.asfortranarray(x + x.T)
+    e = sk.eig_sym(s)
+    w, v = e.eigenvalues, e.eigenvectors
+    fro = np.linalg.norm(s)
+    assert np.all(np.diff(w) <= 0)
+    assert np.max(np.abs(w - np.linalg.eigvalsh(s)[::-1])) <= 1e-13 * fro
+    assert np.linalg.norm(s @ v - v * w) <= 1e-10 * fro  # SPEC: 1e-8
+    assert np.max(np.abs(v.T @ v - np.eye(n))) <= 1e-12
+    assert abs(w.sum() - np.trace(s)) <= 1e-10 * fro
+
+
+def test_eig_matches_reference_gram(sk, ref):
+    a = np.asfortranarray(np.random.default_rng(4).standard_normal((500, 48)))
+    g = ref.gram(a)
+    e = sk.eig_sym(g)
+    w_ref, v_ref = ref.eig_sym(g)
+    assert np.max(np.abs(e.eigenvalues - w_ref) / w_ref) < 1e-12
+    from tests.parity import per_vector_sines
+    single, cluster = per_vector_sines(e.eigenvectors, w_ref, v_ref)
+    assert single < 1e-10 and cluster < 1e-10
+
+
+def test_eig_errors(sk):
+    with pytest.raises(errors.DimensionError):
+        sk.eig_sym(np.ones((2, 3)))
+    with pytest.raises(errors.ParamError):
+        sk.eig_sym([[1.0, 0.5], [0.0, 1.0]])
+    x = np.random.default_rng(1).standard_normal((200, 200))
+    with pytest.raises(errors.NumericalError) as e:
+        sk.eig_sym(x + x.T, max_sweeps=1)
+    assert e.value.residual() > 0
+
+
+@pytest.mark.parametrize("m,p", [(1, 1), (2, 1), (3, 2), (500, 37), (5000, 256), (20000, 300)])
+def test_qr_thin(sk, m, p):
+    h = np.asfortranarray(np.random.default_rng(m + p).standard_normal((m, p)))
+    r = sk.qr_thin(h)
+    assert r.rank == p
+    assert np.max(np.abs(r.q.T @ r.q - np.eye(p))) <= 1e-13
+    assert np.linalg.norm(r.q @ r.r - h) <= 1e-13 * np.linalg.norm(h)
+    assert np.allclose(np.tril(r.r, -1), 0) and np.all(np.diag(r.r) >= 0)
+
+
+def test_qr_kats(sk):
+    r = sk.qr_thin([[3.0], [4.0]])
+    assert np.allclose(r.q[:, 0], [0.6, 0.8], atol=1e-15) and abs(r.r[0, 0] - 5) < 1e-14
+    r = sk.qr_thin([[1.0, 0], [1, 1], [0, 1]])
+    assert np.allclose(r.q[:, 1], [-0.40824829046386296, 0.40824829046386302, 0.81649658092772603], atol=1e-15)
+
+
+def test_qr_rank_deficient(sk):
+    rng = np.random.default_rng(11)
+    b = rng.standard_normal((400, 5))
+    h = np.asfortranarray(np.hstack([b, b[:, :2] @ rng.standard_normal((2, 3)), np.zeros((400, 1))]))
+    r = sk.qr_thin(h)
+    assert r.rank == 5
+    assert np.max(np.abs(r.q.T @ r.q - np.eye(9))) <= 1e-12
+    assert np.linalg.norm(r.q @ r.r - h) <= 1e-12 * np.linalg.norm(h)
+    z = sk.qr_thin(np.zeros((10, 3)))
+    assert z.rank == 0 and np.max(np.abs(z.q.T @ z.q - np.eye(3))) <= 1e-12
+
+
+def test_qr_ill_conditioned(sk):
+    rng = np.random.default_rng(12)
+    u, _ = np.linalg.qr(rng.standard_normal((3000, 60)))
+    v, _ = np.linalg.qr(rng.standard_normal((60, 60)))
+    h = np.asfortranarray((u * np.logspace(0, -10, 60)) @ v.T)  # kappa 1e10: beyond CholeskyQR2
+    r = sk.qr_thin(h)
+    assert np.max(np.abs(r.q.T @ r.q - np.eye(60))) <= 1e-11
+    assert np.linalg.norm(r.q @ r.r - h) <= 1e-12 * np.linalg.norm(h)
+
+
+def test_select_components_device(sk):
+    assert sk.select_components([4, 3, 2, 1], 10, 0.7) == 2
+    assert sk.select_components([4, 3, 2, 1], 10, 0.0) == 1
+    assert sk.select_components([4, 3, 2, 1], 11, 1.0) is None
+    for bad in (([4, 3], 10, 1.5), ([4, 3], 0.0, 0.5), ([3, 4], 10, 0.5), ([], 10, 0.5), ([1, -1], 10, 0.5)):
+        with pytest.raises(errors.ParamError):
+            sk.select_components(*bad)
+
+
+def test_center_matches_reference(sk, ref):
+    a = np.asfortranarray(np.random.default_rng(2).standard_normal((301, 17)) + 3.0)
+    for o in (0, 1):
+        c = sk.center(a, o)
+        cr, mr = ref.center(a, o)
+        assert np.max(np.abs(c.mean - mr)) <= 1e-14 * (np.abs(mr).max() + 1)
+        assert np.max(np.abs(c.centered - cr)) <= 1e-13

@@ -1,0 +1,25 @@
+"""Run one eig_sym(n) on the GPU (for ncu launch lists / timing)."""
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+from paper_1906_12085_b200.engine import Engine, colmajor  # noqa: E402
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+eng = Engine(0)
+torch.cuda.set_stream(eng.stream)
+g = torch.Generator(device="cuda").manual_seed(1)
+x = torch.randn(n, n, dtype=torch.float64, device="cuda", generator=g)
+s = colmajor(n, n, ld=n)
+s.copy_(x + x.t())
+for _ in range(reps):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    w, v = eng.eig_sym(s)
+    e1.record()
+    torch.cuda.synchronize()
+    print(f"eig n={n}: {e0.elapsed_time(e1):.2f} ms, sweeps={eng.ctx.last_sweeps()}", flush=True)
+ref = torch.linalg.eigvalsh(s.contiguous()).flip(0)
+print("max |dw| / ||S||_F =", float((w - ref).abs().max() / torch.linalg.norm(s)))
