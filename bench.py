@@ -1,0 +1,459 @@
+#!/usr/bin/env python
+"""bench.py — PCA throughput of the B200 FP64 engine on BASELINE.json's configs.
+
+Default workload (N=1): config c2 — randomized PCA of a 200000 x 1024 FP64
+matrix (l = min(k + p, n) = 1024, q = 2 power iterations, CholeskyQR2,
+t = 0.99), i.e. BASELINE.json configs[1]. A "step" is one full fit_pca +
+select_components pass (center -> total variance -> range finder -> small
+SVD -> U back-projection -> K) over the device-resident matrix.
+
+  python bench.py [--gpus N --steps K --warmup W] [--config c1..c5] [--impl reference]
+
+Multi-GPU (torchrun, one process per GPU): each rank holds its own m-row
+shard (weak scaling); every reduction over rows is an NCCL allreduce inside
+the engine. Timing: CUDA events on the engine's stream, barrier +
+synchronize on both sides, max over ranks. A (>= 1.6 GB) is larger than
+L2, so no explicit flush is needed between steps.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# measured on this pool's B200s (profiles/fp64_peaks.json): cuBLAS DGEMM
+# 8192^3 sustained 35.4 TF/s (the FP64 roofline denominator, same method as
+# MEASURED_PEAKS.json's bf16 figure) and the raw DMMA pipe 37.0 TF/s.
+FP64_PEAK_TFLOPS = 35.43
+FP64_PIPE_TFLOPS = 37.0
+
+CONFIGS = {
+    "c1": dict(m=20000, n=256, method="truncated", l=0, q=0, t=0.95, spec="c1", noise=1e-3,
+               desc="c1: truncated SVD via Gram, 20000x256, t=0.95"),
+    "c2": dict(m=200000, n=1024, method="randomized", l=1024, q=2, t=0.99, spec="c2", noise=1e-3,
+               desc="c2: randomized PCA 200000x1024, l=min(1024+10,1024), q=2, CholeskyQR2, t=0.99"),
+    "c3": dict(m=500000, n=2048, method="lanczos", l=0, q=0, t=0.95, spec="c3", noise=1e-4,
+               desc="c3: Lanczos on A^T A, 500000x2048, n steps, full reorth, t=0.95"),
+    "c4": dict(m=8388608, n=1024, method="truncated", l=0, q=0, t=0.95, spec="c4", noise=1e-3,
+               desc="c4: row-sharded truncated SVD 8388608x1024 (64 GB), t=0.95"),
+    "c5": dict(m=65536, n=4096, method="truncated", l=0, q=0, t=0.90, spec="c5", noise=1e-2,
+               desc="c5: full-spectrum truncated SVD 65536x4096, t=0.90"),
+}
+METHOD_ID = {"truncated": 0, "randomized": 1, "krylov": 2, "lanczos": 3}
+SPECTRA = {
+    "c1": lambda i: math.exp(-i / 20.0),
+    "c2": lambda i: i ** -1.5,
+    "c3": lambda i: math.exp(-i / 200.0),
+    "c4": lambda i: 1.0 / i,
+    "c5": lambda i: 1.0 / (1.0 + 0.01 * i),
+}
+
+
+# --------------------------------------------------------------------------- helpers
+def method_flops(cfg, m):
+    """Algorithmic FP64 flops of one pipeline pass (SURVEY 8d counts)."""
+    n, l, q = cfg["n"], cfg["l"], cfg["q"]
+    if cfg["method"] == "truncated":
+        return m * n * (n + 1) + 2.0 * m * n * n  # Gram + U = A V
+    if cfg["method"] == "randomized":
+        gemms = 2.0 * m * n * l * (1 + 2 * q + 1)  # A Omega, q x (A^T Y, A Z), T = A^T Q
+        qr = 2 * (m * l * (l + 1) + m * l * l)    # CholeskyQR2: 2 x (SYRK + TRSM)
+        return gemms + qr + 2.0 * m * l * l       # + U = Q W
+    if cfg["method"] == "lanczos":
+        return 4.0 * m * n * n + 2.0 * m * n * n  # n GEMV pairs + U
+    return float("nan")
+
+
+def clocks_sampler_start(path):
+    q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    try:
+        return subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "200"],
+                                stdout=open(path, "w"), stderr=subprocess.DEVNULL)
+    except Exception:
+        return None
+
+
+def clocks_sampler_stop(proc, path, device):
+    if proc is None:
+        return None
+    proc.terminate()
+    try:
+        proc.wait(timeout=5)
+    except Exception:
+        proc.kill()
+    sm, mx, reasons = [], None, set()
+    names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+    for line in open(path):
+        f = [x.strip() for x in line.split(",")]
+        if len(f) < 9 or f[0] != str(device):
+            continue
+        try:
+            sm.append(float(f[1]))
+            mx = float(f[2])
+        except ValueError:
+            continue
+        for nm, v in zip(names, f[5:9]):
+            if v.lower() == "active":
+                reasons.add(nm)
+    if not sm:
+        return None
+    return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- data
+def generate(cfg, m, device, rank, seed=42):
+    """A = U0 diag(s) V0^T + noise N, column-centred: U0 = X R^-1
+    with X Gaussian and R the Cholesky factor of X^T X (CholeskyQR; the Q of
+    X's thin QR), generated in row chunks so only A itself stays resident."""
+    import torch
+
+    from paper_1906_12085_b200.engine import colmajor
+    n = cfg["n"]
+    f64 = torch.float64
+    gen = torch.Generator(device=device)
+    chunk = 1 << 17
+
+    def xchunk(c0, rows):
+        gen.manual_seed((seed * 1000003 + rank * 7919 + c0 // chunk) % (2 ** 63))
+        return torch.randn(rows, n, dtype=f64, device=device, generator=gen)
+
+    G = torch.zeros(n, n, dtype=f64, device=device)
+    for c0 in range(0, m, chunk):
+        x = xchunk(c0, min(chunk, m - c0))
+        G += x.T @ x
+    L = torch.linalg.cholesky(G)  # G = L L^T, R = L^T
+    gen.manual_seed(seed + 17)
+    v0, _ = torch.linalg.qr(torch.randn(n, n, dtype=f64, device=device, generator=gen))
+    s = torch.tensor([SPECTRA[cfg["spec"]](i) for i in range(1, n + 1)], dtype=f64, device=device)
+    Mx = torch.linalg.solve_triangular(L.T, s[:, None] * v0.T, upper=True)  # R^-1 S V0^T
+    A = colmajor(m, n, device)
+    noise_gen = torch.Generator(device=device)
+    for c0 in range(0, m, chunk):
+        rows = min(chunk, m - c0)
+        x = xchunk(c0, rows)
+        noise_gen.manual_seed((seed * 31 + rank * 131071 + c0 // chunk + 99991) % (2 ** 63))
+        A[c0:c0 + rows] = x @ Mx + cfg["noise"] * torch.randn(rows, n, dtype=f64, device=device, generator=noise_gen)
+        del x
+    mean = A.sum(0) / m
+    A -= mean
+    torch.cuda.synchronize()
+    return A
+
+
+# --------------------------------------------------------------------------- reference arm
+def reference_arm(args, cfg):
+    """The reference's own CPU implementation (oracle/_ref: the unmodified
+    reference sources compiled in place) on a bounded row sample of the same
+    workload, single-threaded (the reference is single-threaded by design,
+    SPEC.md:115). Work that scales with m (centering, the tall GEMMs,
+    Householder QR, U = Q W) is timed every step on m_s rows and scaled by
+    m / m_s; the m-independent small problem (Gram of T + eig_sym(l) +
+    T W, or eig_sym(n) for the Gram route) is timed once per process at the
+    full size n and added to every step."""
+    import numpy as np
+
+    from oracle.pyoracle import Oracle, available
+    if not available("ref"):
+        raise SystemExit(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+    ref = Oracle("ref")
+    m, n, l, q = cfg["m"] * args.gpus, cfg["n"], cfg["l"], cfg["q"]
+    rng = np.random.default_rng(7)
+    full = cfg["m"] * cfg["n"] <= 20000 * 256  # c1 runs whole
+    ms = m if full else max(n, 1024)
+    a = np.asfortranarray(rng.standard_normal((ms, n)) * np.array([SPECTRA[cfg["spec"]](i) for i in range(1, n + 1)]))
+
+    def rows_part():
+        t0 = time.perf_counter()
+        c, _ = ref.center(a, 1)
+        ref.frobenius_norm_sq(c)
+        if cfg["method"] == "randomized":
+            om = ref.gaussian_matrix(n, l, 4242)
+            h = ref.matmul(c, om)
+            for _ in range(q):
+                h = ref.matmul(c, ref.matmul_tl(c, h))
+            qq, _, _ = ref.qr_thin(h)
+            t = ref.matmul_tl(c, qq)
+            ref.matmul(qq, np.asfortranarray(np.eye(l)))  # U = Q W  (m x l x l)
+            return time.perf_counter() - t0, t
+        g = ref.gram(c)
+        ref.matmul(c, np.asfortranarray(np.eye(n)))  # U = A V (m x n x n)
+        return time.perf_counter() - t0, g
+
+    fixed = 0.0
+    sample = ""
+    if full:
+        def step():
+            t0 = time.perf_counter()
+            c, _ = ref.center(a, 1)
+            ref.frobenius_norm_sq(c)
+            ref.truncated_svd(c)
+            return time.perf_counter() - t0
+        sample = f"full reference fit_pca (center, total, truncated_svd) on {m}x{n}"
+    else:
+        _, small = rows_part()
+        extrap = ""
+        t0 = time.perf_counter()
+        if cfg["method"] == "randomized":
+            g = ref.gram(small)
+            w, v = ref.eig_sym(g)
+            ref.matmul(small, v)
+        elif n <= 1024:
+            ref.eig_sym(small)
+        else:
+            # eig_sym(n) takes 17 min at n = 2048 and ~3.4 h at 4096 on one core:
+            # time it at 512 and scale by the measured 12x per doubling of n
+            # (0.54 / 6.75 / 82.0 / 1002.7 s for n = 256..2048)
+            ref.eig_sym(np.asfortranarray(small[:512, :512]))
+            extrap = f", eig_sym({n}) extrapolated from n=512 by 12^log2(n/512)"
+        fixed = time.perf_counter() - t0
+        if extrap:
+            fixed *= 12.0 ** math.log2(n / 512)
+
+        def step():
+            t, _ = rows_part()
+            return t * (m / ms) + fixed
+        sample = (f"reference kernels on {ms} of {m} rows (x{m / ms:.0f}, m-proportional phases) + "
+                  f"m-independent small problem timed once ({fixed:.1f} s{extrap})")
+    for _ in range(args.warmup):
+        step()
+    ts = [step() for _ in range(args.steps)]
+    sec = sum(ts) / len(ts)
+    value = m / sec
+    return {"metric": "pca_rows_per_sec", "value": value, "unit": "rows/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded Gaussian sample)",
+            "impl": "reference",
+            "config": {"workload": cfg["desc"], "m": m, "n": n, "method": cfg["method"], "l": l, "q": q},
+            "cpu_baseline": {"value": value, "unit": "rows/s", "cores": 1, "kind": "reference", "sample": sample},
+            "e2e": {"value": value, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+# --------------------------------------------------------------------------- our arm
+def ours(args, cfg):
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1906_12085_b200 import _lib
+    from paper_1906_12085_b200.engine import Engine, colmajor
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    eng = Engine(local)
+    torch.cuda.set_stream(eng.stream)
+    if world > 1:
+        obj = [_lib.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        eng.ctx.attach_nccl(obj[0], rank, world)
+
+    m, n = cfg["m"], cfg["n"]
+    if cfg.get("strong"):
+        m = m // world
+    mid = METHOD_ID[cfg["method"]]
+    A = generate(cfg, m, torch.device("cuda", local), rank)
+
+    cpu_proc = None
+    cpu_out = tempfile.NamedTemporaryFile(suffix=".json", delete=False).name
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        ncpu = os.cpu_count() or 1
+        env = dict(os.environ, CUDA_VISIBLE_DEVICES="")
+        cmd = [sys.executable, os.path.abspath(__file__), "--impl", "reference", "--config", args.config,
+               "--steps", "1", "--warmup", "0"]
+        if ncpu > 2:
+            cmd = ["taskset", "-c", str(ncpu - 1)] + cmd
+            os.sched_setaffinity(0, set(range(ncpu - 1)))
+        cpu_proc = subprocess.Popen(cmd, stdout=open(cpu_out, "w"), stderr=subprocess.DEVNULL, env=env)
+
+    out = None
+
+    def step():
+        return eng.pca(A, method=mid, l=cfg["l"], q=cfg["q"], seed=4242, center=True, threshold=cfg["t"],
+                       out=out)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    out = step()  # allocates the output buffers reused by every later step
+    for _ in range(max(args.warmup - 1, 0)):
+        out = step()
+    torch.cuda.synchronize()
+
+    # ---------------- timed region (device-resident A) ----------------
+    eng.ctx.set_timing(True)
+    eng.ctx.timing_reset()
+    clk_path = tempfile.NamedTemporaryFile(suffix=".csv", delete=False).name
+    clk = clocks_sampler_start(clk_path) if rank == 0 else None
+    l0 = eng.launches()
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(eng.stream)
+    for _ in range(args.steps):
+        out = step()
+    e1.record(eng.stream)
+    torch.cuda.synchronize()
+    barrier()
+    launches = eng.launches() - l0
+    clocks = clocks_sampler_stop(clk, clk_path, local) if rank == 0 else None
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    names = eng.ctx.timing_names()
+    phases = {nm: eng.ctx.timing(nm) for nm in names}
+    eng.ctx.set_timing(False)
+    ms_step = ms / args.steps
+    rows_total = m * world
+    value = rows_total * args.steps / (ms / 1e3)
+
+    # ---------------- e2e: host buffers through the C-ABI ----------------
+    e2e_bytes_in = 8 * m * n
+    width = {"randomized": cfg["l"]}.get(cfg["method"], n)
+    if world == 1:
+        lib = _lib.load()
+        host = torch.empty(n, m, dtype=torch.float64, pin_memory=True).t()
+        host.copy_(A)
+        basis = torch.empty(width, n, dtype=torch.float64, pin_memory=True)
+        eig = torch.empty(width, dtype=torch.float64, pin_memory=True)
+        mean = torch.empty(n, dtype=torch.float64, pin_memory=True)
+        total, rank_c = C.c_double(0), C.c_int64(0)
+        kk = C.c_int64(0)
+
+        def e2e_step():
+            _lib.check(lib.svdk_fit_pca(eng.ctx.handle, C.c_void_p(host.data_ptr()), m, n, 1, mid, cfg["l"],
+                                        cfg["q"], 4242, 1, C.c_void_p(basis.data_ptr()), C.c_void_p(eig.data_ptr()),
+                                        C.byref(total), C.c_void_p(mean.data_ptr()), C.byref(rank_c)))
+            _lib.check(lib.svdk_select_components(eng.ctx.handle, C.c_void_p(eig.data_ptr()), rank_c.value,
+                                                  total.value, cfg["t"], C.byref(kk)))
+        e2e_step()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        torch.cuda.synchronize()
+        e2e_sec = (time.perf_counter() - t0) / args.steps
+        e2e_out = 8 * (n * rank_c.value + rank_c.value + n)
+        e2e_k = kk.value
+    else:
+        host = torch.empty(n, m, dtype=torch.float64, pin_memory=True).t()
+        host.copy_(A)
+        dev = colmajor(m, n)
+        res = torch.empty(n * width + width + n, dtype=torch.float64, pin_memory=True)
+
+        def e2e_step():
+            dev.copy_(host, non_blocking=True)
+            o = eng.pca(dev, method=mid, l=cfg["l"], q=cfg["q"], seed=4242, center=True, threshold=cfg["t"])
+            r = o.rank
+            res[:n * r].copy_(o.v[:, :r].t().reshape(-1), non_blocking=True)
+            res[n * r:n * r + r].copy_(o.sigma[:r], non_blocking=True)
+            return o
+        e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            o = e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        tt = torch.tensor([(time.perf_counter() - t0) / args.steps], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_sec = float(tt.item())
+        e2e_out = 8 * (n * o.rank + o.rank)
+        e2e_k = o.k
+    e2e_value = rows_total / e2e_sec
+
+    # ---------------- roofline of the dominant kernel (DMMA GEMM/SYRK) ----------------
+    g = phases.get("dmma_gemm", {"count": 0, "ms": 0.0, "flops": 0.0, "bytes": 0.0})
+    achieved = g["flops"] / (g["ms"] / 1e3) / 1e12 if g["ms"] > 0 else 0.0
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", f"dram_traffic_{args.config}.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "tensor", "kernel": "gemm_kernel (FP64 DMMA.8x8x4 + TMA)", "achieved": achieved,
+                "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
+                "traffic": traffic, "launches": g["count"], "share_of_step": g["ms"] / ms if ms else None,
+                "peak_source": "measured cuBLAS DGEMM 8192^3 sustained on B200 (profiles/fp64_peaks.json); "
+                               f"DMMA pipe peak {FP64_PIPE_TFLOPS} TF/s -> frac_pipe "
+                               f"{achieved / FP64_PIPE_TFLOPS:.3f}"}
+
+    cpu = None
+    if cpu_proc is not None:
+        cpu_proc.wait()
+        try:
+            line = [x for x in open(cpu_out).read().splitlines() if x.startswith("{")][-1]
+            r = json.loads(line)
+            cpu = r.get("cpu_baseline") or {"unavailable": r.get("unavailable")}
+        except Exception as e:  # pragma: no cover
+            cpu = {"unavailable": f"cpu baseline failed: {e}"}
+
+    if rank == 0:
+        flops = method_flops(cfg, m) * world
+        line = {
+            "metric": "pca_rows_per_sec", "value": value, "unit": "rows/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong" if cfg.get("strong") else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: seeded low-rank + Gaussian noise generator of SURVEY 8d, column-centred",
+            "config": {"workload": cfg["desc"], "m_per_gpu": m, "n": n, "method": cfg["method"], "l": cfg["l"],
+                       "q": cfg["q"], "threshold": cfg["t"], "parallelism": f"dp{world} (row shards, NCCL allreduce)",
+                       "l2": "no flush: A is larger than the 126 MB L2"},
+            "pipeline_tflops": flops / (ms_step / 1e3) / 1e12,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "rows/s", "h2d_bytes_per_step": e2e_bytes_in,
+                    "d2h_bytes_per_step": e2e_out, "path": "svdk_fit_pca + svdk_select_components (host buffers)"
+                    if world == 1 else "H2D shard + svdk_dev_pca + D2H basis/sigma"},
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "phases_ms_per_step": {k: round(v["ms"] / args.steps, 3) for k, v in phases.items()},
+            "result": {"rank": out.rank, "K": out.k, "total_variance": out.total, "e2e_K": e2e_k},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = dict(CONFIGS[args.config])
+    if args.config == "c4":
+        cfg["strong"] = True
+    if args.impl == "reference":
+        if int(os.environ.get("RANK", 0)) != 0:
+            return
+        cfg_ref = dict(cfg)
+        if cfg.get("strong"):
+            args.gpus = 1  # the reference works on the whole matrix
+        print(json.dumps(reference_arm(args, cfg_ref)), flush=True)
+        return
+    ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

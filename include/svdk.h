@@ -64,6 +64,15 @@ int64_t svdk_ctx_launches(svdk_ctx* ctx);
 /* Sweeps used by the most recent eig_sym on this context. */
 int svdk_ctx_last_sweeps(svdk_ctx* ctx);
 const char* svdk_version(void);
+/* Per-kernel device timing with CUDA events on the context stream (bench
+ * evidence): records carry the algorithmic flops / bytes of each launch.
+ * Query sums the records whose phase name matches (NULL = all); names are
+ * e.g. "dmma_gemm", "splitk_reduce", "eig_sym", "qr_thin", "gemv_pair". */
+int svdk_ctx_set_timing(svdk_ctx* ctx, int enable);
+int svdk_ctx_timing_reset(svdk_ctx* ctx);
+int svdk_ctx_timing_query(svdk_ctx* ctx, const char* name, int64_t* count, double* ms,
+                          double* flops, double* bytes);
+int svdk_ctx_timing_names(svdk_ctx* ctx, char* buf, int64_t len);
 
 /* ---- row-sharded multi-GPU (one process per GPU, NCCL over NVLink) ---- */
 /* 128-byte NCCL unique id, produced on rank 0 and shared out of band. */

@@ -33,6 +33,10 @@ SIGNATURES = {
     "svdk_ctx_launches": (_i64, [_ctxp]),
     "svdk_ctx_last_sweeps": (C.c_int, [_ctxp]),
     "svdk_version": (C.c_char_p, []),
+    "svdk_ctx_set_timing": (C.c_int, [_ctxp, C.c_int]),
+    "svdk_ctx_timing_reset": (C.c_int, [_ctxp]),
+    "svdk_ctx_timing_query": (C.c_int, [_ctxp, C.c_char_p, _ip64, _dp, _dp, _dp]),
+    "svdk_ctx_timing_names": (C.c_int, [_ctxp, C.c_char_p, _i64]),
     "svdk_nccl_unique_id": (C.c_int, [C.c_char_p]),
     "svdk_ctx_attach_nccl": (C.c_int, [_ctxp, C.c_char_p, C.c_int, C.c_int]),
     "svdk_matmul": (C.c_int, [_ctxp, _vp, _i64, _i64, _vp, _i64, _vp]),
@@ -115,6 +119,24 @@ class Context:
 
     def last_sweeps(self) -> int:
         return int(load().svdk_ctx_last_sweeps(self._h))
+
+    def set_timing(self, enable: bool) -> None:
+        check(load().svdk_ctx_set_timing(self._h, 1 if enable else 0))
+
+    def timing_reset(self) -> None:
+        check(load().svdk_ctx_timing_reset(self._h))
+
+    def timing(self, name: str | None = None) -> dict:
+        """{count, ms, flops, bytes} summed over records named `name` (None = all)."""
+        cnt, ms, fl, by = C.c_int64(0), C.c_double(0), C.c_double(0), C.c_double(0)
+        check(load().svdk_ctx_timing_query(self._h, name.encode() if name else None, C.byref(cnt), C.byref(ms),
+                                           C.byref(fl), C.byref(by)))
+        return {"count": cnt.value, "ms": ms.value, "flops": fl.value, "bytes": by.value}
+
+    def timing_names(self) -> list:
+        buf = C.create_string_buffer(4096)
+        check(load().svdk_ctx_timing_names(self._h, buf, 4096))
+        return [x for x in buf.value.decode().split(",") if x]
 
     def attach_nccl(self, unique_id: bytes, rank: int, world: int) -> None:
         check(load().svdk_ctx_attach_nccl(self._h, unique_id, int(rank), int(world)))

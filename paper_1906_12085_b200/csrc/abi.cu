@@ -211,6 +211,7 @@ int svdk_ctx_destroy(svdk_ctx* ctx) {
         destroy_comm(ctx);
         ctx->pool.trim();
         if (ctx->d_flags) cudaFree(ctx->d_flags);
+        for (cudaEvent_t e : ctx->event_pool) cudaEventDestroy(e);
         if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
         delete ctx;
     });
@@ -235,6 +236,60 @@ int svdk_ctx_sync(svdk_ctx* ctx) {
 
 int64_t svdk_ctx_launches(svdk_ctx* ctx) { return ctx ? ctx->launches : 0; }
 int svdk_ctx_last_sweeps(svdk_ctx* ctx) { return ctx ? ctx->jacobi_sweeps : 0; }
+
+int svdk_ctx_set_timing(svdk_ctx* ctx, int enable) {
+    return guarded([&] {
+        need_ctx(ctx);
+        ctx->timing = enable != 0;
+    });
+}
+
+int svdk_ctx_timing_reset(svdk_ctx* ctx) {
+    return guarded([&] {
+        need_ctx(ctx);
+        sync(ctx);
+        ctx->records.clear();
+        ctx->events_used = 0;
+    });
+}
+
+int svdk_ctx_timing_query(svdk_ctx* ctx, const char* name, int64_t* count, double* ms,
+                          double* flops, double* bytes) {
+    return guarded([&] {
+        need_ctx(ctx);
+        sync(ctx);
+        int64_t n = 0;
+        double t = 0.0, f = 0.0, b = 0.0;
+        for (const auto& r : ctx->records) {
+            if (name && std::strcmp(name, r.name) != 0) continue;
+            float e = 0.0f;
+            SVDK_CUDA(cudaEventElapsedTime(&e, r.e0, r.e1));
+            ++n;
+            t += e;
+            f += r.flops;
+            b += r.bytes;
+        }
+        if (count) *count = n;
+        if (ms) *ms = t;
+        if (flops) *flops = f;
+        if (bytes) *bytes = b;
+    });
+}
+
+int svdk_ctx_timing_names(svdk_ctx* ctx, char* buf, int64_t len) {
+    return guarded([&] {
+        need_ctx(ctx);
+        std::string s;
+        for (const auto& r : ctx->records) {
+            const std::string nm(r.name);
+            if (("," + s + ",").find("," + nm + ",") == std::string::npos) s += (s.empty() ? "" : ",") + nm;
+        }
+        if (buf && len > 0) {
+            std::strncpy(buf, s.c_str(), static_cast<size_t>(len - 1));
+            buf[len - 1] = 0;
+        }
+    });
+}
 
 int svdk_gaussian_matrix(int64_t rows, int64_t cols, uint64_t seed, double* out) {
     return guarded([&] {

@@ -224,6 +224,7 @@ bool cholqr_pass(Ctx* c, double* H, int64_t ldh, int64_t m, int64_t p, double* Q
 int64_t qr_thin(Ctx* c, const double* H, int64_t ldh, int64_t m, int64_t p, double* Q, int64_t ldq,
                 double* R, const RowComm* comm) {
     if (p == 0) return 0;
+    PhaseTimer timer(c, "qr_thin");
     const int64_t ldw = round_up(std::max<int64_t>(m, 1), 2);
     DBuf W(c, static_cast<size_t>(ldw) * p), Q1(c, static_cast<size_t>(ldw) * p);
     DBuf R1(c, static_cast<size_t>(p) * p), R2(c, static_cast<size_t>(p) * p);

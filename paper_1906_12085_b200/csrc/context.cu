@@ -96,6 +96,29 @@ void DBuf::reset() {
     n_ = 0;
 }
 
+namespace {
+cudaEvent_t take_event(Ctx* c) {
+    if (c->events_used == c->event_pool.size()) {
+        cudaEvent_t e;
+        SVDK_CUDA(cudaEventCreate(&e));
+        c->event_pool.push_back(e);
+    }
+    return c->event_pool[c->events_used++];
+}
+}  // namespace
+
+PhaseTimer::PhaseTimer(Ctx* c, const char* name, double flops, double bytes) : c_(c) {
+    if (!c->timing) return;
+    PhaseRecord r{name, take_event(c), take_event(c), flops, bytes};
+    SVDK_CUDA(cudaEventRecord(r.e0, c->stream));
+    idx_ = static_cast<long>(c->records.size());
+    c->records.push_back(r);
+}
+
+PhaseTimer::~PhaseTimer() {
+    if (idx_ >= 0) cudaEventRecord(c_->records[idx_].e1, c_->stream);
+}
+
 void h2d(Ctx* c, double* dst, const double* src, int64_t count) {
     if (count <= 0) return;
     SVDK_CUDA(cudaMemcpyAsync(dst, src, sizeof(double) * count, cudaMemcpyHostToDevice, c->stream));

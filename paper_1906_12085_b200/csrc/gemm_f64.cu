@@ -408,13 +408,22 @@ void launch(Ctx* c, Params& p, const CUtensorMap& ma, const CUtensorMap& mb) {
         p.partial = partial.p();
     }
     const int grid = std::min(p.units, c->num_sms);
-    if (p.a_mmajor)
-        gemm_kernel<true><<<grid, THREADS, SMEM_BYTES, c->stream>>>(ma, mb, p);
-    else
-        gemm_kernel<false><<<grid, THREADS, SMEM_BYTES, c->stream>>>(ma, mb, p);
-    SVDK_CHECK_LAUNCH();
-    c->launches++;
+    // algorithmic work: Gram m n (n+1); GEMM 2 M N K
+    const double flops = p.kind == KIND_SYRK ? static_cast<double>(p.K) * p.M * (p.M + 1)
+                                             : 2.0 * p.M * p.N * p.K;
+    const double bytes = p.kind == KIND_SYRK ? 8.0 * (p.K * p.M + p.M * p.M)
+                                             : 8.0 * (p.M * p.K + p.K * p.N + p.M * p.N);
+    {
+        PhaseTimer timer(c, "dmma_gemm", flops, bytes);
+        if (p.a_mmajor)
+            gemm_kernel<true><<<grid, THREADS, SMEM_BYTES, c->stream>>>(ma, mb, p);
+        else
+            gemm_kernel<false><<<grid, THREADS, SMEM_BYTES, c->stream>>>(ma, mb, p);
+        SVDK_CHECK_LAUNCH();
+        c->launches++;
+    }
     if (p.splits > 1) {
+        PhaseTimer timer(c, "splitk_reduce", 0.0, 8.0 * p.units * TILE_ELEMS);
         splitk_reduce_kernel<<<dim3(p.n_tiles, 8), 256, 0, c->stream>>>(p);
         SVDK_CHECK_LAUNCH();
         c->launches++;

@@ -508,6 +508,7 @@ void eig_sym(Ctx* c, const double* S, int64_t lds, int64_t n, int max_sweeps, do
              double* Vout, int64_t ldv) {
     if (max_sweeps <= 0) max_sweeps = 30;
     if (n == 0) return;
+    PhaseTimer timer(c, "eig_sym");
     // symmetry check (kernels.cpp:251-262)
     {
         const int blocks = static_cast<int>(

@@ -209,8 +209,12 @@ int64_t lanczos_svd(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n, 
     double prev_beta = 0.0;
     for (int64_t j = 0; j < steps; ++j) {
         const double* qj = Q.p() + j * n;
-        gemv_pair_kernel<<<parts, GV_THREADS, gv_smem, c->stream>>>(A, lda, m, n, qj, partial.p());
-        SVDK_CHECK_LAUNCH();
+        {
+            PhaseTimer timer(c, "gemv_pair", 4.0 * m * n, 8.0 * m * n);
+            gemv_pair_kernel<<<parts, GV_THREADS, gv_smem, c->stream>>>(A, lda, m, n, qj,
+                                                                        partial.p());
+            SVDK_CHECK_LAUNCH();
+        }
         reduce_parts_kernel<<<static_cast<unsigned>(ceil_div(n, 256)), 256, 0, c->stream>>>(
             partial.p(), parts, n, w.p());
         SVDK_CHECK_LAUNCH();

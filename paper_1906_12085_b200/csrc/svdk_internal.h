@@ -87,6 +87,15 @@ struct DMat {
     double* col(int64_t j) const { return p + j * ld; }
 };
 
+// Per-phase device timing (CUDA events on the context stream), enabled by
+// svdk_ctx_set_timing: algorithmic flops / bytes are attached to each record
+// so bench.py can report achieved TFLOP/s or GB/s per kernel.
+struct PhaseRecord {
+    const char* name;
+    cudaEvent_t e0, e1;
+    double flops, bytes;
+};
+
 struct Ctx {
     int device = 0;
     int num_sms = 148;
@@ -100,10 +109,28 @@ struct Ctx {
     // multi-GPU (row-sharded) state
     void* nccl_comm = nullptr;
     int rank = 0, world = 1;
+    // timing
+    bool timing = false;
+    std::vector<PhaseRecord> records;
+    std::vector<cudaEvent_t> event_pool;
+    size_t events_used = 0;
     // counters for bench/introspection
     int64_t launches = 0;
     int jacobi_sweeps = 0;
     double last_off_norm = 0.0;
+};
+
+// RAII phase timer: records e0 now and e1 at scope exit (no-op unless timing).
+class PhaseTimer {
+public:
+    PhaseTimer(Ctx* c, const char* name, double flops = 0.0, double bytes = 0.0);
+    ~PhaseTimer();
+    PhaseTimer(const PhaseTimer&) = delete;
+    PhaseTimer& operator=(const PhaseTimer&) = delete;
+
+private:
+    Ctx* c_;
+    long idx_ = -1;
 };
 
 inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
