@@ -117,18 +117,26 @@ void validate_sketch(int64_t m, int64_t n, int64_t l, int64_t q, bool krylov) {
 int64_t run_method(Ctx* c, int method, const double* dA, int64_t lda, int64_t m, int64_t n,
                    int64_t l, int64_t q, uint64_t seed, double* dU, int64_t ldu, double* dS,
                    double* dV, int64_t ldv, const RowComm* comm) {
+    reset_nonfinite(c);
+    int64_t r = 0;
     switch (method) {
         case SVDK_TRUNCATED:
-            return truncated_svd(c, dA, lda, m, n, dU, ldu, dS, dV, ldv, comm);
+            r = truncated_svd(c, dA, lda, m, n, dU, ldu, dS, dV, ldv, comm);
+            break;
         case SVDK_RANDOMIZED:
-            return randomized_pca(c, dA, lda, m, n, l, q, seed, dU, ldu, dS, dV, ldv, comm);
+            r = randomized_pca(c, dA, lda, m, n, l, q, seed, dU, ldu, dS, dV, ldv, comm);
+            break;
         case SVDK_KRYLOV:
-            return krylov_svd(c, dA, lda, m, n, l, q, seed, dU, ldu, dS, dV, ldv, comm);
+            r = krylov_svd(c, dA, lda, m, n, l, q, seed, dU, ldu, dS, dV, ldv, comm);
+            break;
         case SVDK_LANCZOS:
-            return lanczos_svd(c, dA, lda, m, n, l, seed, dU, ldu, dS, dV, ldv, comm);
+            r = lanczos_svd(c, dA, lda, m, n, l, seed, dU, ldu, dS, dV, ldv, comm);
+            break;
         default:
             fail(SVDK_E_PARAM, "compute_svd: unknown method");
     }
+    raise_if_nonfinite(c);  // kernels.cpp:39-43, once per call
+    return r;
 }
 
 // Output column bound of each method for a tall m x n input.
@@ -209,6 +217,7 @@ int svdk_ctx_destroy(svdk_ctx* ctx) {
         cudaSetDevice(ctx->device);
         cudaStreamSynchronize(ctx->stream);
         destroy_comm(ctx);
+        release_host_staging(ctx);
         ctx->pool.trim();
         if (ctx->d_flags) cudaFree(ctx->d_flags);
         for (cudaEvent_t e : ctx->event_pool) cudaEventDestroy(e);
@@ -483,6 +492,13 @@ int svdk_fit_pca(svdk_ctx* c, const double* data, int64_t m, int64_t n, int orie
         // pca.cpp:91-116: center -> total -> compute_svd_any -> basis, sigma^2
         const bool cols_ex = orientation == SVDK_COLUMNS_ARE_EXAMPLES;
         const int64_t nm = cols_ex ? m : n;
+        {
+            const int64_t tn = std::min(m, n);  // the tall problem's width
+            if ((method == SVDK_RANDOMIZED || method == SVDK_KRYLOV) && l >= 1 && l <= tn)
+                omega_prefetch(c, tn, l, seed);
+            else if (method == SVDK_LANCZOS)
+                omega_prefetch(c, tn, 1, seed);
+        }
         int64_t lda, ldc;
         DBuf dA = upload(c, data, m, n, lda);
         DBuf dC = alloc_mat(c, m, n, ldc);

@@ -73,26 +73,22 @@ __global__ void __launch_bounds__(256)
         const int i = e % bs, j = e / bs;
         R[(k0 + i) + (k0 + j) * ldr] = i <= j ? S[i + j * LD] : 0.0;
     }
-    // R^-1 by column back substitution; column c is computed by thread c and
-    // kept transposed in the free strictly-lower part of S: X[i][c] -> S[c][i].
-    if (tid < bs) {
-        const int c = tid;
-        const double xcc = dinv[c];
-        for (int i = c - 1; i >= 0; --i) {
-            double s = S[i + c * LD] * xcc;
-            for (int k = i + 1; k < c; ++k) s += S[i + k * LD] * S[c + k * LD];
-            S[c + i * LD] = -s * dinv[i];
+    // R^-1 by row-step back substitution, parallel over columns: for i from
+    // the bottom, X[i][c] = -(sum_{k=i+1..c} R[i][k] X[k][c]) / R[i][i].
+    // X (upper) is kept transposed in the free strictly-lower part of S:
+    // X[i][c] -> S[c][i] for i < c; its diagonal is dinv.
+    __syncthreads();
+    for (int i = bs - 2; i >= 0; --i) {
+        for (int cc = i + 1 + tid; cc < bs; cc += blockDim.x) {
+            double s = S[i + cc * LD] * dinv[cc];
+            for (int k = i + 1; k < cc; ++k) s = fma(S[i + k * LD], S[cc + k * LD], s);
+            S[cc + i * LD] = -s * dinv[i];
         }
-        for (int i = 0; i < bs; ++i) {
-            double x;
-            if (i < c)
-                x = S[c + i * LD];
-            else if (i == c)
-                x = xcc;
-            else
-                x = 0.0;
-            Rinv[i + c * ldri] = x;
-        }
+        __syncthreads();
+    }
+    for (int e = tid; e < bs * bs; e += blockDim.x) {
+        const int i = e % bs, cc = e / bs;
+        Rinv[i + cc * ldri] = i < cc ? S[cc + i * LD] : (i == cc ? dinv[cc] : 0.0);
     }
 }
 

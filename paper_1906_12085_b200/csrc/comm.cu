@@ -99,6 +99,12 @@ double frob_sq_rows(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n,
     return out;
 }
 
+void frob_sq_rows_dev(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n, double* d_out,
+                      const RowComm* comm) {
+    frob_sq_dev(c, A, lda, m, n, d_out);
+    if (comm && comm->world() > 1) comm->allreduce(d_out, 1);
+}
+
 void eig_sym_rows(Ctx* c, const double* S, int64_t lds, int64_t n, double* w, double* V,
                   int64_t ldv, const RowComm* comm) {
     if (!comm || comm->world() == 1) {

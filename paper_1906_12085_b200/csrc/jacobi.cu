@@ -53,6 +53,32 @@ __host__ __device__ __forceinline__ void circle_pair(int P, int r, int i, int& a
     }
 }
 
+// Jacobi rotation annihilating a_pq (reference kernels.cpp:282-290):
+//   tau = (a_qq - a_pp) / (2 a_pq), t = sgn(tau) / (|tau| + sqrt(1 + tau^2)),
+//   c = 1 / sqrt(1 + t^2), s = t c.
+// Evaluated in the algebraically identical division-free form
+//   d = a_qq - a_pp, e = 2 a_pq, D = |d| + sqrt(d^2 + e^2),
+//   c = D / sqrt(D^2 + e^2), s = sgn(tau) |e| / sqrt(D^2 + e^2)
+// which shortens the dependent FP64 sqrt/div chain on the critical path of
+// every inner round (one sqrt + one rsqrt instead of 2 sqrt + 3 div). Values
+// outside [1e-140, 1e140] fall back to the reference evaluation.
+__device__ __forceinline__ void rotation(double app, double aqq, double apq, double& c, double& s) {
+    const double d = aqq - app, e = 2.0 * apq;
+    const double big = fmax(fabs(d), fabs(e));
+    if (big < 1e140 && big > 1e-140) {
+        const double D = fabs(d) + sqrt(fma(d, d, e * e));
+        const double inv = rsqrt(fma(D, D, e * e));
+        c = D * inv;
+        s = (d > 0.0 ? e : (d < 0.0 ? -e : fabs(e))) * inv;  // tau = +-0 -> t = +1
+        return;
+    }
+    const double tau = d / e;
+    const double t = tau >= 0.0 ? 1.0 / (tau + sqrt(1.0 + tau * tau))
+                                : -1.0 / (-tau + sqrt(1.0 + tau * tau));
+    c = 1.0 / sqrt(1.0 + t * t);
+    s = t * c;
+}
+
 // Global index of local index i (0..2b-1) of the pair (I, J).
 __device__ __forceinline__ int64_t gidx(int B, int I, int J, int i) {
     return i < B ? static_cast<int64_t>(I) * B + i : static_cast<int64_t>(J) * B + (i - B);
@@ -130,7 +156,6 @@ __global__ void __launch_bounds__(256)
     double* Q = sm + TB * LD;
     double* T = Q + TB * LD;
     __shared__ double cs[NP], sn[NP];
-    __shared__ int pp_s[NP], qq_s[NP], on_s[NP];
     __shared__ int any_applied;
 
     const int tid = threadIdx.x;
@@ -157,48 +182,36 @@ __global__ void __launch_bounds__(256)
                     circle_pair(TB, rr, tid, p, q);
                     const double apq = M[p + q * LD];
                     double c = 1.0, s = 0.0;
-                    int on = 0;
                     if (fabs(apq) > skip_tau) {
-                        // reference kernels.cpp:282-290
-                        const double tau = (M[q + q * LD] - M[p + p * LD]) / (2.0 * apq);
-                        double t;
-                        if (tau >= 0.0)
-                            t = 1.0 / (tau + sqrt(1.0 + tau * tau));
-                        else
-                            t = -1.0 / (-tau + sqrt(1.0 + tau * tau));
-                        c = 1.0 / sqrt(1.0 + t * t);
-                        s = t * c;
-                        on = 1;
+                        rotation(M[p + p * LD], M[q + q * LD], apq, c, s);
                         any_applied = 1;
                     }
-                    pp_s[tid] = p;
-                    qq_s[tid] = q;
                     cs[tid] = c;
                     sn[tid] = s;
-                    on_s[tid] = on;
                 }
                 __syncthreads();
-                // fused 2x2-block update  M <- R^T M R
+                // fused 2x2-block update  M <- R^T M R  (s == 0 marks a skipped pair)
                 for (int e = tid; e < NP * NP; e += blockDim.x) {
                     const int bi = e % NP, bj = e / NP;
-                    const int oi = on_s[bi], oj = on_s[bj];
+                    const double ci = cs[bi], si = sn[bi], cj = cs[bj], sj = sn[bj];
+                    const bool oi = si != 0.0, oj = sj != 0.0;
                     if (!(oi | oj)) continue;
-                    const int pi = pp_s[bi], qi = qq_s[bi], pj = pp_s[bj], qj = qq_s[bj];
+                    int pi, qi, pj, qj;
+                    circle_pair(TB, rr, bi, pi, qi);
+                    circle_pair(TB, rr, bj, pj, qj);
                     double m00 = M[pi + pj * LD], m01 = M[pi + qj * LD];
                     double m10 = M[qi + pj * LD], m11 = M[qi + qj * LD];
                     if (oj) {  // columns pj, qj
-                        const double c = cs[bj], s = sn[bj];
-                        const double a0 = c * m00 - s * m01, b0 = s * m00 + c * m01;
-                        const double a1 = c * m10 - s * m11, b1 = s * m10 + c * m11;
+                        const double a0 = cj * m00 - sj * m01, b0 = sj * m00 + cj * m01;
+                        const double a1 = cj * m10 - sj * m11, b1 = sj * m10 + cj * m11;
                         m00 = a0; m01 = b0; m10 = a1; m11 = b1;
                     }
                     if (oi) {  // rows pi, qi
-                        const double c = cs[bi], s = sn[bi];
-                        const double a0 = c * m00 - s * m10, b0 = s * m00 + c * m10;
-                        const double a1 = c * m01 - s * m11, b1 = s * m01 + c * m11;
+                        const double a0 = ci * m00 - si * m10, b0 = si * m00 + ci * m10;
+                        const double a1 = ci * m01 - si * m11, b1 = si * m01 + ci * m11;
                         m00 = a0; m10 = b0; m01 = a1; m11 = b1;
                     }
-                    if (bi == bj && oi) {  // the rotated pair is annihilated exactly
+                    if (bi == bj) {  // the rotated pair is annihilated exactly
                         m01 = 0.0;
                         m10 = 0.0;
                     }
@@ -209,9 +222,10 @@ __global__ void __launch_bounds__(256)
                 }
                 for (int e = tid; e < TB * NP; e += blockDim.x) {
                     const int r = e % TB, j = e / TB;
-                    if (!on_s[j]) continue;
-                    const int p = pp_s[j], q = qq_s[j];
                     const double c = cs[j], s = sn[j];
+                    if (s == 0.0) continue;
+                    int p, q;
+                    circle_pair(TB, rr, j, p, q);
                     const double x = Q[r + p * LD], y = Q[r + q * LD];
                     Q[r + p * LD] = c * x - s * y;
                     Q[r + q * LD] = s * x + c * y;

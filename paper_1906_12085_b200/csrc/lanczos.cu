@@ -194,16 +194,12 @@ int64_t lanczos_svd(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n, 
     double* alpha = scal.p();
     double* beta = scal.p() + steps;
     double* nrm = scal.p() + 2 * steps;  // [0] after pass 1, [1] after pass 2
-    // q_0 from the reference sampler
-    {
-        std::vector<double> g(n);
-        gaussian_fill(n, 1, seed, g.data());
-        double s = 0.0;
-        for (double x : g) s += x * x;
-        const double inv = 1.0 / std::sqrt(s);
-        for (double& x : g) x *= inv;
-        h2d(c, Q.p(), g.data(), n);
-    }
+    // q_0 = g / ||g|| with g from the reference sampler
+    omega_upload(c, n, 1, seed, w.p());
+    norm_kernel<<<1, 1024, 0, c->stream>>>(w.p(), n, nrm);
+    scale_kernel<<<static_cast<unsigned>(ceil_div(n, 256)), 256, 0, c->stream>>>(w.p(), n, nrm, Q.p());
+    SVDK_CHECK_LAUNCH();
+    c->launches += 2;
     double gnorm = 0.0;  // running Gershgorin bound on ||T||
     std::vector<double> hb(2);
     double prev_beta = 0.0;

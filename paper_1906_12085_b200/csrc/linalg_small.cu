@@ -176,18 +176,26 @@ void transpose(Ctx* c, const double* src, int64_t lds, int64_t rows, int64_t col
     c->launches++;
 }
 
-double frob_sq(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n) {
-    if (m <= 0 || n <= 0) return 0.0;
+void frob_sq_dev(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n, double* d_out) {
+    if (m <= 0 || n <= 0) {
+        fill(c, d_out, 1, 0.0);
+        return;
+    }
     const int blocks = static_cast<int>(
         std::max<int64_t>(1, std::min<int64_t>(ceil_div(m * n, 256), 4 * c->num_sms)));
-    DBuf partial(c, blocks + 1);
+    DBuf partial(c, blocks);
     sumsq_partial_kernel<<<blocks, 256, 0, c->stream>>>(A, lda, m, n, partial.p());
     SVDK_CHECK_LAUNCH();
-    sum_partials_kernel<<<1, 256, 0, c->stream>>>(partial.p(), blocks, partial.p() + blocks);
+    sum_partials_kernel<<<1, 256, 0, c->stream>>>(partial.p(), blocks, d_out);
     SVDK_CHECK_LAUNCH();
     c->launches += 2;
+}
+
+double frob_sq(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n) {
+    DBuf t(c, 1);
+    frob_sq_dev(c, A, lda, m, n, t.p());
     double out = 0.0;
-    d2h(c, &out, partial.p() + blocks, 1);
+    d2h(c, &out, t.p(), 1);
     return out;
 }
 

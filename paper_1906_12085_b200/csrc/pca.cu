@@ -5,6 +5,7 @@
 //   center / total     pca.cpp:13-59
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 
 #include "svdk_methods.h"
 
@@ -22,10 +23,10 @@ int64_t lanczos_svd(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n, 
 namespace {
 
 // status: 0 ok, 1 bad threshold, 2 bad total, 3 not nonneg-descending, 4 empty.
-// out[0] = K (0 = nullopt), out[1] = status. Validation in parallel; the
-// cumulative sum is sequential in index order like the reference, so K is
-// decided by the same rounding.
-__global__ void select_kernel(const double* w, int64_t count, double total, double t,
+// out[0] = K (0 = nullopt), out[1] = status, out[2] = total (bits). Validation
+// in parallel; the cumulative sum is sequential in index order like the
+// reference, so K is decided by the same rounding.
+__global__ void select_kernel(const double* w, int64_t count, const double* total_p, double t,
                               int64_t* out) {
     __shared__ int bad;
     if (threadIdx.x == 0) bad = 0;
@@ -36,6 +37,7 @@ __global__ void select_kernel(const double* w, int64_t count, double total, doub
     }
     __syncthreads();
     if (threadIdx.x != 0) return;
+    const double total = *total_p;
     int64_t status = 0, k = 0;
     if (!(t >= 0.0 && t <= 1.0))
         status = 1;
@@ -57,6 +59,7 @@ __global__ void select_kernel(const double* w, int64_t count, double total, doub
     }
     out[0] = k;
     out[1] = status;
+    out[2] = __double_as_longlong(total);
 }
 
 __global__ void square_kernel(const double* s, int64_t r, double* w) {
@@ -67,15 +70,19 @@ __global__ void square_kernel(const double* s, int64_t r, double* w) {
 
 }  // namespace
 
-int64_t select_components(Ctx* c, const double* d_w, int64_t count, double total, double t) {
-    DBuf out(c, 2);
+// pca.cpp:61-89 with the total variance on the device; returns K (0 =
+// nullopt) and optionally the total read back with it (one D2H).
+int64_t select_components_dev(Ctx* c, const double* d_w, int64_t count, const double* d_total,
+                              double t, double* total_out) {
+    DBuf out(c, 3);
     int64_t* o = reinterpret_cast<int64_t*>(out.p());
-    select_kernel<<<1, 256, 0, c->stream>>>(d_w, count, total, t, o);
+    select_kernel<<<1, 256, 0, c->stream>>>(d_w, count, d_total, t, o);
     SVDK_CHECK_LAUNCH();
     c->launches++;
-    int64_t h[2];
+    int64_t h[3];
     SVDK_CUDA(cudaMemcpyAsync(h, o, sizeof h, cudaMemcpyDeviceToHost, c->stream));
     SVDK_CUDA(cudaStreamSynchronize(c->stream));
+    if (total_out) std::memcpy(total_out, &h[2], sizeof(double));
     switch (h[1]) {
         case 1: {
             char buf[64];
@@ -95,6 +102,12 @@ int64_t select_components(Ctx* c, const double* d_w, int64_t count, double total
     return h[0];
 }
 
+int64_t select_components(Ctx* c, const double* d_w, int64_t count, double total, double t) {
+    DBuf dt(c, 1);
+    h2d(c, dt.p(), &total, 1);
+    return select_components_dev(c, d_w, count, dt.p(), t, nullptr);
+}
+
 void dev_pca(Ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, int method, int64_t l,
              int64_t q, uint64_t seed, bool center, double threshold, double* U, int64_t ldu,
              double* sigma, double* V, int64_t ldv, double* mean, int64_t* rank, int64_t* k,
@@ -102,6 +115,13 @@ void dev_pca(Ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, int met
     RowComm rc{c};
     const RowComm* comm = c->nccl_comm ? &rc : nullptr;
     const int world = comm ? comm->world() : 1;
+    // The reference sampler's Omega (or Lanczos v0) is generated on a host
+    // thread while the device centres A and forms the total variance.
+    if (method == SVDK_RANDOMIZED || method == SVDK_KRYLOV) {
+        if (l >= 1 && l <= n) omega_prefetch(c, n, l, seed);
+    } else if (method == SVDK_LANCZOS) {
+        omega_prefetch(c, n, 1, seed);
+    }
     // global row count
     double mg = static_cast<double>(m);
     if (world > 1) {
@@ -113,9 +133,10 @@ void dev_pca(Ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, int met
     if (static_cast<int64_t>(mg) < n || n == 0)
         fail(SVDK_E_DIM, "fit_pca: needs rows >= cols (tall, RowsAreExamples)");
     const int64_t ldc = round_up(std::max<int64_t>(m, 1), 2);
-    DBuf C;
+    DBuf C, d_total(c, 1);
     const double* X = A;
     int64_t ldx = lda;
+    reset_nonfinite(c);
     if (center) {
         // pca.cpp:37-53: column means over ALL rows, subtract
         C = DBuf(c, static_cast<size_t>(ldc) * n);
@@ -134,7 +155,7 @@ void dev_pca(Ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, int met
     } else {
         fill(c, mean, n, 0.0);
     }
-    *total = frob_sq_rows(c, X, ldx, m, n, comm);  // pca.cpp:57-59
+    frob_sq_rows_dev(c, X, ldx, m, n, d_total.p(), comm);  // pca.cpp:57-59
     int64_t r = 0;
     switch (method) {
         case SVDK_TRUNCATED:
@@ -159,15 +180,15 @@ void dev_pca(Ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, int met
     }
     *rank = r;
     // eigenvalues = sigma^2 (pca.cpp:111-114), then K (pca.cpp:61-89)
-    if (r == 0) {
-        *k = select_components(c, sigma, 0, *total, threshold);  // raises: empty spectrum
-        return;
+    DBuf w(c, std::max<int64_t>(r, 1));
+    if (r > 0) {
+        square_kernel<<<static_cast<unsigned>(ceil_div(r, 256)), 256, 0, c->stream>>>(sigma, r,
+                                                                                      w.p());
+        SVDK_CHECK_LAUNCH();
+        c->launches++;
     }
-    DBuf w(c, r);
-    square_kernel<<<static_cast<unsigned>(ceil_div(r, 256)), 256, 0, c->stream>>>(sigma, r, w.p());
-    SVDK_CHECK_LAUNCH();
-    c->launches++;
-    *k = select_components(c, w.p(), r, *total, threshold);
+    raise_if_nonfinite(c);
+    *k = select_components_dev(c, w.p(), r, d_total.p(), threshold, total);
 }
 
 }  // namespace svdk

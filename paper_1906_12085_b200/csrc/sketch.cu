@@ -10,6 +10,7 @@
 // T = A^T Q, then the small SVD of T through the Gram route. Every product
 // over the row index is a DMMA GEMM followed (row-sharded) by an allreduce.
 #include <algorithm>
+#include <thread>
 #include <vector>
 
 #include "svdk_methods.h"
@@ -19,17 +20,72 @@ void gaussian_fill(int64_t rows, int64_t cols, uint64_t seed, double* out);
 int64_t qr_thin(Ctx* c, const double* H, int64_t ldh, int64_t m, int64_t p, double* Q, int64_t ldq,
                 double* R, const RowComm* comm);
 
-namespace {
+// ---------------------------------------------------------------------------
+// Reference Gaussian sampler staged through pinned memory, asynchronously.
+// ---------------------------------------------------------------------------
+struct HostJob {
+    int64_t rows, cols;
+    uint64_t seed;
+    std::thread th;
+};
 
-// Omega (n x l) from the reference sampler, uploaded through pinned memory.
-void upload_omega(Ctx* c, int64_t n, int64_t l, uint64_t seed, double* dO) {
-    double* h = nullptr;
-    SVDK_CUDA(cudaMallocHost(&h, sizeof(double) * n * l));
-    gaussian_fill(n, l, seed, h);
-    SVDK_CUDA(cudaMemcpyAsync(dO, h, sizeof(double) * n * l, cudaMemcpyHostToDevice, c->stream));
-    SVDK_CUDA(cudaStreamSynchronize(c->stream));
-    cudaFreeHost(h);
+namespace {
+double* staging(Ctx* c, size_t count) {
+    if (!c->pinned_ev) SVDK_CUDA(cudaEventCreateWithFlags(&c->pinned_ev, cudaEventDisableTiming));
+    // the previous H2D out of the buffer must have landed before we refill it
+    SVDK_CUDA(cudaEventSynchronize(c->pinned_ev));
+    if (c->pinned_cap < count) {
+        if (c->pinned) cudaFreeHost(c->pinned);
+        c->pinned = nullptr;
+        c->pinned_cap = 0;
+        SVDK_CUDA(cudaMallocHost(&c->pinned, sizeof(double) * count));
+        c->pinned_cap = count;
+    }
+    return c->pinned;
 }
+
+void join_job(Ctx* c) {
+    if (c->omega_job) {
+        if (c->omega_job->th.joinable()) c->omega_job->th.join();
+        delete c->omega_job;
+        c->omega_job = nullptr;
+    }
+}
+}  // namespace
+
+void omega_prefetch(Ctx* c, int64_t rows, int64_t cols, uint64_t seed) {
+    join_job(c);
+    double* buf = staging(c, static_cast<size_t>(rows) * cols);
+    auto* job = new HostJob{rows, cols, seed, {}};
+    job->th = std::thread([=] { gaussian_fill(rows, cols, seed, buf); });
+    c->omega_job = job;
+}
+
+void omega_upload(Ctx* c, int64_t rows, int64_t cols, uint64_t seed, double* d_out) {
+    const bool ready = c->omega_job && c->omega_job->rows == rows && c->omega_job->cols == cols &&
+                       c->omega_job->seed == seed;
+    if (ready) {
+        join_job(c);
+    } else {
+        join_job(c);
+        gaussian_fill(rows, cols, seed, staging(c, static_cast<size_t>(rows) * cols));
+    }
+    SVDK_CUDA(cudaMemcpyAsync(d_out, c->pinned, sizeof(double) * rows * cols,
+                              cudaMemcpyHostToDevice, c->stream));
+    SVDK_CUDA(cudaEventRecord(c->pinned_ev, c->stream));
+}
+
+void release_host_staging(Ctx* c) {
+    join_job(c);
+    if (c->pinned_ev) cudaEventSynchronize(c->pinned_ev);
+    if (c->pinned) cudaFreeHost(c->pinned);
+    if (c->pinned_ev) cudaEventDestroy(c->pinned_ev);
+    c->pinned = nullptr;
+    c->pinned_cap = 0;
+    c->pinned_ev = nullptr;
+}
+
+namespace {
 
 // Y <- A (A^T Y): one power iteration (svd_methods.cpp:165-167).
 void power_step(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n, const double* Y,
@@ -49,9 +105,7 @@ int64_t finish_sketch(Ctx* c, const double* Q, int64_t ldq, int64_t m, int64_t w
         DBuf iu(c, static_cast<size_t>(ldiu) * w), iv(c, static_cast<size_t>(w) * w);
         const int64_t r = truncated_svd(c, T, n, n, w, iu.p(), ldiu, sigma, iv.p(), w, nullptr);
         if (r == 0) return 0;
-        reset_nonfinite(c);
         gemm(c, false, m, r, w, Q, ldq, iv.p(), w, U, ldu, nullptr, true);  // U = Q inner.v
-        raise_if_nonfinite(c);
         copy_mat(c, iu.p(), ldiu, V, ldv, n, r);                             // V = inner.u
         normalize_signs_uv(c, U, ldu, m, V, ldv, n, r);
         return r;
@@ -63,9 +117,7 @@ int64_t finish_sketch(Ctx* c, const double* Q, int64_t ldq, int64_t m, int64_t w
     DBuf iu(c, static_cast<size_t>(ldt) * n), iv(c, static_cast<size_t>(n) * n);
     const int64_t r = truncated_svd(c, Tt.p(), ldt, w, n, iu.p(), ldt, sigma, iv.p(), n, nullptr);
     if (r == 0) return 0;
-    reset_nonfinite(c);
     gemm(c, false, m, r, w, Q, ldq, iu.p(), ldt, U, ldu, nullptr, true);  // U = Q inner.v
-    raise_if_nonfinite(c);
     copy_mat(c, iv.p(), n, V, ldv, n, r);                                  // V = inner.u
     normalize_signs_uv(c, U, ldu, m, V, ldv, n, r);
     return r;
@@ -77,14 +129,12 @@ int64_t randomized_pca(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t 
     const int64_t ldh = round_up(std::max<int64_t>(m, 1), 2);
     DBuf Om(c, static_cast<size_t>(n) * l), H(c, static_cast<size_t>(ldh) * l),
         H2(c, static_cast<size_t>(ldh) * l), Z(c, static_cast<size_t>(n) * l);
-    upload_omega(c, n, l, seed, Om.p());
-    reset_nonfinite(c);
+    omega_upload(c, n, l, seed, Om.p());
     gemm(c, false, m, l, n, A, lda, Om.p(), n, H.p(), ldh, nullptr, true);  // H = A Omega
     for (int64_t j = 0; j < q; ++j) {
         power_step(c, A, lda, m, n, H.p(), ldh, l, H2.p(), ldh, Z.p(), comm);
         std::swap(H, H2);
     }
-    raise_if_nonfinite(c);
     Om.reset();
     // Q = qr_thin(H).q  (H2 reused as Q)
     qr_thin(c, H.p(), ldh, m, l, H2.p(), ldh, nullptr, comm);
@@ -100,13 +150,11 @@ int64_t krylov_svd(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n, i
     const int64_t ldh = round_up(std::max<int64_t>(m, 1), 2);
     DBuf Om(c, static_cast<size_t>(n) * l), H(c, static_cast<size_t>(ldh) * w),
         Z(c, static_cast<size_t>(n) * std::max(w, l));
-    upload_omega(c, n, l, seed, Om.p());
-    reset_nonfinite(c);
+    omega_upload(c, n, l, seed, Om.p());
     gemm(c, false, m, l, n, A, lda, Om.p(), n, H.p(), ldh, nullptr, true);  // block 0 = A G
     for (int64_t b = 1; b < blocks; ++b)  // block b = A (A^T block b-1)
         power_step(c, A, lda, m, n, H.p() + (b - 1) * l * ldh, ldh, l, H.p() + b * l * ldh, ldh,
                    Z.p(), comm);
-    raise_if_nonfinite(c);
     Om.reset();
     DBuf Q(c, static_cast<size_t>(ldh) * w);
     qr_thin(c, H.p(), ldh, m, w, Q.p(), ldh, nullptr, comm);

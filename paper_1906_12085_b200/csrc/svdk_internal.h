@@ -109,6 +109,12 @@ struct Ctx {
     // multi-GPU (row-sharded) state
     void* nccl_comm = nullptr;
     int rank = 0, world = 1;
+    // pinned host staging for the reference Gaussian sampler (Omega, v0),
+    // filled by an asynchronous host job that overlaps device work
+    struct HostJob* omega_job = nullptr;
+    double* pinned = nullptr;
+    size_t pinned_cap = 0;
+    cudaEvent_t pinned_ev = nullptr;  // last H2D out of `pinned` completed
     // timing
     bool timing = false;
     std::vector<PhaseRecord> records;
@@ -161,6 +167,7 @@ void transpose(Ctx* c, const double* src, int64_t lds, int64_t rows, int64_t col
                int64_t ldd);
 // Sum of squares of an m x n block, deterministic fixed-order reduction.
 double frob_sq(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n);
+void frob_sq_dev(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n, double* d_out);
 // Column means (RowsAreExamples) + subtract in place into dst; returns mean on device.
 void center_rows_are_examples(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n,
                               double* dst, int64_t ldd, double* d_mean);

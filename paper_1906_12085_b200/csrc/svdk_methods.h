@@ -34,6 +34,19 @@ void nccl_unique_id(char out[128]);
 void attach_nccl(Ctx* c, const char id[128], int rank, int world);
 void destroy_comm(Ctx* c);
 
+// Total of squares over all row shards into a device scalar (no host sync).
+void frob_sq_rows_dev(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n, double* d_out,
+                      const RowComm* comm);
+// Reference Gaussian sampler (host, bit-identical) staged through pinned
+// memory. omega_prefetch starts filling it on a host thread so the sample is
+// ready when the first GEMM needs it; omega_upload joins (or generates) and
+// issues the H2D copy on the context stream.
+void omega_prefetch(Ctx* c, int64_t rows, int64_t cols, uint64_t seed);
+void omega_upload(Ctx* c, int64_t rows, int64_t cols, uint64_t seed, double* d_out);
+void release_host_staging(Ctx* c);
+
+// Non-finite GEMM results (kernels.cpp:39-43) set a sticky device flag; the
+// method entry points reset it and raise NumericalError once at the end.
 void raise_if_nonfinite(Ctx* c);
 void reset_nonfinite(Ctx* c);
 // sigma from eigenvalues + numerical rank (svd_methods.cpp:127-135)
