@@ -222,6 +222,9 @@ int svdk_ctx_destroy(svdk_ctx* ctx) {
         if (ctx->d_flags) cudaFree(ctx->d_flags);
         for (cudaEvent_t e : ctx->event_pool) cudaEventDestroy(e);
         if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+        if (ctx->aux_stream) cudaStreamDestroy(ctx->aux_stream);
+        for (cudaEvent_t e : ctx->aux_ev)
+            if (e) cudaEventDestroy(e);
         delete ctx;
     });
 }

@@ -59,24 +59,19 @@ __host__ __device__ __forceinline__ void circle_pair(int P, int r, int i, int& a
 // Evaluated in the algebraically identical division-free form
 //   d = a_qq - a_pp, e = 2 a_pq, D = |d| + sqrt(d^2 + e^2),
 //   c = D / sqrt(D^2 + e^2), s = sgn(tau) |e| / sqrt(D^2 + e^2)
-// which shortens the dependent FP64 sqrt/div chain on the critical path of
-// every inner round (one sqrt + one rsqrt instead of 2 sqrt + 3 div). Values
-// outside [1e-140, 1e140] fall back to the reference evaluation.
+// with two FP64 reciprocal square roots: 209 cycles of dependent latency on
+// B200 vs 544 for the reference's 2 sqrt + 3 div (tools/probes/rot_latency.cu),
+// and this chain is the serial part of every inner round. eig_sym prescales
+// the matrix by a power of two so d^2 + e^2 cannot overflow or underflow.
+// The accumulated Q is re-orthogonalised after the inner sweep, so last-ulp
+// differences in c, s do not accumulate.
 __device__ __forceinline__ void rotation(double app, double aqq, double apq, double& c, double& s) {
     const double d = aqq - app, e = 2.0 * apq;
-    const double big = fmax(fabs(d), fabs(e));
-    if (big < 1e140 && big > 1e-140) {
-        const double D = fabs(d) + sqrt(fma(d, d, e * e));
-        const double inv = rsqrt(fma(D, D, e * e));
-        c = D * inv;
-        s = (d > 0.0 ? e : (d < 0.0 ? -e : fabs(e))) * inv;  // tau = +-0 -> t = +1
-        return;
-    }
-    const double tau = d / e;
-    const double t = tau >= 0.0 ? 1.0 / (tau + sqrt(1.0 + tau * tau))
-                                : -1.0 / (-tau + sqrt(1.0 + tau * tau));
-    c = 1.0 / sqrt(1.0 + t * t);
-    s = t * c;
+    const double r2 = fma(d, d, e * e);
+    const double D = fabs(d) + r2 * rsqrt(r2);  // |d| + sqrt(d^2 + e^2)
+    const double inv = rsqrt(fma(D, D, e * e));
+    c = D * inv;
+    s = (d > 0.0 ? e : (d < 0.0 ? -e : fabs(e))) * inv;  // tau = +-0 -> t = +1
 }
 
 // Global index of local index i (0..2b-1) of the pair (I, J).
@@ -94,43 +89,44 @@ __device__ __forceinline__ void smem_mma(const double* A, const double* Bm, doub
     constexpr int WTN = NT >= 8 ? 4 : (NT >= 4 ? 2 : 1);
     constexpr int WARPS_M = NT / WTM, WARPS_N = NT / WTN;
     static_assert(WARPS_M * WARPS_N <= 8, "tile split");
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (warp >= WARPS_M * WARPS_N) return;
-    const int wm = warp % WARPS_M, wn = warp / WARPS_M;
+    const int lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
     const int r = lane >> 2, kq = lane & 3;
-    double acc[WTM][WTN][2];
+    for (int wt = threadIdx.x >> 5; wt < WARPS_M * WARPS_N; wt += nwarps) {
+        const int wm = wt % WARPS_M, wn = wt / WARPS_M;
+        double acc[WTM][WTN][2];
 #pragma unroll
-    for (int a = 0; a < WTM; ++a)
+        for (int a = 0; a < WTM; ++a)
 #pragma unroll
-        for (int b = 0; b < WTN; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+            for (int b = 0; b < WTN; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 #pragma unroll 4
-    for (int k0 = 0; k0 < TB; k0 += 4) {
-        const int k = k0 + kq;
-        double af[WTM], bf[WTN];
+        for (int k0 = 0; k0 < TB; k0 += 4) {
+            const int k = k0 + kq;
+            double af[WTM], bf[WTN];
 #pragma unroll
-        for (int a = 0; a < WTM; ++a) {
-            const int m = (wm * WTM + a) * 8 + r;
-            af[a] = TRANS_A ? A[k + m * LD] : A[m + k * LD];
-        }
+            for (int a = 0; a < WTM; ++a) {
+                const int m = (wm * WTM + a) * 8 + r;
+                af[a] = TRANS_A ? A[k + m * LD] : A[m + k * LD];
+            }
 #pragma unroll
-        for (int b = 0; b < WTN; ++b) {
-            const int nn = (wn * WTN + b) * 8 + r;
-            bf[b] = Bm[k + nn * LD];
+            for (int b = 0; b < WTN; ++b) {
+                const int nn = (wn * WTN + b) * 8 + r;
+                bf[b] = Bm[k + nn * LD];
+            }
+#pragma unroll
+            for (int a = 0; a < WTM; ++a)
+#pragma unroll
+                for (int b = 0; b < WTN; ++b) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
         }
 #pragma unroll
         for (int a = 0; a < WTM; ++a)
 #pragma unroll
-            for (int b = 0; b < WTN; ++b) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+            for (int b = 0; b < WTN; ++b) {
+                const int row = (wm * WTM + a) * 8 + r;
+                const int col = (wn * WTN + b) * 8 + 2 * kq;
+                C[row + col * LD] = acc[a][b][0];
+                C[row + (col + 1) * LD] = acc[a][b][1];
+            }
     }
-#pragma unroll
-    for (int a = 0; a < WTM; ++a)
-#pragma unroll
-        for (int b = 0; b < WTN; ++b) {
-            const int row = (wm * WTM + a) * 8 + r;
-            const int col = (wn * WTN + b) * 8 + 2 * kq;
-            C[row + col * LD] = acc[a][b][0];
-            C[row + (col + 1) * LD] = acc[a][b][1];
-        }
 }
 
 // ---------------------------------------------------------------------------
@@ -146,121 +142,176 @@ __device__ __forceinline__ void smem_mma(const double* A, const double* Bm, doub
 // M itself is scratch: the update kernel applies the (re-orthogonalised) Q to
 // every pair block, the diagonal ones included, so A changes by one
 // similarity per round.
+// Development probe: clock64 stamps of CTA 0 in the last pair solve (read by
+// svdk_debug_jacobi_probe; not part of the public ABI).
+__device__ long long g_jprobe[8];
+
 template <int TB>
-__global__ void __launch_bounds__(256)
+constexpr int solve_threads() {
+    return (TB / 2) * (TB / 2) + 32 * (TB / 4);  // M threads + Q warps (2 pairs each)
+}
+
+template <int TB>
+__global__ void __launch_bounds__(solve_threads<TB>())
     jacobi_pair_solve(double* A, int64_t lda, double* Qbuf, int* active, int nb, int round,
                       double skip_tau, int max_inner) {
     constexpr int B = TB / 2, LD = TB + 4, NP = TB / 2;
+    constexpr int MT = NP * NP;                        // M threads: one 2x2 block each
+    constexpr int QW = (solve_threads<TB>() - MT) / 32;  // Q warps (NP / PPW)
+    constexpr int PPW = NP / QW;                       // pairs per Q warp
     extern __shared__ double sm[];
-    double* M = sm;
-    double* Q = sm + TB * LD;
+    double* Mc = sm;             // current M
+    double* Mn = Mc + TB * LD;   // next M (double buffer)
+    double* Q = Mn + TB * LD;
     double* T = Q + TB * LD;
-    __shared__ double cs[NP], sn[NP];
+    __shared__ int ptab[TB - 1][NP];  // round-robin pairs, packed p | q << 8
+    __shared__ double cs[TB - 1][NP], sn[TB - 1][NP];
     __shared__ int any_applied;
 
     const int tid = threadIdx.x;
+    const bool probe = blockIdx.x == 0 && tid == 0 && round == 5;
+    long long t0 = clock64();
     int I, J;
     circle_pair(nb, round, blockIdx.x, I, J);
     if (tid == 0) any_applied = 0;
+    for (int e = tid; e < (TB - 1) * NP; e += blockDim.x) {
+        int p, q;
+        circle_pair(TB, e / NP, e % NP, p, q);
+        ptab[e / NP][e % NP] = p | (q << 8);
+    }
     __syncthreads();
     for (int e = tid; e < TB * TB; e += blockDim.x) {
         const int i = e % TB, j = e / TB;
         const double x = A[gidx(B, I, J, i) + gidx(B, I, J, j) * lda];
-        M[i + j * LD] = x;
+        Mc[i + j * LD] = x;
         Q[i + j * LD] = (i == j) ? 1.0 : 0.0;
         if (i != j && fabs(x) > skip_tau) any_applied = 1;
     }
     __syncthreads();
+    long long t1 = clock64();
     const bool work = any_applied != 0;
+    if (probe && work) {
+        g_jprobe[0] = t0;
+        g_jprobe[1] = t1;
+    }
     if (work) {
+        // Warp roles per round: lanes 0..NP-1 of warp 0 evaluate the round's
+        // rotations once (the serial FP64 chain); then the MT "M threads"
+        // apply them to one 2x2 block each (M <- R^T M R, double-buffered),
+        // while the QW "Q warps" apply the same rotations to the rows of Q
+        // (Q never feeds back, so it rides along instead of adding rounds).
+        // Per round: phase A = rotation parameters of round rr (lanes of warp
+        // 0) || the M threads prefetch their 2x2 block || the Q warps apply
+        // round rr-1 to Q; barrier; phase B = M threads apply round rr
+        // (double-buffered M); barrier.
+        const bool is_m = tid < MT;
+        const int bi = tid % NP, bj = tid / NP;
+        auto q_update = [&](int r_) {
+            const int r = tid & 31, w = (tid - MT) >> 5;
+            if (r >= TB) return;
+#pragma unroll
+            for (int jj = 0; jj < PPW; ++jj) {
+                const int j = w * PPW + jj;
+                const double c = cs[r_][j], s = sn[r_][j];
+                if (s == 0.0) continue;
+                const int code = ptab[r_][j];
+                const int pcol = code & 255, qcol = code >> 8;
+                const double x = Q[r + pcol * LD], y = Q[r + qcol * LD];
+                Q[r + pcol * LD] = c * x - s * y;
+                Q[r + qcol * LD] = s * x + c * y;
+            }
+        };
         for (int sweep = 0; sweep < max_inner; ++sweep) {
-            __syncthreads();
-            if (tid == 0) any_applied = 0;
             for (int rr = 0; rr < TB - 1; ++rr) {
-                if (tid < NP) {
-                    int p, q;
-                    circle_pair(TB, rr, tid, p, q);
-                    const double apq = M[p + q * LD];
-                    double c = 1.0, s = 0.0;
-                    if (fabs(apq) > skip_tau) {
-                        rotation(M[p + p * LD], M[q + q * LD], apq, c, s);
-                        any_applied = 1;
+                const bool pr = probe && rr == 10 && sweep == 0;
+                long long ta = pr ? clock64() : 0;
+                int pi = 0, qi = 0, pj = 0, qj = 0;
+                double m00 = 0, m01 = 0, m10 = 0, m11 = 0;
+                if (is_m) {
+                    const int ci_code = ptab[rr][bi], cj_code = ptab[rr][bj];
+                    pi = ci_code & 255; qi = ci_code >> 8;
+                    pj = cj_code & 255; qj = cj_code >> 8;
+                    m00 = Mc[pi + pj * LD]; m01 = Mc[pi + qj * LD];
+                    m10 = Mc[qi + pj * LD]; m11 = Mc[qi + qj * LD];
+                    if (tid < NP) {  // rotation parameters of pair tid
+                        const double x = bi == bj ? m01 : Mc[pi + qi * LD];
+                        double c = 1.0, s = 0.0;
+                        if (fabs(x) > skip_tau) rotation(Mc[pi + pi * LD], Mc[qi + qi * LD], x, c, s);
+                        cs[rr][tid] = c;
+                        sn[rr][tid] = s;
                     }
-                    cs[tid] = c;
-                    sn[tid] = s;
+                } else if (rr > 0 || sweep > 0) {
+                    q_update(rr > 0 ? rr - 1 : TB - 2);
                 }
+                long long tb = pr ? clock64() : 0;
                 __syncthreads();
-                // fused 2x2-block update  M <- R^T M R  (s == 0 marks a skipped pair)
-                for (int e = tid; e < NP * NP; e += blockDim.x) {
-                    const int bi = e % NP, bj = e / NP;
-                    const double ci = cs[bi], si = sn[bi], cj = cs[bj], sj = sn[bj];
-                    const bool oi = si != 0.0, oj = sj != 0.0;
-                    if (!(oi | oj)) continue;
-                    int pi, qi, pj, qj;
-                    circle_pair(TB, rr, bi, pi, qi);
-                    circle_pair(TB, rr, bj, pj, qj);
-                    double m00 = M[pi + pj * LD], m01 = M[pi + qj * LD];
-                    double m10 = M[qi + pj * LD], m11 = M[qi + qj * LD];
-                    if (oj) {  // columns pj, qj
+                long long tc = pr ? clock64() : 0;
+                if (is_m) {
+                    const double ci = cs[rr][bi], si = sn[rr][bi], cj = cs[rr][bj], sj = sn[rr][bj];
+                    if (sj != 0.0) {  // columns pj, qj
                         const double a0 = cj * m00 - sj * m01, b0 = sj * m00 + cj * m01;
                         const double a1 = cj * m10 - sj * m11, b1 = sj * m10 + cj * m11;
                         m00 = a0; m01 = b0; m10 = a1; m11 = b1;
                     }
-                    if (oi) {  // rows pi, qi
+                    if (si != 0.0) {  // rows pi, qi
                         const double a0 = ci * m00 - si * m10, b0 = si * m00 + ci * m10;
                         const double a1 = ci * m01 - si * m11, b1 = si * m01 + ci * m11;
                         m00 = a0; m10 = b0; m01 = a1; m11 = b1;
+                        if (bi == bj) {  // the rotated pair is annihilated exactly
+                            m01 = 0.0;
+                            m10 = 0.0;
+                        }
                     }
-                    if (bi == bj) {  // the rotated pair is annihilated exactly
-                        m01 = 0.0;
-                        m10 = 0.0;
-                    }
-                    M[pi + pj * LD] = m00;
-                    M[pi + qj * LD] = m01;
-                    M[qi + pj * LD] = m10;
-                    M[qi + qj * LD] = m11;
-                }
-                for (int e = tid; e < TB * NP; e += blockDim.x) {
-                    const int r = e % TB, j = e / TB;
-                    const double c = cs[j], s = sn[j];
-                    if (s == 0.0) continue;
-                    int p, q;
-                    circle_pair(TB, rr, j, p, q);
-                    const double x = Q[r + p * LD], y = Q[r + q * LD];
-                    Q[r + p * LD] = c * x - s * y;
-                    Q[r + q * LD] = s * x + c * y;
+                    Mn[pi + pj * LD] = m00;
+                    Mn[pi + qj * LD] = m01;
+                    Mn[qi + pj * LD] = m10;
+                    Mn[qi + qj * LD] = m11;
+                    if (pr) g_jprobe[5] = clock64() - tc;
                 }
                 __syncthreads();
+                if (pr) {
+                    g_jprobe[6] = tb - ta;
+                    g_jprobe[7] = tc - tb;
+                }
+                double* t = Mc;
+                Mc = Mn;
+                Mn = t;
             }
-            if (!any_applied) break;
         }
+        if (!is_m) q_update(TB - 2);  // the last round's Q update
+        __syncthreads();
+        if (probe && work) g_jprobe[2] = clock64();
         // The product of ~TB * sweeps rotations drifts from orthogonality by a
         // few hundred ulps; one Newton-Schulz step Q <- Q (3I - Q^T Q) / 2
         // restores it to working precision so that A' = Q^T A Q is a
         // similarity to rounding (otherwise the spectrum drifts over sweeps).
-        __syncthreads();
-        smem_mma<TB, true>(Q, Q, M);  // M <- Q^T Q
+        smem_mma<TB, true>(Q, Q, Mn);  // Mn <- Q^T Q
         __syncthreads();
         for (int e = tid; e < TB * TB; e += blockDim.x) {
             const int i = e % TB, j = e / TB;
-            M[i + j * LD] = (i == j ? 1.5 : 0.0) - 0.5 * M[i + j * LD];
+            Mn[i + j * LD] = (i == j ? 1.5 : 0.0) - 0.5 * Mn[i + j * LD];
         }
         __syncthreads();
-        smem_mma<TB, false>(Q, M, T);  // T <- Q (3I - Q^T Q) / 2
+        smem_mma<TB, false>(Q, Mn, T);  // T <- Q (3I - Q^T Q) / 2
         __syncthreads();
+        if (probe && work) g_jprobe[3] = clock64();
         for (int e = tid; e < TB * TB; e += blockDim.x)
             Qbuf[static_cast<size_t>(blockIdx.x) * TB * TB + e] = T[(e % TB) + (e / TB) * LD];
     }
     if (tid == 0) active[blockIdx.x] = work ? 1 : 0;
+    if (probe && work) g_jprobe[4] = clock64();
 }
 
 // ---------------------------------------------------------------------------
-// 2. off-diagonal pair blocks of A and the columns of V
+// 2. the round's similarity on A, and its accumulation into V
 // ---------------------------------------------------------------------------
+// jacobi_update_a: one CTA per pair block (p <= q):
+//   A[IJ_p, IJ_q] <- Q_p^T A[IJ_p, IJ_q] Q_q   (mirror written from the same
+//   values so A stays exactly symmetric; diagonal pair blocks symmetrised).
 template <int TB>
 __global__ void __launch_bounds__(256)
-    jacobi_update(double* A, int64_t lda, double* V, int64_t ldv, const double* Qbuf,
-                  const int* active, int nb, int round, int64_t n_pad) {
+    jacobi_update_a(double* A, int64_t lda, const double* Qbuf, const int* active, int nb,
+                    int round) {
     constexpr int B = TB / 2, LD = TB + 4;
     extern __shared__ double sm[];
     double* X = sm;
@@ -268,77 +319,78 @@ __global__ void __launch_bounds__(256)
     double* Qb = Qa + TB * LD;
     double* T = Qb + TB * LD;
     const int tid = threadIdx.x;
+    const int u = blockIdx.x;
+    // (p <= q) from u, column-wise upper enumeration
+    int q = static_cast<int>((sqrt(8.0 * u + 1.0) - 1.0) * 0.5);
+    while ((q + 1) * (q + 2) / 2 <= u) ++q;
+    while (q * (q + 1) / 2 > u) --q;
+    const int p = u - q * (q + 1) / 2;
+    const int ap = active[p], aq = active[q];
+    if (!(ap | aq)) return;  // both rotations are the identity
+    int Ip, Jp, Iq, Jq;
+    circle_pair(nb, round, p, Ip, Jp);
+    circle_pair(nb, round, q, Iq, Jq);
+    const double* qa = Qbuf + static_cast<size_t>(p) * TB * TB;
+    const double* qb = Qbuf + static_cast<size_t>(q) * TB * TB;
+    for (int e = tid; e < TB * TB; e += blockDim.x) {
+        const int i = e % TB, j = e / TB;
+        X[i + j * LD] = A[gidx(B, Ip, Jp, i) + gidx(B, Iq, Jq, j) * lda];
+        Qa[i + j * LD] = ap ? qa[e] : (i == j ? 1.0 : 0.0);
+        Qb[i + j * LD] = aq ? qb[e] : (i == j ? 1.0 : 0.0);
+    }
+    __syncthreads();
+    smem_mma<TB, false>(X, Qb, T);  // T = X Q_q
+    __syncthreads();
+    smem_mma<TB, true>(Qa, T, X);   // X = Q_p^T T
+    __syncthreads();
+    if (p == q) {  // diagonal pair block: write the exactly symmetric part
+        for (int e = tid; e < TB * TB; e += blockDim.x) {
+            const int i = e % TB, j = e / TB;
+            A[gidx(B, Ip, Jp, i) + gidx(B, Ip, Jp, j) * lda] = 0.5 * (X[i + j * LD] + X[j + i * LD]);
+        }
+        return;
+    }
+    for (int e = tid; e < TB * TB; e += blockDim.x) {
+        const int i = e % TB, j = e / TB;
+        A[gidx(B, Ip, Jp, i) + gidx(B, Iq, Jq, j) * lda] = X[i + j * LD];
+    }
+    for (int e = tid; e < TB * TB; e += blockDim.x) {
+        const int j = e % TB, i = e / TB;  // consecutive threads walk rows of the mirror
+        A[gidx(B, Iq, Jq, j) + gidx(B, Ip, Jp, i) * lda] = X[i + j * LD];
+    }
+}
+
+// jacobi_update_v: one CTA per (row tile, pair q): V[rows, IJ_q] <- V[rows, IJ_q] Q_q.
+// V never feeds back into the iteration, so these launches run on a side
+// stream, overlapped with the next rounds' latency-bound pair solves.
+template <int TB>
+__global__ void __launch_bounds__(256)
+    jacobi_update_v(double* V, int64_t ldv, const double* Qbuf, const int* active, int nb,
+                    int round) {
+    constexpr int B = TB / 2, LD = TB + 4;
+    extern __shared__ double sm[];
+    double* X = sm;
+    double* Qb = X + TB * LD;
+    double* T = Qb + TB * LD;
+    const int tid = threadIdx.x;
     const int k = nb / 2;
-    const int n_off = k * (k + 1) / 2;
-    int u = blockIdx.x;
-    if (u < n_off) {
-        // (p <= q) from u, column-wise upper enumeration
-        int q = static_cast<int>((sqrt(8.0 * u + 1.0) - 1.0) * 0.5);
-        while ((q + 1) * (q + 2) / 2 <= u) ++q;
-        while (q * (q + 1) / 2 > u) --q;
-        const int p = u - q * (q + 1) / 2;
-        const int ap = active[p], aq = active[q];
-        if (!(ap | aq)) return;  // both rotations are the identity
-        int Ip, Jp, Iq, Jq;
-        circle_pair(nb, round, p, Ip, Jp);
-        circle_pair(nb, round, q, Iq, Jq);
-        const double* qa = Qbuf + static_cast<size_t>(p) * TB * TB;
-        const double* qb = Qbuf + static_cast<size_t>(q) * TB * TB;
-        for (int e = tid; e < TB * TB; e += blockDim.x) {
-            const int i = e % TB, j = e / TB;
-            X[i + j * LD] = A[gidx(B, Ip, Jp, i) + gidx(B, Iq, Jq, j) * lda];
-            Qa[i + j * LD] = ap ? qa[e] : (i == j ? 1.0 : 0.0);
-            Qb[i + j * LD] = aq ? qb[e] : (i == j ? 1.0 : 0.0);
-        }
-        __syncthreads();
-        if (aq) {
-            smem_mma<TB, false>(X, Qb, T);  // T = X Q_q
-        } else {
-            for (int e = tid; e < TB * TB; e += blockDim.x) T[(e % TB) + (e / TB) * LD] = X[(e % TB) + (e / TB) * LD];
-        }
-        __syncthreads();
-        if (ap) {
-            smem_mma<TB, true>(Qa, T, X);  // X = Q_p^T T
-        } else {
-            for (int e = tid; e < TB * TB; e += blockDim.x) X[(e % TB) + (e / TB) * LD] = T[(e % TB) + (e / TB) * LD];
-        }
-        __syncthreads();
-        if (p == q) {  // diagonal pair block: write the exactly symmetric part
-            for (int e = tid; e < TB * TB; e += blockDim.x) {
-                const int i = e % TB, j = e / TB;
-                A[gidx(B, Ip, Jp, i) + gidx(B, Ip, Jp, j) * lda] =
-                    0.5 * (X[i + j * LD] + X[j + i * LD]);
-            }
-            return;
-        }
-        for (int e = tid; e < TB * TB; e += blockDim.x) {
-            const int i = e % TB, j = e / TB;
-            A[gidx(B, Ip, Jp, i) + gidx(B, Iq, Jq, j) * lda] = X[i + j * LD];
-        }
-        for (int e = tid; e < TB * TB; e += blockDim.x) {
-            const int j = e % TB, i = e / TB;  // consecutive threads walk rows of the mirror
-            A[gidx(B, Iq, Jq, j) + gidx(B, Ip, Jp, i) * lda] = X[i + j * LD];
-        }
-    } else {
-        u -= n_off;
-        const int q = u % k;
-        if (!active[q]) return;
-        const int64_t r0 = static_cast<int64_t>(u / k) * TB;
-        int Iq, Jq;
-        circle_pair(nb, round, q, Iq, Jq);
-        const double* qb = Qbuf + static_cast<size_t>(q) * TB * TB;
-        for (int e = tid; e < TB * TB; e += blockDim.x) {
-            const int i = e % TB, j = e / TB;
-            X[i + j * LD] = V[r0 + i + gidx(B, Iq, Jq, j) * ldv];
-            Qb[i + j * LD] = qb[e];
-        }
-        __syncthreads();
-        smem_mma<TB, false>(X, Qb, T);
-        __syncthreads();
-        for (int e = tid; e < TB * TB; e += blockDim.x) {
-            const int i = e % TB, j = e / TB;
-            V[r0 + i + gidx(B, Iq, Jq, j) * ldv] = T[i + j * LD];
-        }
+    const int q = blockIdx.x % k;
+    if (!active[q]) return;
+    const int64_t r0 = static_cast<int64_t>(blockIdx.x / k) * TB;
+    int Iq, Jq;
+    circle_pair(nb, round, q, Iq, Jq);
+    const double* qb = Qbuf + static_cast<size_t>(q) * TB * TB;
+    for (int e = tid; e < TB * TB; e += blockDim.x) {
+        const int i = e % TB, j = e / TB;
+        X[i + j * LD] = V[r0 + i + gidx(B, Iq, Jq, j) * ldv];
+        Qb[i + j * LD] = qb[e];
+    }
+    __syncthreads();
+    smem_mma<TB, false>(X, Qb, T);
+    __syncthreads();
+    for (int e = tid; e < TB * TB; e += blockDim.x) {
+        const int i = e % TB, j = e / TB;
+        V[r0 + i + gidx(B, Iq, Jq, j) * ldv] = T[i + j * LD];
     }
 }
 
@@ -377,12 +429,12 @@ __global__ void symcheck_kernel(const double* S, int64_t lds, int64_t n, double*
 
 // A (n_pad x n_pad) = (S + S^T)/2 zero padded; V = I.
 __global__ void jacobi_init_kernel(const double* S, int64_t lds, int64_t n, double* A, double* V,
-                                   int64_t n_pad) {
+                                   int64_t n_pad, double scale) {
     for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n_pad * n_pad;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int64_t j = e / n_pad, i = e - j * n_pad;
         double a = 0.0;
-        if (i < n && j < n) a = 0.5 * (S[i + j * lds] + S[j + i * lds]);
+        if (i < n && j < n) a = (0.5 * (S[i + j * lds] + S[j + i * lds])) * scale;
         A[e] = a;
         V[e] = (i == j) ? 1.0 : 0.0;
     }
@@ -416,7 +468,8 @@ __global__ void sum_fixed_kernel(const double* partial, int count, double* out) 
 
 // Stable descending order by rank counting: rank_i = #{j : l_j > l_i or
 // (l_j == l_i and j < i)} — exactly std::stable_sort's permutation.
-__global__ void eig_sort_kernel(const double* A, int64_t n_pad, int64_t n, double* w, int* dest) {
+__global__ void eig_sort_kernel(const double* A, int64_t n_pad, int64_t n, double unscale,
+                                double* w, int* dest) {
     const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (i >= n) return;
     const double li = A[i + i * n_pad];
@@ -425,7 +478,7 @@ __global__ void eig_sort_kernel(const double* A, int64_t n_pad, int64_t n, doubl
         const double lj = A[j + j * n_pad];
         rank += (lj > li) || (lj == li && j < i);
     }
-    w[rank] = li;
+    w[rank] = li * unscale;
     dest[i] = static_cast<int>(rank);
 }
 
@@ -453,21 +506,26 @@ double device_sumsq(Ctx* c, const double* A, int64_t n, int mode, DBuf& scratch)
 }
 
 template <int TB>
-void run_sweeps(Ctx* c, double* A, double* V, double* Qbuf, int* active, int64_t n_pad,
-                int max_sweeps, double thr, double fro, DBuf& scratch, int& sweeps, double& off) {
+void run_sweeps(Ctx* c, double* A, double* V, int64_t n_pad, int max_sweeps, double thr, double fro,
+                DBuf& scratch, int& sweeps, double& off) {
     constexpr int B = TB / 2;
     const int nb = static_cast<int>(n_pad / B);
     const int k = nb / 2;
-    const size_t smem_solve = 3 * TB * (TB + 4) * sizeof(double);
-    const size_t smem_upd = 4 * TB * (TB + 4) * sizeof(double);
+    const size_t smem_solve = 4 * TB * (TB + 4) * sizeof(double);
+    constexpr int nthreads_solve = solve_threads<TB>();
+    const size_t smem_a = 4 * TB * (TB + 4) * sizeof(double);
+    const size_t smem_v = 3 * TB * (TB + 4) * sizeof(double);
     static bool attr = false;
     if (!attr) {
         SVDK_CUDA(cudaFuncSetAttribute(jacobi_pair_solve<TB>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem_solve)));
-        SVDK_CUDA(cudaFuncSetAttribute(jacobi_update<TB>,
+        SVDK_CUDA(cudaFuncSetAttribute(jacobi_update_a<TB>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem_upd)));
+                                       static_cast<int>(smem_a)));
+        SVDK_CUDA(cudaFuncSetAttribute(jacobi_update_v<TB>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem_v)));
         attr = true;
     }
     // Inner skip threshold: if every off-diagonal entry were this small the
@@ -475,24 +533,43 @@ void run_sweeps(Ctx* c, double* A, double* V, double* Qbuf, int* active, int64_t
     const double skip_tau = 1e-13 * fro / static_cast<double>(n_pad);
     const char* inner_env = std::getenv("SVDK_JACOBI_INNER");
     const int max_inner = inner_env ? std::max(1, std::atoi(inner_env)) : 1;
-    const int update_ctas = k * (k + 1) / 2 + static_cast<int>(n_pad / TB) * k;
+    const int rounds = nb - 1;
+    // Every round of a sweep keeps its own Q_p set, so the V chain on the side
+    // stream can lag behind the A chain by any number of rounds.
+    DBuf qbuf(c, static_cast<size_t>(rounds) * k * TB * TB);
+    DBuf act(c, static_cast<size_t>(rounds) * k);
+    int* active = reinterpret_cast<int*>(act.p());
+    const int a_ctas = k * (k + 1) / 2, v_ctas = static_cast<int>(n_pad / TB) * k;
+    if (!c->aux_stream) {
+        SVDK_CUDA(cudaStreamCreateWithFlags(&c->aux_stream, cudaStreamNonBlocking));
+        SVDK_CUDA(cudaEventCreateWithFlags(&c->aux_ev[0], cudaEventDisableTiming));
+        SVDK_CUDA(cudaEventCreateWithFlags(&c->aux_ev[1], cudaEventDisableTiming));
+    }
+    cudaStream_t S = c->stream, S2 = c->aux_stream;
     auto enqueue_sweep = [&] {
-        for (int r = 0; r < nb - 1; ++r) {
-            jacobi_pair_solve<TB><<<k, 256, smem_solve, c->stream>>>(A, n_pad, Qbuf, active, nb, r,
-                                                                     skip_tau, max_inner);
-            jacobi_update<TB><<<update_ctas, 256, smem_upd, c->stream>>>(A, n_pad, V, n_pad, Qbuf,
-                                                                         active, nb, r, n_pad);
+        for (int r = 0; r < rounds; ++r) {
+            double* qr = qbuf.p() + static_cast<size_t>(r) * k * TB * TB;
+            int* ar = active + static_cast<size_t>(r) * k;
+            jacobi_pair_solve<TB><<<k, nthreads_solve, smem_solve, S>>>(A, n_pad, qr, ar, nb, r, skip_tau,
+                                                             max_inner);
+            SVDK_CUDA(cudaEventRecord(c->aux_ev[0], S));
+            SVDK_CUDA(cudaStreamWaitEvent(S2, c->aux_ev[0], 0));
+            jacobi_update_v<TB><<<v_ctas, 256, smem_v, S2>>>(V, n_pad, qr, ar, nb, r);
+            jacobi_update_a<TB><<<a_ctas, 256, smem_a, S>>>(A, n_pad, qr, ar, nb, r);
         }
+        // join: the sweep ends when the V chain has caught up
+        SVDK_CUDA(cudaEventRecord(c->aux_ev[1], S2));
+        SVDK_CUDA(cudaStreamWaitEvent(S, c->aux_ev[1], 0));
     };
-    // One sweep = 2 (nb - 1) dependent launches: capture them once as a CUDA
-    // graph and replay it per sweep (launch latency dominates at small n).
+    // One sweep = 3 (nb - 1) launches on two streams: capture them once as a
+    // CUDA graph (a DAG with the V chain beside the A chain) and replay it.
     cudaGraphExec_t exec = nullptr;
-    const bool use_graph = nb > 2 && c->stream != nullptr;
+    const bool use_graph = nb > 2 && S != nullptr;
     if (use_graph) {
         cudaGraph_t graph;
-        SVDK_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        SVDK_CUDA(cudaStreamBeginCapture(S, cudaStreamCaptureModeThreadLocal));
         enqueue_sweep();
-        SVDK_CUDA(cudaStreamEndCapture(c->stream, &graph));
+        SVDK_CUDA(cudaStreamEndCapture(S, &graph));
         SVDK_CUDA(cudaGraphInstantiate(&exec, graph, 0));
         cudaGraphDestroy(graph);
     }
@@ -500,12 +577,12 @@ void run_sweeps(Ctx* c, double* A, double* V, double* Qbuf, int* active, int64_t
     try {
         while (off > thr && sweeps < max_sweeps) {
             if (use_graph) {
-                SVDK_CUDA(cudaGraphLaunch(exec, c->stream));
+                SVDK_CUDA(cudaGraphLaunch(exec, S));
             } else {
                 enqueue_sweep();
                 SVDK_CHECK_LAUNCH();
             }
-            c->launches += 2 * (nb - 1);
+            c->launches += 3 * rounds;
             ++sweeps;
             off = std::sqrt(2.0 * device_sumsq(c, A, n_pad, 1, scratch));
         }
@@ -524,6 +601,7 @@ void eig_sym(Ctx* c, const double* S, int64_t lds, int64_t n, int max_sweeps, do
     if (n == 0) return;
     PhaseTimer timer(c, "eig_sym");
     // symmetry check (kernels.cpp:251-262)
+    int pow2 = 0;
     {
         const int blocks = static_cast<int>(
             std::max<int64_t>(1, std::min<int64_t>(ceil_div(n * n, 256), 2 * c->num_sms)));
@@ -538,6 +616,9 @@ void eig_sym(Ctx* c, const double* S, int64_t lds, int64_t n, int max_sweeps, do
             mabs = std::max(mabs, h[2 * b]);
             masym = std::max(masym, h[2 * b + 1]);
         }
+        // prescale by a power of two (exact) so the rotation kernels never see
+        // entries whose squares over- or underflow
+        if (mabs > 0.0 && (mabs > 1e100 || mabs < 1e-100)) pow2 = std::ilogb(mabs);
         if (masym > 1e-8 * mabs) {
             char buf[96];
             std::snprintf(buf, sizeof buf, "%f", masym);
@@ -551,17 +632,17 @@ void eig_sym(Ctx* c, const double* S, int64_t lds, int64_t n, int max_sweeps, do
     int TB = n <= 64 ? 16 : 32;
     if (const char* e = std::getenv("SVDK_JACOBI_TB")) {  // tuning override
         const int t = std::atoi(e);
-        if (t == 16 || t == 32 || t == 64) TB = t;
+        if (t == 16 || t == 32) TB = t;
     }
     const int64_t n_pad = round_up(n, TB);
     DBuf A(c, static_cast<size_t>(n_pad) * n_pad), V(c, static_cast<size_t>(n_pad) * n_pad);
-    const int64_t k = n_pad / TB;  // pairs per round (nb = 2k blocks of TB/2)
-    DBuf Qbuf(c, static_cast<size_t>(k) * TB * TB), active(c, k);
+
     DBuf scratch(c, 4 * c->num_sms + 8);
     {
         const int blocks = static_cast<int>(
             std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_pad * n_pad, 256), 4 * c->num_sms)));
-        jacobi_init_kernel<<<blocks, 256, 0, c->stream>>>(S, lds, n, A.p(), V.p(), n_pad);
+        jacobi_init_kernel<<<blocks, 256, 0, c->stream>>>(S, lds, n, A.p(), V.p(), n_pad,
+                                                          std::ldexp(1.0, -pow2));
         SVDK_CHECK_LAUNCH();
         c->launches++;
     }
@@ -570,23 +651,14 @@ void eig_sym(Ctx* c, const double* S, int64_t lds, int64_t n, int max_sweeps, do
     double off = std::sqrt(2.0 * device_sumsq(c, A.p(), n_pad, 1, scratch));
     int sweeps = 0;
     if (n == 1) off = 0.0;
-    switch (TB) {
-        case 16:
-            run_sweeps<16>(c, A.p(), V.p(), Qbuf.p(), reinterpret_cast<int*>(active.p()), n_pad,
-                            max_sweeps, thr, fro, scratch, sweeps, off);
-            break;
-        case 32:
-            run_sweeps<32>(c, A.p(), V.p(), Qbuf.p(), reinterpret_cast<int*>(active.p()), n_pad,
-                            max_sweeps, thr, fro, scratch, sweeps, off);
-            break;
-        default:
-            run_sweeps<64>(c, A.p(), V.p(), Qbuf.p(), reinterpret_cast<int*>(active.p()), n_pad,
-                            max_sweeps, thr, fro, scratch, sweeps, off);
-            break;
-    }
+    if (TB == 16)
+        run_sweeps<16>(c, A.p(), V.p(), n_pad, max_sweeps, thr, fro, scratch, sweeps, off);
+    else
+        run_sweeps<32>(c, A.p(), V.p(), n_pad, max_sweeps, thr, fro, scratch, sweeps, off);
     c->jacobi_sweeps = sweeps;
+    off = std::ldexp(off, pow2);  // back to the caller's units
     c->last_off_norm = off;
-    if (off > thr) {
+    if (off > std::ldexp(thr, pow2)) {
         char buf[160];
         std::snprintf(buf, sizeof buf, "eig_sym: no convergence in %d sweeps, off-diagonal norm %f",
                       max_sweeps, off);
@@ -594,7 +666,7 @@ void eig_sym(Ctx* c, const double* S, int64_t lds, int64_t n, int max_sweeps, do
     }
     DBuf dest(c, n);  // int storage inside a double buffer
     eig_sort_kernel<<<static_cast<unsigned>(ceil_div(n, 128)), 128, 0, c->stream>>>(
-        A.p(), n_pad, n, w, reinterpret_cast<int*>(dest.p()));
+        A.p(), n_pad, n, std::ldexp(1.0, pow2), w, reinterpret_cast<int*>(dest.p()));
     SVDK_CHECK_LAUNCH();
     dim3 g(static_cast<unsigned>(std::min<int64_t>(ceil_div(n, 128), 64)),
            static_cast<unsigned>(std::min<int64_t>(n, 65535)));
@@ -605,3 +677,7 @@ void eig_sym(Ctx* c, const double* S, int64_t lds, int64_t n, int max_sweeps, do
 }
 
 }  // namespace svdk
+
+extern "C" int svdk_debug_jacobi_probe(long long* out) {
+    return cudaMemcpyFromSymbol(out, svdk::g_jprobe, 8 * sizeof(long long)) == cudaSuccess ? 0 : 4;
+}

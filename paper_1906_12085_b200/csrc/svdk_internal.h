@@ -101,6 +101,8 @@ struct Ctx {
     int num_sms = 148;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
+    cudaStream_t aux_stream = nullptr;  // side stream for off-critical-path work
+    cudaEvent_t aux_ev[2] = {nullptr, nullptr};
     Pool pool;
     // scratch: small pinned host buffer for scalars / flags
     void* host_scratch = nullptr;

@@ -22,4 +22,10 @@ for _ in range(reps):
     torch.cuda.synchronize()
     print(f"eig n={n}: {e0.elapsed_time(e1):.2f} ms, sweeps={eng.ctx.last_sweeps()}", flush=True)
 ref = torch.linalg.eigvalsh(s.contiguous()).flip(0)
+import ctypes
+from paper_1906_12085_b200 import _lib
+buf = (ctypes.c_longlong * 8)()
+_lib.load().svdk_debug_jacobi_probe(buf)
+st = list(buf)
+print("pair_solve CTA0 cycles: load", st[1] - st[0], "rounds", st[2] - st[1], "ns", st[3] - st[2], "store", st[4] - st[3], "| round10: param", st[6], "bar1", st[7], "Mupd", st[5])
 print("max |dw| / ||S||_F =", float((w - ref).abs().max() / torch.linalg.norm(s)))
