@@ -136,6 +136,10 @@ int svdk_fit_pca(svdk_ctx* ctx, const double* data, int64_t m, int64_t n, int or
                  int method, int64_t l, int64_t q, uint64_t seed, int center, double* basis,
                  double* eigenvalues, double* total, double* mean, int64_t* rank);
 
+/* pca.cpp:133-168  delta = ||A - U diag(sigma) V^T||_F / ||A||_F ; u m x r, v n x r */
+int svdk_residual_delta(svdk_ctx* ctx, const double* a, int64_t m, int64_t n, const double* u,
+                        const double* sigma, const double* v, int64_t r, double* delta);
+
 /* ---- device-pointer entry points (inputs already resident in HBM) ---- */
 int svdk_dev_gemm(svdk_ctx* ctx, int transa, int64_t m, int64_t n, int64_t k, const double* a,
                   int64_t lda, const double* b, int64_t ldb, double* c, int64_t ldc);

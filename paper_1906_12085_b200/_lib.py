@@ -56,6 +56,7 @@ SIGNATURES = {
     "svdk_select_components": (C.c_int, [_ctxp, _vp, _i64, C.c_double, C.c_double, _ip64]),
     "svdk_fit_pca": (C.c_int, [_ctxp, _vp, _i64, _i64, C.c_int, C.c_int, _i64, _i64, _u64, C.c_int,
                                _vp, _vp, _dp, _vp, _ip64]),
+    "svdk_residual_delta": (C.c_int, [_ctxp, _vp, _i64, _i64, _vp, _vp, _vp, _i64, _dp]),
     "svdk_dev_gemm": (C.c_int, [_ctxp, C.c_int, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64]),
     "svdk_dev_gram": (C.c_int, [_ctxp, _vp, _i64, _i64, _i64, _vp, _i64]),
     "svdk_dev_eig_sym": (C.c_int, [_ctxp, _vp, _i64, _i64, C.c_int, _vp, _vp, _i64]),

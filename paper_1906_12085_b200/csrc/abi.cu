@@ -3,6 +3,7 @@
 // Every entry point validates like the reference function it replaces
 // (file:line in svdk.h), converts engine failures into status codes, and
 // keeps the message / residual in thread-local storage.
+#include <cmath>
 #include <cstring>
 #include <new>
 #include <string>
@@ -546,6 +547,29 @@ int svdk_fit_pca(svdk_ctx* c, const double* data, int64_t m, int64_t n, int orie
         for (int64_t i = 0; i < r; ++i) eigenvalues[i] = s[i] * s[i];
         download(c, mean, dM.p(), nm, nm, 1);
         *rank = r;
+    });
+}
+
+int svdk_residual_delta(svdk_ctx* c, const double* a, int64_t m, int64_t n, const double* u,
+                        const double* sigma, const double* v, int64_t r, double* delta) {
+    return guarded([&] {
+        need_ctx(c);
+        // pca.cpp:133-168: ||A - U diag(sigma) V^T||_F / ||A||_F
+        int64_t lda, ldu, ldv;
+        DBuf dA = upload(c, a, m, n, lda);
+        const double norm_sq = frob_sq(c, dA.p(), lda, m, n);
+        if (norm_sq == 0.0) fail(SVDK_E_PARAM, "residual_delta: ||A||_F = 0, ratio undefined");
+        if (r > 0) {
+            DBuf dU = upload(c, u, m, r, ldu), dV = upload(c, v, n, r, ldv);
+            DBuf dS(c, r), W(c, static_cast<size_t>(round_up(r, 2)) * n);
+            h2d(c, dS.p(), sigma, r);
+            // W = diag(sigma) V^T (r x n), then A <- A - U W
+            const int64_t ldw = round_up(r, 2);
+            transpose(c, dV.p(), ldv, n, r, W.p(), ldw);
+            scale_rows(c, W.p(), ldw, r, n, dS.p());
+            gemm(c, false, m, n, r, dU.p(), ldu, W.p(), ldw, dA.p(), lda, nullptr, false, -1.0, true);
+        }
+        *delta = std::sqrt(frob_sq(c, dA.p(), lda, m, n) / norm_sq);
     });
 }
 

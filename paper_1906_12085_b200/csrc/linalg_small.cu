@@ -136,6 +136,14 @@ __global__ void sub_rowmean_kernel(const double* A, int64_t lda, int64_t m, int6
             dst[i + j * ldd] = A[i + j * lda] - mean[i];
 }
 
+__global__ void scale_rows_kernel(double* W, int64_t ldw, int64_t rows, int64_t cols,
+                                  const double* s) {
+    for (int64_t j = blockIdx.y; j < cols; j += gridDim.y)
+        for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < rows;
+             i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+            W[i + j * ldw] *= s[i];
+}
+
 dim3 grid2d(Ctx* c, int64_t rows, int64_t cols, int threads) {
     int64_t gx = std::min<int64_t>(ceil_div(rows, threads), 4 * c->num_sms);
     int64_t gy = std::min<int64_t>(cols, 65535);
@@ -145,6 +153,13 @@ dim3 grid2d(Ctx* c, int64_t rows, int64_t cols, int threads) {
 }
 
 }  // namespace
+
+void scale_rows(Ctx* c, double* W, int64_t ldw, int64_t rows, int64_t cols, const double* s) {
+    if (rows <= 0 || cols <= 0) return;
+    scale_rows_kernel<<<grid2d(c, rows, cols, 256), 256, 0, c->stream>>>(W, ldw, rows, cols, s);
+    SVDK_CHECK_LAUNCH();
+    c->launches++;
+}
 
 void fill(Ctx* c, double* p, int64_t count, double v) {
     if (count <= 0) return;

@@ -163,6 +163,8 @@ void syrk(Ctx* c, int64_t m, int64_t n, const double* A, int64_t lda, double* G,
 
 // Small helpers (linalg_small.cu)
 void fill(Ctx* c, double* p, int64_t count, double v);
+// W[i, j] *= s[i]
+void scale_rows(Ctx* c, double* W, int64_t ldw, int64_t rows, int64_t cols, const double* s);
 void copy_mat(Ctx* c, const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows,
               int64_t cols);
 void transpose(Ctx* c, const double* src, int64_t lds, int64_t rows, int64_t cols, double* dst,

@@ -24,7 +24,7 @@ __all__ = [
     "frobenius_norm_sq", "frobenius_norm", "qr_thin", "eig_sym", "gaussian_matrix",
     "truncated_svd", "randomized_pca", "krylov_svd", "lanczos_svd", "compute_svd",
     "compute_svd_any", "method_name", "method_from_name", "center", "total_variance",
-    "select_components", "fit_pca",
+    "select_components", "fit_pca", "transform", "residual_delta", "truncate_rank",
 ]
 
 
@@ -355,3 +355,37 @@ def fit_pca(data, orientation: Orientation, method: SvdMethod, params: MethodPar
                                         _ptr(basis), _ptr(eig), C.byref(total), _ptr(mean), C.byref(rank)))
     r = int(rank.value)
     return PcaModel(np.asfortranarray(basis[:, :r]), eig[:r].copy(), total.value, orientation, mean[:nm].copy())
+
+
+def transform(model: PcaModel, a) -> np.ndarray:
+    """pca.cpp:118-131 — project centred data onto the basis."""
+    a = _mat(a)
+    if model.orientation == Orientation.ColumnsAreExamples:
+        if a.shape[0] != model.basis.shape[0]:
+            raise DimensionError(f"transform: data is {_shape(a)} but basis is {_shape(model.basis)} "
+                                 "(feature rows must match)")
+        return matmul_transposed_left(model.basis, a)
+    if a.shape[1] != model.basis.shape[0]:
+        raise DimensionError(f"transform: data is {_shape(a)} but basis is {_shape(model.basis)} "
+                             "(feature columns must match)")
+    return matmul(a, model.basis)
+
+
+def residual_delta(a, s: SvdResult) -> float:
+    """pca.cpp:133-168 — ||A - U diag(sigma) V^T||_F / ||A||_F on the GPU."""
+    a = _mat(a)
+    u, v = _mat(s.u), _mat(s.v)
+    if u.shape[0] != a.shape[0] or v.shape[0] != a.shape[1]:
+        raise DimensionError(f"residual_delta: factors {_shape(u)}/{_shape(v)} do not match data {_shape(a)}")
+    sig = np.ascontiguousarray(s.sigma, dtype=np.float64)
+    out = C.c_double(0.0)
+    _lib.check(_lib.load().svdk_residual_delta(_ctx(), _ptr(a), a.shape[0], a.shape[1], _ptr(u), _ptr(sig),
+                                               _ptr(v), int(s.rank), C.byref(out)))
+    return out.value
+
+
+def truncate_rank(s: SvdResult, k: int) -> SvdResult:
+    """svd_methods.cpp:198-225 — keep the leading k triplets (pure data movement)."""
+    if k < 1 or k > s.rank:
+        raise ParamError(f"truncate_rank: k = {k} outside [1, rank = {s.rank}]")
+    return SvdResult(np.asfortranarray(s.u[:, :k]), s.sigma[:k].copy(), np.asfortranarray(s.v[:, :k]), k, s.method)

@@ -85,3 +85,27 @@ def test_python_mirror_validates_shapes_before_device():
 def test_no_gpu_fails_loudly():
     with pytest.raises(errors.EngineError):
         _lib.Context(0)
+
+
+FACADE_API = ["svdkit::matmul(", "svdkit::matmul_transposed_left(", "svdkit::transpose(", "svdkit::gram(",
+              "svdkit::frobenius_norm_sq(", "svdkit::qr_thin(", "svdkit::eig_sym(", "svdkit::gaussian_matrix(",
+              "svdkit::truncated_svd(", "svdkit::randomized_pca(", "svdkit::krylov_svd(", "svdkit::lanczos_svd(",
+              "svdkit::truncate_rank(", "svdkit::compute_svd(", "svdkit::compute_svd_any(", "svdkit::center(",
+              "svdkit::total_variance(", "svdkit::select_components(", "svdkit::fit_pca(", "svdkit::transform(",
+              "svdkit::residual_delta(", "svdkit::method_name(", "svdkit::method_from_name(",
+              "svdkit::MethodParams::defaults_for(", "svdkit::DenseMatrix::DenseMatrix(", "svdkit::shape_string"]
+
+
+def test_facade_exports_reference_api():
+    lib = os.path.join(ROOT, "facade", "libsvdkit.so")
+    assert os.path.exists(lib), "facade not built"
+    out = subprocess.run(["nm", "-DC", "--defined-only", lib], capture_output=True, text=True, check=True).stdout
+    missing = [f for f in FACADE_API if f not in out]
+    assert not missing, missing
+
+
+@pytest.mark.skipif(HAS_GPU, reason="checks the no-GPU failure path")
+def test_facade_fails_loudly_without_gpu():
+    exe = os.path.join(ROOT, "facade", "facade_test")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode != 0

@@ -139,3 +139,22 @@ def test_fit_pca_columns_are_examples(sk, ref):
     r = ref.truncated_svd(np.asfortranarray(c.T))  # wide -> factor the transpose; basis = U of c = V of c^T
     assert model.basis.shape[0] == 40 and np.allclose(model.mean, mean, atol=1e-14)
     assert eig_rel_err(model.eigenvalues, r.sigma ** 2) < 1e-10
+
+
+def test_residual_delta_transform_truncate(sk, ref):
+    a = np.asfortranarray(np.random.default_rng(14).standard_normal((500, 30)))
+    s = sk.truncated_svd(a)
+    d = sk.residual_delta(a, s)
+    d_ref = ref.residual_delta(a, s.u, s.sigma, s.v)
+    assert d < 1e-13 and abs(d - d_ref) < 1e-13
+    s5 = sk.truncate_rank(s, 5)
+    d5, d5_ref = sk.residual_delta(a, s5), ref.residual_delta(a, s5.u, s5.sigma, s5.v)
+    assert abs(d5 - d5_ref) <= 1e-12 * d5_ref  # Eckart-Young residual of the rank-5 truncation
+    with pytest.raises(errors.ParamError):
+        sk.truncate_rank(s, 0)
+    with pytest.raises(errors.ParamError):
+        sk.residual_delta(np.zeros((4, 2)), sk.SvdResult(np.zeros((4, 1)), np.ones(1), np.zeros((2, 1)), 1))
+    model = sk.fit_pca(a, sk.Orientation.RowsAreExamples, sk.SvdMethod.Truncated, sk.MethodParams(), True)
+    c = sk.center(a, sk.Orientation.RowsAreExamples).centered
+    y = sk.transform(model, c)
+    assert np.allclose(y, c @ model.basis, rtol=0, atol=1e-12)
