@@ -16,6 +16,8 @@
 // hits L2. Per-CTA column partials are reduced in fixed order.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "svdk_methods.h"
@@ -28,17 +30,28 @@ int64_t back_project(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n,
 
 namespace {
 
-constexpr int GV_WARPS = 16;
+constexpr int GV_WARPS = 8;
 constexpr int GV_THREADS = GV_WARPS * 32;
+constexpr int GV_U = 16;     // independent 256-byte column loads in flight per lane
+constexpr int GV_CTAS_PER_SM = 2;  // two CTAs per SM drift out of phase, so one
+                                   // streams HBM (phase 1) while the other
+                                   // re-reads its slab from L2 (phase 2)
 
-// partial[b][j] = sum over this CTA's 32-row slabs of A_slab^T (A_slab q)
-__global__ void __launch_bounds__(GV_THREADS)
+// partial[b][j] = sum over this CTA's 32-row slabs of A_slab^T (A_slab q).
+// Lane l of every warp owns row l of the slab (coalesced 256 B per column).
+//  phase 1: y = A_slab q — warp w sums columns w, w+8, ... with GV_U loads
+//           in flight per lane, then the 16 partial y are combined in smem;
+//  phase 2: for blocks of 32 columns a lane keeps 32 partial products in
+//           registers, and a 31-shuffle butterfly transposes and reduces them
+//           so lane l ends with the full column sum of column l.
+// The slab's second read (phase 2) hits L2: 296 CTAs x 32 rows x n x 8 B.
+__global__ void __launch_bounds__(GV_THREADS, GV_CTAS_PER_SM)
     gemv_pair_kernel(const double* __restrict__ A, int64_t lda, int64_t m, int64_t n,
                      const double* __restrict__ q, double* __restrict__ partial) {
     extern __shared__ double sm[];
-    double* qs = sm;                 // n
-    double* wacc = sm + n;           // n
-    double* ypart = wacc + n;        // GV_WARPS x 32
+    double* qs = sm;            // n
+    double* wacc = sm + n;      // n
+    double* ypart = wacc + n;   // GV_WARPS x 32
     __shared__ double y[32];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     for (int64_t j = tid; j < n; j += GV_THREADS) {
@@ -51,37 +64,142 @@ __global__ void __launch_bounds__(GV_THREADS)
         const int64_t row = s * 32 + lane;
         const bool in = row < m;
         const double* a = A + (in ? row : 0);
-        // phase 1: y = A_slab q  (warp w takes columns w, w+16, ...)
-        double acc0 = 0.0, acc1 = 0.0;
+        // ---- phase 1
+        double acc[GV_U];
+#pragma unroll
+        for (int u = 0; u < GV_U; ++u) acc[u] = 0.0;
         int64_t j = warp;
-        for (; j + GV_WARPS < n; j += 2 * GV_WARPS) {
-            const double x0 = in ? __ldg(a + j * lda) : 0.0;
-            const double x1 = in ? __ldg(a + (j + GV_WARPS) * lda) : 0.0;
-            acc0 = fma(x0, qs[j], acc0);
-            acc1 = fma(x1, qs[j + GV_WARPS], acc1);
+        for (; j + (GV_U - 1) * GV_WARPS < n; j += GV_U * GV_WARPS) {
+            double x[GV_U];
+#pragma unroll
+            for (int u = 0; u < GV_U; ++u) x[u] = in ? __ldg(a + (j + u * GV_WARPS) * lda) : 0.0;
+#pragma unroll
+            for (int u = 0; u < GV_U; ++u) acc[u] = fma(x[u], qs[j + u * GV_WARPS], acc[u]);
         }
-        if (j < n) acc0 = fma(in ? __ldg(a + j * lda) : 0.0, qs[j], acc0);
-        ypart[warp * 32 + lane] = acc0 + acc1;
+        for (; j < n; j += GV_WARPS) acc[0] = fma(in ? a[j * lda] : 0.0, qs[j], acc[0]);
+        double t = 0.0;
+#pragma unroll
+        for (int u = 0; u < GV_U; ++u) t += acc[u];
+        ypart[warp * 32 + lane] = t;
         __syncthreads();
         if (warp == 0) {
-            double t = 0.0;
+            double v = 0.0;
 #pragma unroll
-            for (int w = 0; w < GV_WARPS; ++w) t += ypart[w * 32 + lane];
-            y[lane] = t;
+            for (int w = 0; w < GV_WARPS; ++w) v += ypart[w * 32 + lane];
+            y[lane] = v;
         }
         __syncthreads();
-        // phase 2: wacc += A_slab^T y  (column dot over the 32 lanes)
+        // ---- phase 2: 32-column blocks, warp w takes blocks w, w+GV_WARPS, ...
         const double yl = y[lane];
-        for (int64_t jj = warp; jj < n; jj += GV_WARPS) {
-            double v = (in ? a[jj * lda] : 0.0) * yl;
+        for (int64_t c0 = warp * 32; c0 < n; c0 += GV_WARPS * 32) {
+            double p[32];
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-            if (lane == 0) wacc[jj] += v;
+            for (int c = 0; c < 32; ++c)
+                p[c] = (in && c0 + c < n) ? a[(c0 + c) * lda] * yl : 0.0;
+            // butterfly transpose-reduce: after the step with offset `off`,
+            // lane l holds partial sums for the columns whose index agrees
+            // with l in the bits above `off`
+#pragma unroll
+            for (int off = 16; off >= 1; off >>= 1) {
+                const bool upper = (lane & off) != 0;
+#pragma unroll
+                for (int i = 0; i < off; ++i) {
+                    const double send = upper ? p[i] : p[i + off];
+                    const double keep = upper ? p[i + off] : p[i];
+                    p[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+                }
+            }
+            // lane l now holds the sum of column c0 + l
+            if (c0 + lane < n) wacc[c0 + lane] += p[0];
         }
         // ypart/y are rewritten next slab only after the first barrier above
     }
     __syncthreads();
     for (int64_t j = tid; j < n; j += GV_THREADS) partial[blockIdx.x * n + j] = wacc[j];
+}
+
+// Two-pass streaming form of w = A^T (A q): both passes read A along
+// its columns in long contiguous runs (DRAM-friendly), y (m doubles) lives in
+// L2 between them, and no cross-CTA reduction is needed.
+constexpr int GN_THREADS = 256, GN_ROWS = 4;  // rows per thread in y = A q
+constexpr int GT_THREADS = 256;
+
+// y_c[r] = sum_{j in chunk c} A[r, j] q[j]; CTA (b, c) owns rows
+// [b R, (b+1) R), R = 256 * 4 (thread t rows t, t+256, ...: 256 B runs per
+// warp, 8 KB per CTA) and column chunk c (gridDim.y chunks when m is short).
+__global__ void __launch_bounds__(GN_THREADS)
+    gemv_n_kernel(const double* __restrict__ A, int64_t lda, int64_t m, int64_t n,
+                  const double* __restrict__ q, double* __restrict__ y) {
+    const int64_t r0 = static_cast<int64_t>(blockIdx.x) * GN_THREADS * GN_ROWS + threadIdx.x;
+    const int64_t cw = (n + gridDim.y - 1) / gridDim.y;
+    const int64_t jb = blockIdx.y * cw, je = min(n, jb + cw);
+    y += static_cast<int64_t>(blockIdx.y) * m;
+    double acc[GN_ROWS];
+    bool in[GN_ROWS];
+#pragma unroll
+    for (int u = 0; u < GN_ROWS; ++u) {
+        acc[u] = 0.0;
+        in[u] = r0 + u * GN_THREADS < m;
+    }
+    int64_t j = jb;
+    for (; j + 1 < je; j += 2) {
+        const double q0 = __ldg(q + j), q1 = __ldg(q + j + 1);
+        const double* a0 = A + j * lda + r0;
+        const double* a1 = a0 + lda;
+        double x0[GN_ROWS], x1[GN_ROWS];
+#pragma unroll
+        for (int u = 0; u < GN_ROWS; ++u) {
+            x0[u] = in[u] ? __ldcs(a0 + u * GN_THREADS) : 0.0;
+            x1[u] = in[u] ? __ldcs(a1 + u * GN_THREADS) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < GN_ROWS; ++u) acc[u] = fma(x1[u], q1, fma(x0[u], q0, acc[u]));
+    }
+    if (j < je) {
+        const double qj = __ldg(q + j);
+#pragma unroll
+        for (int u = 0; u < GN_ROWS; ++u)
+            if (in[u]) acc[u] = fma(__ldcs(A + j * lda + r0 + u * GN_THREADS), qj, acc[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < GN_ROWS; ++u)
+        if (in[u]) y[r0 + u * GN_THREADS] = acc[u];
+}
+
+// y[r] = sum_c y_c[r] in chunk order (deterministic)
+__global__ void sum_chunks_kernel(double* y, int64_t m, int chunks) {
+    for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < m;
+         r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        double s = y[r];
+        for (int c = 1; c < chunks; ++c) s += y[c * m + r];
+        y[r] = s;
+    }
+}
+
+// w[j] = sum_i A[i, j] y[i]: one CTA per column, a contiguous m-run.
+__global__ void __launch_bounds__(GT_THREADS)
+    gemv_t_kernel(const double* __restrict__ A, int64_t lda, int64_t m,
+                  const double* __restrict__ y, double* __restrict__ w) {
+    __shared__ double red[GT_THREADS / 32];
+    const double* a = A + static_cast<int64_t>(blockIdx.x) * lda;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int64_t i = threadIdx.x;
+    for (; i + 3 * GT_THREADS < m; i += 4 * GT_THREADS) {
+        s0 = fma(__ldcs(a + i), __ldg(y + i), s0);
+        s1 = fma(__ldcs(a + i + GT_THREADS), __ldg(y + i + GT_THREADS), s1);
+        s2 = fma(__ldcs(a + i + 2 * GT_THREADS), __ldg(y + i + 2 * GT_THREADS), s2);
+        s3 = fma(__ldcs(a + i + 3 * GT_THREADS), __ldg(y + i + 3 * GT_THREADS), s3);
+    }
+    for (; i < m; i += GT_THREADS) s0 = fma(__ldcs(a + i), __ldg(y + i), s0);
+    double s = (s0 + s1) + (s2 + s3);
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int k = 0; k < GT_THREADS / 32; ++k) t += red[k];
+        w[blockIdx.x] = t;
+    }
 }
 
 __global__ void reduce_parts_kernel(const double* partial, int parts, int64_t n, double* w) {
@@ -184,13 +302,22 @@ int64_t lanczos_svd(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n, 
                     uint64_t seed, double* U, int64_t ldu, double* sigma, double* V, int64_t ldv,
                     const RowComm* comm) {
     if (steps <= 0 || steps > n) steps = n;
-    const int parts = c->num_sms;
+    const int parts = GV_CTAS_PER_SM * c->num_sms;
     const size_t gv_smem = (2 * n + GV_WARPS * 32) * sizeof(double);
     if (gv_smem > 200 * 1024) fail(SVDK_E_PARAM, "lanczos_svd: n too large for the fused GEMV");
     SVDK_CUDA(cudaFuncSetAttribute(gemv_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(gv_smem)));
     DBuf Q(c, static_cast<size_t>(n) * (steps + 1)), w(c, n), partial(c, static_cast<size_t>(parts) * n),
         h(c, steps + 1), scal(c, 2 * steps + 8);
+    // GEMV-pair form: "fused" keeps a 32-row slab in L2 between A q and
+    // A^T y (one HBM read, short DRAM runs); "two-pass" streams A twice along
+    // its columns. SVDK_GEMV=fused|twopass overrides the default.
+    const char* gv_env = std::getenv("SVDK_GEMV");
+    const bool two_pass = gv_env ? std::string(gv_env) == "twopass" : true;
+    const int64_t row_blocks = ceil_div(std::max<int64_t>(m, 1), GN_THREADS * GN_ROWS);
+    const int64_t chunks = std::min<int64_t>(std::max<int64_t>(1, ceil_div(2 * c->num_sms, row_blocks)),
+                                             std::max<int64_t>(1, n / 16));
+    DBuf yv(c, static_cast<size_t>(std::max<int64_t>(m, 1)) * chunks);
     double* alpha = scal.p();
     double* beta = scal.p() + steps;
     double* nrm = scal.p() + 2 * steps;  // [0] after pass 1, [1] after pass 2
@@ -205,15 +332,30 @@ int64_t lanczos_svd(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n, 
     double prev_beta = 0.0;
     for (int64_t j = 0; j < steps; ++j) {
         const double* qj = Q.p() + j * n;
-        {
+        if (two_pass) {
             PhaseTimer timer(c, "gemv_pair", 4.0 * m * n, 8.0 * m * n);
-            gemv_pair_kernel<<<parts, GV_THREADS, gv_smem, c->stream>>>(A, lda, m, n, qj,
-                                                                        partial.p());
+            gemv_n_kernel<<<dim3(static_cast<unsigned>(row_blocks), static_cast<unsigned>(chunks)),
+                            GN_THREADS, 0, c->stream>>>(A, lda, m, n, qj, yv.p());
+            SVDK_CHECK_LAUNCH();
+            if (chunks > 1) {
+                sum_chunks_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(m, 256), 4 * c->num_sms)),
+                                    256, 0, c->stream>>>(yv.p(), m, static_cast<int>(chunks));
+                SVDK_CHECK_LAUNCH();
+            }
+            gemv_t_kernel<<<static_cast<unsigned>(n), GT_THREADS, 0, c->stream>>>(A, lda, m, yv.p(),
+                                                                                  w.p());
+            SVDK_CHECK_LAUNCH();
+        } else {
+            {
+                PhaseTimer timer(c, "gemv_pair", 4.0 * m * n, 8.0 * m * n);
+                gemv_pair_kernel<<<parts, GV_THREADS, gv_smem, c->stream>>>(A, lda, m, n, qj,
+                                                                            partial.p());
+                SVDK_CHECK_LAUNCH();
+            }
+            reduce_parts_kernel<<<static_cast<unsigned>(ceil_div(n, 256)), 256, 0, c->stream>>>(
+                partial.p(), parts, n, w.p());
             SVDK_CHECK_LAUNCH();
         }
-        reduce_parts_kernel<<<static_cast<unsigned>(ceil_div(n, 256)), 256, 0, c->stream>>>(
-            partial.p(), parts, n, w.p());
-        SVDK_CHECK_LAUNCH();
         if (comm) comm->allreduce(w.p(), static_cast<size_t>(n));
         alpha_kernel<<<1, 1024, 0, c->stream>>>(w.p(), qj, j > 0 ? Q.p() + (j - 1) * n : nullptr, n,
                                                 j > 0 ? beta + (j - 1) : nullptr, alpha + j);
