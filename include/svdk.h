@@ -152,8 +152,9 @@ int svdk_dev_qr_thin(svdk_ctx* ctx, const double* h, int64_t m, int64_t p, int64
 /* Full PCA pipeline on a device-resident (local row shard of) A, RowsAreExamples:
  * center -> total variance -> SVD (method) -> select_components(threshold).
  * Outputs on device: u (m_local x r, ldu), sigma (r), v (n x r, ldv), mean (n);
- * on host: *rank, *k (0 = nullopt), *total. With an attached NCCL
- * communicator the reductions over rows span all ranks. */
+ * on host: *rank, *k (0 = nullopt), *total. center: 0 = none, 1 = centre a
+ * copy, 2 = centre A in place (A is overwritten; saves an m x n buffer).
+ * With an attached NCCL communicator the reductions over rows span all ranks. */
 int svdk_dev_pca(svdk_ctx* ctx, const double* a, int64_t m_local, int64_t n, int64_t lda,
                  int method, int64_t l, int64_t q, uint64_t seed, int center, double threshold,
                  double* u, int64_t ldu, double* sigma, double* v, int64_t ldv, double* mean,

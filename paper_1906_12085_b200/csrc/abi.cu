@@ -503,20 +503,20 @@ int svdk_fit_pca(svdk_ctx* c, const double* data, int64_t m, int64_t n, int orie
             else if (method == SVDK_LANCZOS)
                 omega_prefetch(c, tn, 1, seed);
         }
-        int64_t lda, ldc;
-        DBuf dA = upload(c, data, m, n, lda);
-        DBuf dC = alloc_mat(c, m, n, ldc);
+        // The upload buffer is ours: centre it in place (no second m x n copy,
+        // which is what lets the 64 GB c4 matrix fit one GPU).
+        int64_t lda;
+        DBuf dC = upload(c, data, m, n, lda);
+        const int64_t ldc = lda;
         DBuf dM(c, std::max<int64_t>(nm, 1));
         if (center) {
             if (cols_ex)
-                center_cols_are_examples(c, dA.p(), lda, m, n, dC.p(), ldc, dM.p());
+                center_cols_are_examples(c, dC.p(), ldc, m, n, dC.p(), ldc, dM.p());
             else
-                center_rows_are_examples(c, dA.p(), lda, m, n, dC.p(), ldc, dM.p());
+                center_rows_are_examples(c, dC.p(), ldc, m, n, dC.p(), ldc, dM.p());
         } else {
-            copy_mat(c, dA.p(), lda, dC.p(), ldc, m, n);
             fill(c, dM.p(), nm, 0.0);
         }
-        dA.reset();
         *total = frob_sq(c, dC.p(), ldc, m, n);
         // tall orientation for the method
         const bool wide = m < n;
@@ -613,8 +613,8 @@ int svdk_dev_pca(svdk_ctx* c, const double* a, int64_t m_local, int64_t n, int64
                  int64_t* k, double* total) {
     return guarded([&] {
         need_ctx(c);
-        dev_pca(c, a, m_local, n, lda, method, l, q, seed, center != 0, threshold, u, ldu, sigma, v,
-                ldv, mean, rank, k, total);
+        dev_pca(c, a, m_local, n, lda, method, l, q, seed, center, threshold, u, ldu, sigma, v, ldv,
+                mean, rank, k, total);
     });
 }
 

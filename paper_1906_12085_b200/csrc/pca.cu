@@ -109,9 +109,10 @@ int64_t select_components(Ctx* c, const double* d_w, int64_t count, double total
 }
 
 void dev_pca(Ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, int method, int64_t l,
-             int64_t q, uint64_t seed, bool center, double threshold, double* U, int64_t ldu,
+             int64_t q, uint64_t seed, int center_mode, double threshold, double* U, int64_t ldu,
              double* sigma, double* V, int64_t ldv, double* mean, int64_t* rank, int64_t* k,
              double* total) {
+    const bool center = center_mode != 0, center_in_place = center_mode == 2;
     RowComm rc{c};
     const RowComm* comm = c->nccl_comm ? &rc : nullptr;
     const int world = comm ? comm->world() : 1;
@@ -138,8 +139,9 @@ void dev_pca(Ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, int met
     int64_t ldx = lda;
     reset_nonfinite(c);
     if (center) {
-        // pca.cpp:37-53: column means over ALL rows, subtract
-        C = DBuf(c, static_cast<size_t>(ldc) * n);
+        // pca.cpp:37-53: column means over ALL rows, subtract (into a copy, or
+        // in place when the caller passed center == 2 and gave up its A)
+        if (!center_in_place) C = DBuf(c, static_cast<size_t>(ldc) * n);
         if (world > 1) {
             column_sums(c, A, lda, m, n, 1.0, mean);
             comm->allreduce(mean, static_cast<size_t>(n));
@@ -149,9 +151,13 @@ void dev_pca(Ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, int met
         } else {
             column_sums(c, A, lda, m, n, mg, mean);
         }
-        subtract_column_means(c, A, lda, m, n, mean, C.p(), ldc);
-        X = C.p();
-        ldx = ldc;
+        if (center_in_place) {
+            subtract_column_means(c, A, lda, m, n, mean, const_cast<double*>(A), lda);
+        } else {
+            subtract_column_means(c, A, lda, m, n, mean, C.p(), ldc);
+            X = C.p();
+            ldx = ldc;
+        }
     } else {
         fill(c, mean, n, 0.0);
     }

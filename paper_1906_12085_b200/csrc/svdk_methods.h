@@ -61,7 +61,7 @@ int64_t truncated_svd(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n
 
 // Full PCA pipeline on a device-resident (local shard of) A; see svdk.h.
 void dev_pca(Ctx* c, const double* A, int64_t m_local, int64_t n, int64_t lda, int method,
-             int64_t l, int64_t q, uint64_t seed, bool center, double threshold, double* U,
+             int64_t l, int64_t q, uint64_t seed, int center_mode, double threshold, double* U,
              int64_t ldu, double* sigma, double* V, int64_t ldv, double* mean, int64_t* rank,
              int64_t* k, double* total);
 

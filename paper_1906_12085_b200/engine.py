@@ -101,9 +101,10 @@ class Engine:
                                              C.byref(rank)))
         return q, r, int(rank.value)
 
-    def pca(self, a, method: int = 0, l: int = 0, q: int = 0, seed: int = 0, center: bool = True,
+    def pca(self, a, method: int = 0, l: int = 0, q: int = 0, seed: int = 0, center=True,
             threshold: float = 0.95, out: PcaOutput | None = None) -> PcaOutput:
-        """Full RowsAreExamples PCA on a device-resident (row shard of) A."""
+        """Full RowsAreExamples PCA on a device-resident (row shard of) A.
+        center: True/1 centre a copy, 2 centre A in place (overwrites A), False/0 none."""
         m, n = a.shape
         width = {1: l, 2: min((q + 1) * l, n), 3: (n if l <= 0 or l > n else l)}.get(int(method), n)
         width = max(width, 1)
@@ -113,7 +114,7 @@ class Engine:
                             0, None, 0.0)
         rank, k, total = C.c_int64(0), C.c_int64(0), C.c_double(0.0)
         _lib.check(self.lib.svdk_dev_pca(self.ctx.handle, _p(a), m, n, _ld(a), int(method), int(l), int(q),
-                                         int(seed) & (2**64 - 1), 1 if center else 0, float(threshold),
+                                         int(seed) & (2**64 - 1), int(center), float(threshold),
                                          _p(out.u), _ld(out.u), _p(out.sigma), _p(out.v), n, _p(out.mean),
                                          C.byref(rank), C.byref(k), C.byref(total)))
         out.rank, out.k, out.total = int(rank.value), (int(k.value) or None), total.value
