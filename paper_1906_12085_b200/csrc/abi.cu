@@ -22,7 +22,7 @@ int64_t lanczos_svd(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n, 
                     uint64_t seed, double* U, int64_t ldu, double* sigma, double* V, int64_t ldv,
                     const RowComm* comm);
 int64_t qr_thin(Ctx* c, const double* H, int64_t ldh, int64_t m, int64_t p, double* Q, int64_t ldq,
-                double* R, const RowComm* comm);
+                double* R, const RowComm* comm, double* Rinv_last = nullptr);
 int64_t select_components(Ctx* c, const double* d_w, int64_t count, double total, double t);
 }  // namespace svdk
 

@@ -5,8 +5,8 @@
 // For the tall-skinny H (m >> p) of the range finder, Householder is a
 // BLAS-2 column sweep; CholeskyQR2 turns it into two FP64 DMMA passes:
 //     G = H^T H (SYRK [+ NCCL allreduce over row shards]);  G = R^T R;
-//     Q = H R^-1 (blocked right-TRSM: one NN GEMM per 128-column panel);
-//     repeat once on Q; R = R2 R1.
+//     Q = H R^-1 (R^-1 by a blocked triangular inverse, then one tall GEMM
+//     that skips R^-1's zero k-tiles); repeat once on Q; R = R2 R1.
 // R has a positive diagonal by construction (the reference's sign
 // convention, kernels.cpp:173-182). Full-rank inputs whose Gram is too
 // ill-conditioned for CholeskyQR2 (a relative Cholesky pivot below 1e-12)
@@ -27,7 +27,7 @@ void gaussian_fill(int64_t rows, int64_t cols, uint64_t seed, double* out);
 
 namespace {
 
-constexpr int NB = 128;  // Cholesky / TRSM panel width
+constexpr int NB = 64;  // Cholesky panel width (diagonal block factored by one CTA)
 
 // Factor the bs x bs diagonal block G[k0.., k0..] (upper part holds the
 // trailing-updated values) as R^T R, write R (upper) and R^-1 (upper).
@@ -60,11 +60,15 @@ __global__ void __launch_bounds__(256)
         const double inv = dinv[j];
         for (int c = j + 1 + tid; c < bs; c += blockDim.x) S[j + c * LD] *= inv;
         __syncthreads();
-        // trailing update of the upper triangle: S[i][c] -= S[j][i] S[j][c], j < i <= c
-        const int t = bs - j - 1;
-        for (int e = tid; e < t * t; e += blockDim.x) {
-            const int i = j + 1 + e % t, c = j + 1 + e / t;
-            if (i <= c) S[i + c * LD] -= S[j + i * LD] * S[j + c * LD];
+        // trailing update of the upper triangle: S[i][c] -= S[j][i] S[j][c],
+        // j < i <= c; a warp per column, lanes down the rows (no idle lanes
+        // on the lower half)
+        {
+            const int warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
+            for (int cc = j + 1 + warp; cc < bs; cc += nw) {
+                const double sjc = S[j + cc * LD];
+                for (int i = j + 1 + lane; i <= cc; i += 32) S[i + cc * LD] -= S[j + i * LD] * sjc;
+            }
         }
         __syncthreads();
     }
@@ -169,28 +173,39 @@ bool potrf_upper(Ctx* c, double* G, int64_t ldg, int64_t p, double* R, int64_t l
     return read_flag(c, 3) == 0;
 }
 
-// Q = H R^-1 for upper R (p x p) with precomputed diagonal-block inverses.
-// W is scratch with H's contents (may alias H when H is disposable).
-void trsm_right_upper(Ctx* c, double* W, int64_t ldw, int64_t m, int64_t p, const double* R,
-                      int64_t ldr, const double* Rinv_blocks, double* Q, int64_t ldq) {
+// R^-1 (p x p, upper) from R and the inverses of its diagonal blocks, by a
+// blocked back substitution: X_IJ = -R_II^-1 (R_I,>I X_>I,J), bottom-up, two
+// small triangular-aware GEMMs per 128-row block.
+void trtri_upper(Ctx* c, const double* R, int64_t ldr, int64_t p, const double* Rinv_blocks,
+                 double* X, int64_t ldx) {
     const int64_t nblk = ceil_div(p, NB);
-    for (int64_t J = 0; J < nblk; ++J) {
-        const int64_t j0 = J * NB;
-        const int64_t bs = std::min<int64_t>(NB, p - j0);
-        if (j0 > 0)  // W_J -= Q[:, :j0] R[:j0, J]
-            gemm(c, false, m, bs, j0, Q, ldq, R + j0 * ldr, ldr, W + j0 * ldw, ldw, nullptr, false,
-                 -1.0, true);
-        gemm(c, false, m, bs, bs, W + j0 * ldw, ldw, Rinv_blocks + J * NB * NB, NB, Q + j0 * ldq,
-             ldq);
+    if (ldx == p)
+        fill(c, X, p * p, 0.0);
+    else
+        for (int64_t j = 0; j < p; ++j) fill(c, X + j * ldx, p, 0.0);
+    for (int64_t kb = 0; kb < nblk; ++kb) {
+        const int64_t k0 = kb * NB, bs = std::min<int64_t>(NB, p - k0);
+        copy_mat(c, Rinv_blocks + kb * NB * NB, NB, X + k0 + k0 * ldx, ldx, bs, bs);
+    }
+    DBuf T(c, static_cast<size_t>(NB) * std::max<int64_t>(p, 1));
+    for (int64_t kb = nblk - 2; kb >= 0; --kb) {
+        const int64_t k0 = kb * NB, k1 = k0 + NB, rest = p - k1;
+        // T = R[I, >I] X[>I, >I]   (X[>I, >I] is upper triangular)
+        gemm(c, false, NB, rest, rest, R + k0 + k1 * ldr, ldr, X + k1 + k1 * ldx, ldx, T.p(), NB,
+             nullptr, false, 1.0, false, true);
+        // X[I, >I] = -R_II^-1 T
+        gemm(c, false, NB, rest, NB, Rinv_blocks + kb * NB * NB, NB, T.p(), NB, X + k0 + k1 * ldx, ldx,
+             nullptr, false, -1.0, false);
     }
 }
 
 namespace {
 
-// One CholeskyQR pass: Q = H R^-1 with R from chol(H^T H + shift I).
-// H is overwritten (used as TRSM scratch). Returns false on breakdown.
-bool cholqr_pass(Ctx* c, double* H, int64_t ldh, int64_t m, int64_t p, double* Q, int64_t ldq,
-                 double* R, double shift_rel, double rel_tol, const RowComm* comm) {
+// One CholeskyQR pass, out of place: Q = H R^-1 with R from
+// chol(H^T H + shift I). Returns false on breakdown.
+bool cholqr_pass(Ctx* c, const double* H, int64_t ldh, int64_t m, int64_t p, double* Q, int64_t ldq,
+                 double* R, double shift_rel, double rel_tol, const RowComm* comm,
+                 double* Rinv_out = nullptr) {
     DBuf G(c, static_cast<size_t>(p) * p), Rinv(c, static_cast<size_t>(ceil_div(p, NB)) * NB * NB);
     gram_rows(c, H, ldh, m, p, G.p(), p, comm);
     if (shift_rel > 0.0) {
@@ -209,50 +224,64 @@ bool cholqr_pass(Ctx* c, double* H, int64_t ldh, int64_t m, int64_t p, double* Q
         c->launches += 2;
     }
     if (!potrf_upper(c, G.p(), p, p, R, p, Rinv.p(), rel_tol)) return false;
-    trsm_right_upper(c, H, ldh, m, p, R, p, Rinv.p(), Q, ldq);
+    // Q = H R^-1: explicit triangular inverse (p^3/3 flops) + ONE tall GEMM
+    // that skips the zero k-tiles of R^-1 (m p^2 flops, like a TRSM).
+    DBuf X;
+    double* xp = Rinv_out;
+    if (!xp) {
+        X = DBuf(c, static_cast<size_t>(p) * p);
+        xp = X.p();
+    }
+    trtri_upper(c, R, p, p, Rinv.p(), xp, p);
+    // implicit form: the caller folds R^-1 into its next small product instead
+    if (!Rinv_out) gemm(c, false, m, p, p, H, ldh, xp, p, Q, ldq, nullptr, false, 1.0, false, true);
     return true;
 }
 
 }  // namespace
 
 // CholeskyQR2 with fallbacks. Q (m x p, ldq), R (p x p, ld p) or nullptr.
-// Returns the numerical rank. H is not modified.
+// Returns the numerical rank. H is not modified. With Rinv_last != nullptr the
+// last CholeskyQR pass is left implicit: Q receives Q1 and the orthonormal
+// factor is Q1 * Rinv_last (p x p upper) — the sketch methods fold Rinv_last
+// into their small n x l / l x l products and save one m x p x p GEMM.
 int64_t qr_thin(Ctx* c, const double* H, int64_t ldh, int64_t m, int64_t p, double* Q, int64_t ldq,
-                double* R, const RowComm* comm) {
+                double* R, const RowComm* comm, double* Rinv_last) {
     if (p == 0) return 0;
     PhaseTimer timer(c, "qr_thin");
     const int64_t ldw = round_up(std::max<int64_t>(m, 1), 2);
-    DBuf W(c, static_cast<size_t>(ldw) * p), Q1(c, static_cast<size_t>(ldw) * p);
+    // W: fallback scratch (on demand). In the implicit form Q1 lives in Q.
+    DBuf W, Q1buf;
+    if (!Rinv_last) Q1buf = DBuf(c, static_cast<size_t>(ldw) * p);
+    struct {
+        double* ptr;
+        double* p() const { return ptr; }
+    } Q1{Rinv_last ? Q : Q1buf.p()};
+    const int64_t ldq1 = Rinv_last ? ldq : ldw;
     DBuf R1(c, static_cast<size_t>(p) * p), R2(c, static_cast<size_t>(p) * p);
-    auto load_w = [&] { copy_mat(c, H, ldh, W.p(), ldw, m, p); };
 
     const double accept = 1e-12;  // relative pivot floor for a plain CholeskyQR pass
     bool ok;
     // --- CholeskyQR2 ---
-    load_w();
-    ok = cholqr_pass(c, W.p(), ldw, m, p, Q1.p(), ldw, R1.p(), 0.0, accept, comm);
+    ok = cholqr_pass(c, H, ldh, m, p, Q1.p(), ldq1, R1.p(), 0.0, accept, comm);
     if (!ok) {
         // --- shifted CholeskyQR3: first pass on G + s I ---
-        load_w();
         const double u = 1.1102230246251565e-16;
         const double mg = static_cast<double>(m) * std::max(1, comm ? comm->world() : 1);
         const double shift_rel = 11.0 * (mg * p + p * (p + 1.0)) * u;
-        ok = cholqr_pass(c, W.p(), ldw, m, p, Q1.p(), ldw, R1.p(), shift_rel, 0.0, comm);
+        W = DBuf(c, static_cast<size_t>(ldw) * p);
+        ok = cholqr_pass(c, H, ldh, m, p, W.p(), ldw, R2.p(), shift_rel, 0.0, comm);
         if (ok) {
-            DBuf R0(c, static_cast<size_t>(p) * p);
-            copy_mat(c, R1.p(), p, R0.p(), p, p, p);
-            copy_mat(c, Q1.p(), ldw, W.p(), ldw, m, p);
-            ok = cholqr_pass(c, W.p(), ldw, m, p, Q1.p(), ldw, R1.p(), 0.0, accept, comm);
-            if (ok) {  // R1 <- R1 R0
+            ok = cholqr_pass(c, W.p(), ldw, m, p, Q1.p(), ldq1, R1.p(), 0.0, accept, comm);
+            if (ok) {  // R1 <- R1 R2
                 DBuf t(c, static_cast<size_t>(p) * p);
-                gemm(c, false, p, p, p, R1.p(), p, R0.p(), p, t.p(), p);
+                gemm(c, false, p, p, p, R1.p(), p, R2.p(), p, t.p(), p);
                 copy_mat(c, t.p(), p, R1.p(), p, p, p);
             }
         }
     }
     if (ok) {
-        copy_mat(c, Q1.p(), ldw, W.p(), ldw, m, p);
-        ok = cholqr_pass(c, W.p(), ldw, m, p, Q, ldq, R2.p(), 0.0, accept, comm);
+        ok = cholqr_pass(c, Q1.p(), ldq1, m, p, Q, ldq, R2.p(), 0.0, accept, comm, Rinv_last);
         if (ok) {
             if (R) gemm(c, false, p, p, p, R2.p(), p, R1.p(), p, R, p);  // R = R2 R1
             return p;
@@ -272,14 +301,14 @@ int64_t qr_thin(Ctx* c, const double* H, int64_t ldh, int64_t m, int64_t p, doub
     SVDK_CHECK_LAUNCH();
     c->launches++;
     const int64_t r = (w0 > 0.0) ? read_flag(c, 4) : 0;
+    if (!W.p()) W = DBuf(c, static_cast<size_t>(ldw) * p);
+    if (!Q1buf.p()) Q1buf = DBuf(c, static_cast<size_t>(ldw) * p);
+    Q1.ptr = Q1buf.p();
     if (r > 0) {
         // Q_r = H W_r Lambda_r^-1/2, then one CholeskyQR2 to clean orthogonality
         gemm(c, false, m, r, p, H, ldh, Wv.p(), p, W.p(), ldw, scale.p());
         ok = cholqr_pass(c, W.p(), ldw, m, r, Q1.p(), ldw, R1.p(), 0.0, 0.0, comm);
-        if (ok) {
-            copy_mat(c, Q1.p(), ldw, W.p(), ldw, m, r);
-            ok = cholqr_pass(c, W.p(), ldw, m, r, Q, ldq, R2.p(), 0.0, 0.0, comm);
-        }
+        if (ok) ok = cholqr_pass(c, Q1.p(), ldw, m, r, Q, ldq, R2.p(), 0.0, 0.0, comm);
         if (!ok) fail(SVDK_E_NUMERICAL, "qr_thin: rank-revealing fallback failed", 0.0);
     }
     if (r < p) {
@@ -297,14 +326,12 @@ int64_t qr_thin(Ctx* c, const double* H, int64_t ldh, int64_t m, int64_t p, doub
                 gemm_tn_rows(c, r, pc, m, Q, ldq, Z.p(), ldw, T.p(), r, comm);
                 gemm(c, false, m, pc, r, Q, ldq, T.p(), r, Z.p(), ldw, nullptr, false, -1.0, true);
             }
-        for (int pass = 0; pass < 2 && ok; ++pass) {
-            ok = cholqr_pass(c, Z.p(), ldw, m, pc, pass == 0 ? Q1.p() : Q + r * ldq,
-                             pass == 0 ? ldw : ldq, R1.p(), 0.0, 0.0, comm);
-            if (pass == 0 && ok) copy_mat(c, Q1.p(), ldw, Z.p(), ldw, m, pc);
-        }
+        ok = cholqr_pass(c, Z.p(), ldw, m, pc, Q1.p(), ldw, R1.p(), 0.0, 0.0, comm);
+        if (ok) ok = cholqr_pass(c, Q1.p(), ldw, m, pc, Q + r * ldq, ldq, R1.p(), 0.0, 0.0, comm);
         if (!ok) fail(SVDK_E_NUMERICAL, "qr_thin: completion of a rank-deficient basis failed", 0.0);
     }
     if (R) gemm_tn_rows(c, p, p, m, Q, ldq, H, ldh, R, p, comm);  // R = Q^T H
+    if (Rinv_last) set_identity(c, Rinv_last, p, p);  // explicit Q: implicit factor I
     return r;
 }
 

@@ -62,6 +62,7 @@ struct Params {
     int* flag;
     double alpha;  // out = alpha * (op(A) B) [+ C_old when beta_one]
     int beta_one;
+    int b_upper;   // B is upper triangular: tile (., col0) only needs k < col0 + BN
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -136,6 +137,8 @@ __device__ __forceinline__ Unit decode(const Params& p, int u) {
     w.diag = (p.kind == KIND_SYRK) && (ti == tj);
     w.k0 = static_cast<int64_t>(split) * p.k_per_split;
     w.k1 = min(p.K, w.k0 + p.k_per_split);
+    if (p.b_upper) w.k1 = min(w.k1, w.col0 + BN);
+    if (w.k1 < w.k0) w.k1 = w.k0;
     return w;
 }
 
@@ -410,7 +413,8 @@ void launch(Ctx* c, Params& p, const CUtensorMap& ma, const CUtensorMap& mb) {
     const int grid = std::min(p.units, c->num_sms);
     // algorithmic work: Gram m n (n+1); GEMM 2 M N K
     const double flops = p.kind == KIND_SYRK ? static_cast<double>(p.K) * p.M * (p.M + 1)
-                                             : 2.0 * p.M * p.N * p.K;
+                         : p.b_upper      ? 1.0 * p.M * p.N * (p.N + 1)  // triangular B: M N (N+1)
+                                          : 2.0 * p.M * p.N * p.K;
     const double bytes = p.kind == KIND_SYRK ? 8.0 * (p.K * p.M + p.M * p.M)
                                              : 8.0 * (p.M * p.K + p.K * p.N + p.M * p.N);
     {
@@ -470,7 +474,7 @@ void syrk(Ctx* c, int64_t m, int64_t n, const double* A, int64_t lda, double* G,
 
 void gemm(Ctx* c, bool transa, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda,
           const double* B, int64_t ldb, double* C, int64_t ldc, const double* col_scale,
-          bool nonfinite_check, double alpha, bool beta_one) {
+          bool nonfinite_check, double alpha, bool beta_one, bool b_upper) {
     if (m == 0 || n == 0) return;
     if (k == 0) {
         if (!beta_one)
@@ -512,6 +516,7 @@ void gemm(Ctx* c, bool transa, int64_t m, int64_t n, int64_t k, const double* A,
     p.col_scale = col_scale;
     p.alpha = alpha;
     p.beta_one = beta_one ? 1 : 0;
+    p.b_upper = b_upper ? 1 : 0;
     if (nonfinite_check) p.flag = c->d_flags;  // sticky; see raise_if_nonfinite()
     const CUtensorMap ma = transa ? make_map(A, k, m, lda, BK, BM) : make_map(A, m, k, lda, 16, BK);
     const CUtensorMap mb = make_map(B, k, n, ldb, BK, BN);

@@ -161,6 +161,20 @@ void scale_rows(Ctx* c, double* W, int64_t ldw, int64_t rows, int64_t cols, cons
     c->launches++;
 }
 
+__global__ void identity_kernel(double* X, int64_t ld, int64_t n) {
+    for (int64_t j = blockIdx.y; j < n; j += gridDim.y)
+        for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+             i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+            X[i + j * ld] = i == j ? 1.0 : 0.0;
+}
+
+void set_identity(Ctx* c, double* X, int64_t ld, int64_t n) {
+    if (n <= 0) return;
+    identity_kernel<<<grid2d(c, n, n, 256), 256, 0, c->stream>>>(X, ld, n);
+    SVDK_CHECK_LAUNCH();
+    c->launches++;
+}
+
 void fill(Ctx* c, double* p, int64_t count, double v) {
     if (count <= 0) return;
     const int64_t blocks = std::min<int64_t>(ceil_div(count, 256), 8 * c->num_sms);

@@ -18,7 +18,7 @@
 namespace svdk {
 void gaussian_fill(int64_t rows, int64_t cols, uint64_t seed, double* out);
 int64_t qr_thin(Ctx* c, const double* H, int64_t ldh, int64_t m, int64_t p, double* Q, int64_t ldq,
-                double* R, const RowComm* comm);
+                double* R, const RowComm* comm, double* Rinv_last);
 
 // ---------------------------------------------------------------------------
 // Reference Gaussian sampler staged through pinned memory, asynchronously.
@@ -96,16 +96,21 @@ void power_step(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n, cons
 
 }  // namespace
 
-// svd_methods.cpp:97-117. Q (m x w, row-sharded), T = A^T Q (n x w, replicated).
+// svd_methods.cpp:97-117. The orthonormal basis is Q1 Rinv (Q1 m x w
+// row-sharded, Rinv w x w upper: CholeskyQR2's implicit last pass), T = A^T Q
+// (n x w, replicated).
 int64_t finish_sketch(Ctx* c, const double* Q, int64_t ldq, int64_t m, int64_t w, const double* T,
-                      int64_t n, double* U, int64_t ldu, double* sigma, double* V, int64_t ldv) {
+                      int64_t n, double* U, int64_t ldu, double* sigma, double* V, int64_t ldv,
+                      const double* Rinv) {
     // The small SVD works on replicated data: no row communicator.
     if (n >= w) {
         const int64_t ldiu = round_up(n, 2);
         DBuf iu(c, static_cast<size_t>(ldiu) * w), iv(c, static_cast<size_t>(w) * w);
         const int64_t r = truncated_svd(c, T, n, n, w, iu.p(), ldiu, sigma, iv.p(), w, nullptr);
         if (r == 0) return 0;
-        gemm(c, false, m, r, w, Q, ldq, iv.p(), w, U, ldu, nullptr, true);  // U = Q inner.v
+        DBuf rv(c, static_cast<size_t>(w) * r);  // Rinv inner.v (w x r)
+        gemm(c, false, w, r, w, Rinv, w, iv.p(), w, rv.p(), w);
+        gemm(c, false, m, r, w, Q, ldq, rv.p(), w, U, ldu, nullptr, true);  // U = Q inner.v
         copy_mat(c, iu.p(), ldiu, V, ldv, n, r);                             // V = inner.u
         normalize_signs_uv(c, U, ldu, m, V, ldv, n, r);
         return r;
@@ -117,7 +122,9 @@ int64_t finish_sketch(Ctx* c, const double* Q, int64_t ldq, int64_t m, int64_t w
     DBuf iu(c, static_cast<size_t>(ldt) * n), iv(c, static_cast<size_t>(n) * n);
     const int64_t r = truncated_svd(c, Tt.p(), ldt, w, n, iu.p(), ldt, sigma, iv.p(), n, nullptr);
     if (r == 0) return 0;
-    gemm(c, false, m, r, w, Q, ldq, iu.p(), ldt, U, ldu, nullptr, true);  // U = Q inner.v
+    DBuf rv(c, static_cast<size_t>(w) * r);  // Rinv inner.v (w x r)
+    gemm(c, false, w, r, w, Rinv, w, iu.p(), ldt, rv.p(), w);
+    gemm(c, false, m, r, w, Q, ldq, rv.p(), w, U, ldu, nullptr, true);  // U = Q inner.v
     copy_mat(c, iv.p(), n, V, ldv, n, r);                                  // V = inner.u
     normalize_signs_uv(c, U, ldu, m, V, ldv, n, r);
     return r;
@@ -136,11 +143,13 @@ int64_t randomized_pca(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t 
         std::swap(H, H2);
     }
     Om.reset();
-    // Q = qr_thin(H).q  (H2 reused as Q)
-    qr_thin(c, H.p(), ldh, m, l, H2.p(), ldh, nullptr, comm);
+    // Q = qr_thin(H).q = Q1 Rinv  (H2 reused as Q1)
+    DBuf Rinv(c, static_cast<size_t>(l) * l), T(c, static_cast<size_t>(n) * l);
+    qr_thin(c, H.p(), ldh, m, l, H2.p(), ldh, nullptr, comm, Rinv.p());
     H.reset();
-    gemm_tn_rows(c, n, l, m, A, lda, H2.p(), ldh, Z.p(), n, comm);  // T = A^T Q
-    return finish_sketch(c, H2.p(), ldh, m, l, Z.p(), n, U, ldu, sigma, V, ldv);
+    gemm_tn_rows(c, n, l, m, A, lda, H2.p(), ldh, Z.p(), n, comm);  // A^T Q1
+    gemm(c, false, n, l, l, Z.p(), n, Rinv.p(), l, T.p(), n, nullptr, false, 1.0, false, true);  // T = A^T Q
+    return finish_sketch(c, H2.p(), ldh, m, l, T.p(), n, U, ldu, sigma, V, ldv, Rinv.p());
 }
 
 int64_t krylov_svd(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n, int64_t l,
@@ -156,11 +165,13 @@ int64_t krylov_svd(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n, i
         power_step(c, A, lda, m, n, H.p() + (b - 1) * l * ldh, ldh, l, H.p() + b * l * ldh, ldh,
                    Z.p(), comm);
     Om.reset();
-    DBuf Q(c, static_cast<size_t>(ldh) * w);
-    qr_thin(c, H.p(), ldh, m, w, Q.p(), ldh, nullptr, comm);
+    DBuf Q(c, static_cast<size_t>(ldh) * w), Rinv(c, static_cast<size_t>(w) * w),
+        T(c, static_cast<size_t>(n) * w);
+    qr_thin(c, H.p(), ldh, m, w, Q.p(), ldh, nullptr, comm, Rinv.p());
     H.reset();
-    gemm_tn_rows(c, n, w, m, A, lda, Q.p(), ldh, Z.p(), n, comm);  // T = A^T Q (n x w)
-    return finish_sketch(c, Q.p(), ldh, m, w, Z.p(), n, U, ldu, sigma, V, ldv);
+    gemm_tn_rows(c, n, w, m, A, lda, Q.p(), ldh, Z.p(), n, comm);  // A^T Q1 (n x w)
+    gemm(c, false, n, w, w, Z.p(), n, Rinv.p(), w, T.p(), n, nullptr, false, 1.0, false, true);  // T = A^T Q
+    return finish_sketch(c, Q.p(), ldh, m, w, T.p(), n, U, ldu, sigma, V, ldv, Rinv.p());
 }
 
 }  // namespace svdk

@@ -153,16 +153,19 @@ inline int64_t ceil_div(int64_t x, int64_t m) { return (x + m - 1) / m; }
 // B is k x n (K-major). Optional per-column scale of the output (epilogue).
 // If nonfinite_check, raises SVDK_E_NUMERICAL on a non-finite output entry
 // (reference kernels.cpp:39-43).
-// Epilogue: C = alpha * (op(A) B) (+ C_old when beta_one).
+// Epilogue: C = alpha * (op(A) B) (+ C_old when beta_one). b_upper: B is
+// upper triangular (K = N), zero k-tiles below the diagonal are skipped.
 void gemm(Ctx* c, bool transa, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda,
           const double* B, int64_t ldb, double* C, int64_t ldc, const double* col_scale = nullptr,
-          bool nonfinite_check = false, double alpha = 1.0, bool beta_one = false);
+          bool nonfinite_check = false, double alpha = 1.0, bool beta_one = false,
+          bool b_upper = false);
 // G = alpha A^T A (+ G_old) (n x n, exactly symmetric), A m x n.
 void syrk(Ctx* c, int64_t m, int64_t n, const double* A, int64_t lda, double* G, int64_t ldg,
           double alpha = 1.0, bool beta_one = false);
 
 // Small helpers (linalg_small.cu)
 void fill(Ctx* c, double* p, int64_t count, double v);
+void set_identity(Ctx* c, double* X, int64_t ld, int64_t n);
 // W[i, j] *= s[i]
 void scale_rows(Ctx* c, double* W, int64_t ldw, int64_t rows, int64_t cols, const double* s);
 void copy_mat(Ctx* c, const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows,
