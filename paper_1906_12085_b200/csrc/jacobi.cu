@@ -148,44 +148,91 @@ __device__ long long g_jprobe[8];
 
 template <int TB>
 constexpr int solve_threads() {
-    return (TB / 2) * (TB / 2) + 32 * (TB / 4);  // M threads + Q warps (2 pairs each)
+    // M threads (one 2x2 block each) + Q warps (2 pairs each) + 1 lookahead warp
+    return (TB / 2) * (TB / 2) + 32 * (TB / 4) + 32;
+}
+
+// R_i^T B R_j on the 2x2 block B = [[m00, m01], [m10, m11]] of rows (p_i, q_i)
+// and columns (p_j, q_j); s == 0 marks an identity rotation; `same` (i == j)
+// annihilates the rotated pair exactly. Written with explicit fma so every
+// thread that evaluates the same block gets the same bits.
+__device__ __forceinline__ void xform2x2(double& m00, double& m01, double& m10, double& m11,
+                                         double ci, double si, double cj, double sj, bool same) {
+    if (sj != 0.0) {  // columns
+        const double a0 = fma(cj, m00, -(sj * m01)), b0 = fma(sj, m00, cj * m01);
+        const double a1 = fma(cj, m10, -(sj * m11)), b1 = fma(sj, m10, cj * m11);
+        m00 = a0; m01 = b0; m10 = a1; m11 = b1;
+    }
+    if (si != 0.0) {  // rows
+        const double a0 = fma(ci, m00, -(si * m10)), b0 = fma(si, m00, ci * m10);
+        const double a1 = fma(ci, m01, -(si * m11)), b1 = fma(si, m01, ci * m11);
+        m00 = a0; m10 = b0; m01 = a1; m11 = b1;
+        if (same) {
+            m01 = 0.0;
+            m10 = 0.0;
+        }
+    }
 }
 
 template <int TB>
 __global__ void __launch_bounds__(solve_threads<TB>())
     jacobi_pair_solve(double* A, int64_t lda, double* Qbuf, int* active, int nb, int round,
                       double skip_tau, int max_inner) {
-    constexpr int B = TB / 2, LD = TB + 4, NP = TB / 2;
-    constexpr int MT = NP * NP;                        // M threads: one 2x2 block each
-    constexpr int QW = (solve_threads<TB>() - MT) / 32;  // Q warps (NP / PPW)
-    constexpr int PPW = NP / QW;                       // pairs per Q warp
+    constexpr int B = TB / 2, LD = TB + 4, NP = TB / 2, R = TB - 1;
+    constexpr int MT = NP * NP;        // M threads
+    constexpr int QT = 32 * (TB / 4);  // Q warps' threads
+    constexpr int PPW = NP / (TB / 4);  // pairs per Q warp
     extern __shared__ double sm[];
     double* Mc = sm;             // current M
     double* Mn = Mc + TB * LD;   // next M (double buffer)
     double* Q = Mn + TB * LD;
     double* T = Q + TB * LD;
-    __shared__ int ptab[TB - 1][NP];  // round-robin pairs, packed p | q << 8
-    __shared__ double cs[TB - 1][NP], sn[TB - 1][NP];
+    __shared__ int ptab[R][NP];            // round-robin pairs, packed p | q << 8
+    __shared__ unsigned char pinv[R][TB];  // pinv[r][x] = pair of x in round r | role << 7
+    __shared__ unsigned long long look[R][NP];  // lookahead descriptors (see below)
+    __shared__ double cs[R][NP], sn[R][NP];
     __shared__ int any_applied;
 
     const int tid = threadIdx.x;
-    const bool probe = blockIdx.x == 0 && tid == 0 && round == 5;
+    const bool probe = blockIdx.x == 0 && tid == MT + QT && round == 5;
     long long t0 = clock64();
     int I, J;
     circle_pair(nb, round, blockIdx.x, I, J);
     if (tid == 0) any_applied = 0;
-    for (int e = tid; e < (TB - 1) * NP; e += blockDim.x) {
+    for (int e = tid; e < R * NP; e += blockDim.x) {
         int p, q;
-        circle_pair(TB, e / NP, e % NP, p, q);
-        ptab[e / NP][e % NP] = p | (q << 8);
+        const int r = e / NP, i = e % NP;
+        circle_pair(TB, r, i, p, q);
+        ptab[r][i] = p | (q << 8);
+        pinv[r][p] = static_cast<unsigned char>(i);
+        pinv[r][q] = static_cast<unsigned char>(i | 128);
     }
-    __syncthreads();
     for (int e = tid; e < TB * TB; e += blockDim.x) {
         const int i = e % TB, j = e / TB;
         const double x = A[gidx(B, I, J, i) + gidx(B, I, J, j) * lda];
         Mc[i + j * LD] = x;
         Q[i + j * LD] = (i == j) ? 1.0 : 0.0;
         if (i != j && fabs(x) > skip_tau) any_applied = 1;
+    }
+    __syncthreads();
+    // look[rr][i]: for rotation i of round rr+1 = (p, q), the round-rr pairs
+    // bp, bq holding p and q, their roles, and bp's / bq's (row, col) indices:
+    // bits 0-4 bp, 5-9 bq, 10 role_p, 11 role_q, 12-16 p_bp, 17-21 q_bp,
+    // 22-26 p_bq, 27-31 q_bq — one LDS instead of a 3-level lookup chain.
+    for (int e = tid; e < R * NP; e += blockDim.x) {
+        const int rr = e / NP, i = e % NP, nr = (rr + 1) % R;
+        const int code = ptab[nr][i];
+        const int ip = pinv[rr][code & 255], iq = pinv[rr][code >> 8];
+        const int bp = ip & 127, bq = iq & 127;
+        const unsigned long long d =
+            static_cast<unsigned long long>(bp) | (static_cast<unsigned long long>(bq) << 5) |
+            (static_cast<unsigned long long>(ip >> 7) << 10) |
+            (static_cast<unsigned long long>(iq >> 7) << 11) |
+            (static_cast<unsigned long long>(ptab[rr][bp] & 255) << 12) |
+            (static_cast<unsigned long long>(ptab[rr][bp] >> 8) << 17) |
+            (static_cast<unsigned long long>(ptab[rr][bq] & 255) << 22) |
+            (static_cast<unsigned long long>(ptab[rr][bq] >> 8) << 27);
+        look[rr][i] = d;
     }
     __syncthreads();
     long long t1 = clock64();
@@ -195,92 +242,100 @@ __global__ void __launch_bounds__(solve_threads<TB>())
         g_jprobe[1] = t1;
     }
     if (work) {
-        // Warp roles per round: lanes 0..NP-1 of warp 0 evaluate the round's
-        // rotations once (the serial FP64 chain); then the MT "M threads"
-        // apply them to one 2x2 block each (M <- R^T M R, double-buffered),
-        // while the QW "Q warps" apply the same rotations to the rows of Q
-        // (Q never feeds back, so it rides along instead of adding rounds).
-        // Per round: phase A = rotation parameters of round rr (lanes of warp
-        // 0) || the M threads prefetch their 2x2 block || the Q warps apply
-        // round rr-1 to Q; barrier; phase B = M threads apply round rr
-        // (double-buffered M); barrier.
-        const bool is_m = tid < MT;
-        const int bi = tid % NP, bj = tid / NP;
-        auto q_update = [&](int r_) {
-            const int r = tid & 31, w = (tid - MT) >> 5;
-            if (r >= TB) return;
-#pragma unroll
-            for (int jj = 0; jj < PPW; ++jj) {
-                const int j = w * PPW + jj;
-                const double c = cs[r_][j], s = sn[r_][j];
-                if (s == 0.0) continue;
-                const int code = ptab[r_][j];
-                const int pcol = code & 255, qcol = code >> 8;
-                const double x = Q[r + pcol * LD], y = Q[r + qcol * LD];
-                Q[r + pcol * LD] = c * x - s * y;
-                Q[r + qcol * LD] = s * x + c * y;
-            }
+        // Roles: MT "M threads" apply round rr to one 2x2 block each
+        // (M <- R^T M R, double-buffered); the Q warps apply it to the rows of
+        // Q; and the lookahead warp (lanes < NP) already evaluates round rr+1's
+        // rotations: it recomputes, from M_rr and round rr's rotations, exactly
+        // the three entries of M_rr+1 each new rotation needs (same xform2x2,
+        // same bits as the M threads). The serial FP64 rotation chain then
+        // overlaps the round's update, and a round costs ONE barrier.
+        const int lane = tid - (MT + QT);
+        auto rot_of = [&](int r, int i, const double* M) {  // initial round only
+            const int code = ptab[r][i];
+            const int p = code & 255, q = code >> 8;
+            const double x = M[p + q * LD];
+            double c = 1.0, s = 0.0;
+            if (fabs(x) > skip_tau) rotation(M[p + p * LD], M[q + q * LD], x, c, s);
+            cs[r][i] = c;
+            sn[r][i] = s;
         };
-        for (int sweep = 0; sweep < max_inner; ++sweep) {
-            for (int rr = 0; rr < TB - 1; ++rr) {
-                const bool pr = probe && rr == 10 && sweep == 0;
-                long long ta = pr ? clock64() : 0;
-                int pi = 0, qi = 0, pj = 0, qj = 0;
-                double m00 = 0, m01 = 0, m10 = 0, m11 = 0;
-                if (is_m) {
-                    const int ci_code = ptab[rr][bi], cj_code = ptab[rr][bj];
-                    pi = ci_code & 255; qi = ci_code >> 8;
-                    pj = cj_code & 255; qj = cj_code >> 8;
-                    m00 = Mc[pi + pj * LD]; m01 = Mc[pi + qj * LD];
-                    m10 = Mc[qi + pj * LD]; m11 = Mc[qi + qj * LD];
-                    if (tid < NP) {  // rotation parameters of pair tid
-                        const double x = bi == bj ? m01 : Mc[pi + qi * LD];
-                        double c = 1.0, s = 0.0;
-                        if (fabs(x) > skip_tau) rotation(Mc[pi + pi * LD], Mc[qi + qi * LD], x, c, s);
-                        cs[rr][tid] = c;
-                        sn[rr][tid] = s;
-                    }
-                } else if (rr > 0 || sweep > 0) {
-                    q_update(rr > 0 ? rr - 1 : TB - 2);
-                }
-                long long tb = pr ? clock64() : 0;
-                __syncthreads();
-                long long tc = pr ? clock64() : 0;
-                if (is_m) {
-                    const double ci = cs[rr][bi], si = sn[rr][bi], cj = cs[rr][bj], sj = sn[rr][bj];
-                    if (sj != 0.0) {  // columns pj, qj
-                        const double a0 = cj * m00 - sj * m01, b0 = sj * m00 + cj * m01;
-                        const double a1 = cj * m10 - sj * m11, b1 = sj * m10 + cj * m11;
-                        m00 = a0; m01 = b0; m10 = a1; m11 = b1;
-                    }
-                    if (si != 0.0) {  // rows pi, qi
-                        const double a0 = ci * m00 - si * m10, b0 = si * m00 + ci * m10;
-                        const double a1 = ci * m01 - si * m11, b1 = si * m01 + ci * m11;
-                        m00 = a0; m10 = b0; m01 = a1; m11 = b1;
-                        if (bi == bj) {  // the rotated pair is annihilated exactly
-                            m01 = 0.0;
-                            m10 = 0.0;
-                        }
-                    }
-                    Mn[pi + pj * LD] = m00;
-                    Mn[pi + qj * LD] = m01;
-                    Mn[qi + pj * LD] = m10;
-                    Mn[qi + qj * LD] = m11;
-                    if (pr) g_jprobe[5] = clock64() - tc;
-                }
-                __syncthreads();
-                if (pr) {
-                    g_jprobe[6] = tb - ta;
-                    g_jprobe[7] = tc - tb;
-                }
-                double* t = Mc;
-                Mc = Mn;
-                Mn = t;
-            }
-        }
-        if (!is_m) q_update(TB - 2);  // the last round's Q update
+        if (lane >= 0 && lane < NP) rot_of(0, lane, Mc);
         __syncthreads();
-        if (probe && work) g_jprobe[2] = clock64();
+        const int total = max_inner * R;
+        for (int it = 0; it < total; ++it) {
+            const int rr = it % R;
+            const bool pr = probe && it == 10;
+            long long ta = pr ? clock64() : 0;
+            if (tid < MT) {
+                const int bi = tid % NP, bj = tid / NP;
+                const int ci_code = ptab[rr][bi], cj_code = ptab[rr][bj];
+                const int pi = ci_code & 255, qi = ci_code >> 8;
+                const int pj = cj_code & 255, qj = cj_code >> 8;
+                double m00 = Mc[pi + pj * LD], m01 = Mc[pi + qj * LD];
+                double m10 = Mc[qi + pj * LD], m11 = Mc[qi + qj * LD];
+                xform2x2(m00, m01, m10, m11, cs[rr][bi], sn[rr][bi], cs[rr][bj], sn[rr][bj], bi == bj);
+                Mn[pi + pj * LD] = m00;
+                Mn[pi + qj * LD] = m01;
+                Mn[qi + pj * LD] = m10;
+                Mn[qi + qj * LD] = m11;
+            } else if (tid < MT + QT) {
+                const int r = tid & 31, w = (tid - MT) >> 5;
+                if (r < TB) {
+#pragma unroll
+                    for (int jj = 0; jj < PPW; ++jj) {
+                        const int j = w * PPW + jj;
+                        const double c = cs[rr][j], s = sn[rr][j];
+                        if (s == 0.0) continue;
+                        const int code = ptab[rr][j];
+                        const int pcol = code & 255, qcol = code >> 8;
+                        const double x = Q[r + pcol * LD], y = Q[r + qcol * LD];
+                        Q[r + pcol * LD] = c * x - s * y;
+                        Q[r + qcol * LD] = s * x + c * y;
+                    }
+                }
+            } else if (lane < NP && it + 1 < total) {
+                // lookahead: rotation `lane` of round nr from M_{rr+1} entries
+                const int nr = (it + 1) % R;
+                const unsigned long long d = look[rr][lane];
+                const int bp = d & 31, bq = (d >> 5) & 31;
+                const int rp = (d >> 10) & 1, rq = (d >> 11) & 1;
+                const int p1 = (d >> 12) & 31, q1 = (d >> 17) & 31;
+                const int p2 = (d >> 22) & 31, q2 = (d >> 27) & 31;
+                const double cp = cs[rr][bp], sp = sn[rr][bp], cq = cs[rr][bq], sq = sn[rr][bq];
+                // diagonal blocks (bp, bp), (bq, bq) and the coupling block (bp, bq)
+                double a00 = Mc[p1 + p1 * LD], a01 = Mc[p1 + q1 * LD];
+                double a10 = Mc[q1 + p1 * LD], a11 = Mc[q1 + q1 * LD];
+                double b00 = Mc[p2 + p2 * LD], b01 = Mc[p2 + q2 * LD];
+                double b10 = Mc[q2 + p2 * LD], b11 = Mc[q2 + q2 * LD];
+                double x00 = Mc[p1 + p2 * LD], x01 = Mc[p1 + q2 * LD];
+                double x10 = Mc[q1 + p2 * LD], x11 = Mc[q1 + q2 * LD];
+                xform2x2(a00, a01, a10, a11, cp, sp, cp, sp, true);
+                xform2x2(b00, b01, b10, b11, cq, sq, cq, sq, true);
+                xform2x2(x00, x01, x10, x11, cp, sp, cq, sq, false);
+                const double app = rp ? a11 : a00;
+                const double aqq = rq ? b11 : b00;
+                const double x = rp ? (rq ? x11 : x10) : (rq ? x01 : x00);
+                long long t1 = pr ? clock64() : 0;
+                double c = 1.0, s = 0.0;
+                if (fabs(x) > skip_tau) rotation(app, aqq, x, c, s);
+                cs[nr][lane] = c;
+                sn[nr][lane] = s;
+                if (pr) {
+                    g_jprobe[3] = t1 - ta;
+                    g_jprobe[4] = clock64() - t1;
+                }
+            }
+            long long tb = pr ? clock64() : 0;
+            __syncthreads();
+            if (pr) {
+                g_jprobe[6] = tb - ta;
+                g_jprobe[7] = clock64() - tb;
+            }
+            double* t = Mc;
+            Mc = Mn;
+            Mn = t;
+        }
+        if (probe) g_jprobe[2] = clock64();
         // The product of ~TB * sweeps rotations drifts from orthogonality by a
         // few hundred ulps; one Newton-Schulz step Q <- Q (3I - Q^T Q) / 2
         // restores it to working precision so that A' = Q^T A Q is a
@@ -294,12 +349,10 @@ __global__ void __launch_bounds__(solve_threads<TB>())
         __syncthreads();
         smem_mma<TB, false>(Q, Mn, T);  // T <- Q (3I - Q^T Q) / 2
         __syncthreads();
-        if (probe && work) g_jprobe[3] = clock64();
         for (int e = tid; e < TB * TB; e += blockDim.x)
             Qbuf[static_cast<size_t>(blockIdx.x) * TB * TB + e] = T[(e % TB) + (e / TB) * LD];
     }
     if (tid == 0) active[blockIdx.x] = work ? 1 : 0;
-    if (probe && work) g_jprobe[4] = clock64();
 }
 
 // ---------------------------------------------------------------------------

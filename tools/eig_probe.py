@@ -9,6 +9,7 @@ from paper_1906_12085_b200.engine import Engine, colmajor  # noqa: E402
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 eng = Engine(0)
+
 torch.cuda.set_stream(eng.stream)
 g = torch.Generator(device="cuda").manual_seed(1)
 x = torch.randn(n, n, dtype=torch.float64, device="cuda", generator=g)
@@ -27,5 +28,5 @@ from paper_1906_12085_b200 import _lib
 buf = (ctypes.c_longlong * 8)()
 _lib.load().svdk_debug_jacobi_probe(buf)
 st = list(buf)
-print("pair_solve CTA0 cycles: load", st[1] - st[0], "rounds", st[2] - st[1], "ns", st[3] - st[2], "store", st[4] - st[3], "| round10: param", st[6], "bar1", st[7], "Mupd", st[5])
+print("pair_solve CTA0 cycles: load", st[1] - st[0], "rounds", st[2] - st[1], "| round10 lookahead: to-barrier", st[6], "(entries", st[3], "rotation", st[4], ") barrier", st[7])
 print("max |dw| / ||S||_F =", float((w - ref).abs().max() / torch.linalg.norm(s)))
