@@ -148,8 +148,8 @@ __device__ long long g_jprobe[8];
 
 template <int TB>
 constexpr int solve_threads() {
-    // M threads (one 2x2 block each) + Q warps (2 pairs each) + 1 lookahead warp
-    return (TB / 2) * (TB / 2) + 32 * (TB / 4) + 32;
+    // M threads (one 2x2 block each) + 1 Q warp (Q in registers) + 1 lookahead warp
+    return (TB / 2) * (TB / 2) + 32 + 32;
 }
 
 // R_i^T B R_j on the 2x2 block B = [[m00, m01], [m10, m11]] of rows (p_i, q_i)
@@ -179,9 +179,8 @@ __global__ void __launch_bounds__(solve_threads<TB>())
     jacobi_pair_solve(double* A, int64_t lda, double* Qbuf, int* active, int nb, int round,
                       double skip_tau, int max_inner) {
     constexpr int B = TB / 2, LD = TB + 4, NP = TB / 2, R = TB - 1;
-    constexpr int MT = NP * NP;        // M threads
-    constexpr int QT = 32 * (TB / 4);  // Q warps' threads
-    constexpr int PPW = NP / (TB / 4);  // pairs per Q warp
+    constexpr int MT = NP * NP;  // M threads
+    constexpr int QT = 32;       // the Q warp: lane l holds column l of Q in registers
     extern __shared__ double sm[];
     double* Mc = sm;             // current M
     double* Mn = Mc + TB * LD;   // next M (double buffer)
@@ -260,6 +259,9 @@ __global__ void __launch_bounds__(solve_threads<TB>())
             sn[r][i] = s;
         };
         if (lane >= 0 && lane < NP) rot_of(0, lane, Mc);
+        double qreg[TB];  // the Q warp's column (lane < TB)
+#pragma unroll
+        for (int i = 0; i < TB; ++i) qreg[i] = (i == ((tid - MT) & 31)) ? 1.0 : 0.0;
         __syncthreads();
         const int total = max_inner * R;
         for (int it = 0; it < total; ++it) {
@@ -279,19 +281,19 @@ __global__ void __launch_bounds__(solve_threads<TB>())
                 Mn[qi + pj * LD] = m10;
                 Mn[qi + qj * LD] = m11;
             } else if (tid < MT + QT) {
-                const int r = tid & 31, w = (tid - MT) >> 5;
-                if (r < TB) {
+                // Q <- Q J: columns p, q of a rotation mix; partner columns are
+                // exchanged by warp shuffles (no shared-memory traffic)
+                const int l = tid - MT;
+                const int code = pinv[rr][l & (TB - 1)];
+                const int j = code & 127, role = code >> 7;
+                const int pq = ptab[rr][j];
+                const int partner = role ? (pq & 255) : (pq >> 8);
+                // branch-free: a skipped pair has (c, s) = (1, 0)
+                const double c = cs[rr][j], b = role ? sn[rr][j] : -sn[rr][j];
 #pragma unroll
-                    for (int jj = 0; jj < PPW; ++jj) {
-                        const int j = w * PPW + jj;
-                        const double c = cs[rr][j], s = sn[rr][j];
-                        if (s == 0.0) continue;
-                        const int code = ptab[rr][j];
-                        const int pcol = code & 255, qcol = code >> 8;
-                        const double x = Q[r + pcol * LD], y = Q[r + qcol * LD];
-                        Q[r + pcol * LD] = c * x - s * y;
-                        Q[r + qcol * LD] = s * x + c * y;
-                    }
+                for (int i = 0; i < TB; ++i) {
+                    const double other = __shfl_sync(0xffffffffu, qreg[i], partner);
+                    qreg[i] = fma(b, other, c * qreg[i]);
                 }
             } else if (lane < NP && it + 1 < total) {
                 // lookahead: rotation `lane` of round nr from M_{rr+1} entries
@@ -335,6 +337,12 @@ __global__ void __launch_bounds__(solve_threads<TB>())
             Mc = Mn;
             Mn = t;
         }
+        if (tid >= MT && tid < MT + TB) {  // Q columns back to shared memory
+            const int l = tid - MT;
+#pragma unroll
+            for (int i = 0; i < TB; ++i) Q[i + l * LD] = qreg[i];
+        }
+        __syncthreads();
         if (probe) g_jprobe[2] = clock64();
         // The product of ~TB * sweeps rotations drifts from orthogonality by a
         // few hundred ulps; one Newton-Schulz step Q <- Q (3I - Q^T Q) / 2
