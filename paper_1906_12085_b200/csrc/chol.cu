@@ -29,6 +29,8 @@ namespace {
 
 constexpr int NB = 64;  // Cholesky panel width (diagonal block factored by one CTA)
 
+__device__ long long g_cprobe[4];  // development probe (svdk_debug_chol_probe)
+
 // Factor the bs x bs diagonal block G[k0.., k0..] (upper part holds the
 // trailing-updated values) as R^T R, write R (upper) and R^-1 (upper).
 // flag |= 1 on a pivot d <= rel_tol * diag0[k] (or d <= 0).
@@ -37,20 +39,26 @@ __global__ void __launch_bounds__(256)
                      double* Rinv, int ldri, const double* diag0, double rel_tol, int* flag) {
     constexpr int LD = NB + 1;
     extern __shared__ double S[];  // NB x LD
-    __shared__ double dinv[NB];
+    __shared__ double dinv[NB], dref[NB];
     const int tid = threadIdx.x;
+    if (tid < bs) dref[tid] = diag0[k0 + tid];  // no global load inside the pivot chain
+    const long long t_start = clock64();
+    // upper triangle is authoritative: coalesced column reads, mirrored in smem
     for (int e = tid; e < bs * bs; e += blockDim.x) {
         const int i = e % bs, j = e / bs;
-        // upper triangle is authoritative; mirror it
-        const int r = min(i, j), c = max(i, j);
-        S[i + j * LD] = G[(k0 + r) + (k0 + c) * ldg];
+        if (i <= j) {
+            const double v = G[(k0 + i) + (k0 + j) * ldg];
+            S[i + j * LD] = v;
+            S[j + i * LD] = v;
+        }
     }
     __syncthreads();
+    long long tl = clock64();
     for (int j = 0; j < bs; ++j) {
         // pivot
         if (tid == 0) {
             const double d = S[j + j * LD];
-            const double ref = diag0[k0 + j];
+            const double ref = dref[j];
             if (!(d > 0.0) || d <= rel_tol * ref) atomicOr(flag, 1);
             const double r = sqrt(fmax(d, 0.0));
             S[j + j * LD] = r;
@@ -61,38 +69,102 @@ __global__ void __launch_bounds__(256)
         for (int c = j + 1 + tid; c < bs; c += blockDim.x) S[j + c * LD] *= inv;
         __syncthreads();
         // trailing update of the upper triangle: S[i][c] -= S[j][i] S[j][c],
-        // j < i <= c; a warp per column, lanes down the rows (no idle lanes
-        // on the lower half)
+        // j < i <= c; a warp per column, lanes down the rows. Every load of
+        // the step is issued before any store (explicit register staging):
+        // otherwise possible smem aliasing serialises load-use-store chains.
         {
-            const int warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
-            for (int cc = j + 1 + warp; cc < bs; cc += nw) {
-                const double sjc = S[j + cc * LD];
-                for (int i = j + 1 + lane; i <= cc; i += 32) S[i + cc * LD] -= S[j + i * LD] * sjc;
+            constexpr int CPW = NB / 8;  // columns per warp (256 threads = 8 warps)
+            const int warp = tid >> 5, lane = tid & 31;
+            double sjc[CPW], sji[2], v[CPW][2];
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                const int i = j + 1 + lane + 32 * r;
+                sji[r] = i < bs ? S[j + i * LD] : 0.0;
+            }
+#pragma unroll
+            for (int k = 0; k < CPW; ++k) {
+                const int cc = j + 1 + warp + 8 * k;
+                sjc[k] = cc < bs ? S[j + cc * LD] : 0.0;
+#pragma unroll
+                for (int r = 0; r < 2; ++r) {
+                    const int i = j + 1 + lane + 32 * r;
+                    v[k][r] = (cc < bs && i <= cc) ? S[i + cc * LD] : 0.0;
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < CPW; ++k) {
+                const int cc = j + 1 + warp + 8 * k;
+#pragma unroll
+                for (int r = 0; r < 2; ++r) {
+                    const int i = j + 1 + lane + 32 * r;
+                    if (cc < bs && i <= cc) S[i + cc * LD] = v[k][r] - sji[r] * sjc[k];
+                }
             }
         }
         __syncthreads();
     }
+    long long tf = clock64();
     // R out (upper, zero strictly-lower)
     for (int e = tid; e < bs * bs; e += blockDim.x) {
         const int i = e % bs, j = e / bs;
         R[(k0 + i) + (k0 + j) * ldr] = i <= j ? S[i + j * LD] : 0.0;
     }
-    // R^-1 by row-step back substitution, parallel over columns: for i from
-    // the bottom, X[i][c] = -(sum_{k=i+1..c} R[i][k] X[k][c]) / R[i][i].
-    // X (upper) is kept transposed in the free strictly-lower part of S:
-    // X[i][c] -> S[c][i] for i < c; its diagonal is dinv.
+    // R^-1 by recursive doubling (log depth instead of a bs-step chain):
+    // invert the 8x8 diagonal blocks (one warp each, a lane per column), then
+    // for s = 8, 16, 32: X_IJ = -X_II (R_IJ X_JJ) for every adjacent pair of
+    // s-blocks, each output entry an independent length-s dot product.
+    // (R's strictly-lower part of S is zeroed so partial blocks stay exact.)
+    double* X = S + NB * LD;   // R^-1, same layout
+    double* T = X + NB * LD;   // scratch R_IJ X_JJ
+    for (int e = tid; e < NB * LD; e += blockDim.x) {
+        X[e] = 0.0;
+        const int i = e % LD, j = e / LD;
+        if (i > j || i >= bs || j >= bs) S[e] = (i == j && i >= bs) ? 1.0 : (i > j || i >= bs || j >= bs ? 0.0 : S[e]);
+    }
     __syncthreads();
-    for (int i = bs - 2; i >= 0; --i) {
-        for (int cc = i + 1 + tid; cc < bs; cc += blockDim.x) {
-            double s = S[i + cc * LD] * dinv[cc];
-            for (int k = i + 1; k < cc; ++k) s = fma(S[i + k * LD], S[cc + k * LD], s);
-            S[cc + i * LD] = -s * dinv[i];
+    {
+        const int warp = tid >> 5, lane = tid & 31;
+        if (lane < 8 && warp < NB / 8) {  // column lane of 8x8 block `warp`
+            const int b0 = warp * 8, cidx = b0 + lane;
+            const double dc = cidx < bs ? dinv[cidx] : 1.0;
+            X[cidx + cidx * LD] = dc;
+            for (int i = cidx - 1; i >= b0; --i) {
+                double sacc = 0.0;
+                for (int k = i + 1; k <= cidx; ++k) sacc = fma(S[i + k * LD], X[k + cidx * LD], sacc);
+                X[i + cidx * LD] = -sacc * (i < bs ? dinv[i] : 1.0);
+            }
+        }
+    }
+    __syncthreads();
+    for (int sz = 8; sz < NB; sz *= 2) {
+        const int pairs = NB / (2 * sz), per = sz * sz;
+        // T = R_IJ X_JJ   (X_JJ upper triangular: k <= col)
+        for (int e = tid; e < pairs * per; e += blockDim.x) {
+            const int pr = e / per, w = e % per, r = w % sz, col = w / sz;
+            const int I = 2 * pr * sz, Jb = I + sz;
+            double acc = 0.0;
+            for (int k = 0; k <= col; ++k) acc = fma(S[(I + r) + (Jb + k) * LD], X[(Jb + k) + (Jb + col) * LD], acc);
+            T[(I + r) + (Jb + col) * LD] = acc;
+        }
+        __syncthreads();
+        // X_IJ = -X_II T   (X_II upper triangular: k >= r)
+        for (int e = tid; e < pairs * per; e += blockDim.x) {
+            const int pr = e / per, w = e % per, r = w % sz, col = w / sz;
+            const int I = 2 * pr * sz, Jb = I + sz;
+            double acc = 0.0;
+            for (int k = r; k < sz; ++k) acc = fma(X[(I + r) + (I + k) * LD], T[(I + k) + (Jb + col) * LD], acc);
+            X[(I + r) + (Jb + col) * LD] = -acc;
         }
         __syncthreads();
     }
     for (int e = tid; e < bs * bs; e += blockDim.x) {
         const int i = e % bs, cc = e / bs;
-        Rinv[i + cc * ldri] = i < cc ? S[cc + i * LD] : (i == cc ? dinv[cc] : 0.0);
+        Rinv[i + cc * ldri] = X[i + cc * LD];
+    }
+    if (tid == 0 && k0 == 0) {
+        g_cprobe[0] = tl - t_start;
+        g_cprobe[1] = tf - tl;
+        g_cprobe[2] = clock64() - tf;
     }
 }
 
@@ -133,7 +205,7 @@ int read_flag(Ctx* c, int idx) {
 bool potrf_upper(Ctx* c, double* G, int64_t ldg, int64_t p, double* R, int64_t ldr,
                  double* Rinv_blocks, double rel_tol) {
     static bool attr = false;
-    const size_t smem = static_cast<size_t>(NB) * (NB + 1) * sizeof(double);
+    const size_t smem = 3 * static_cast<size_t>(NB) * (NB + 1) * sizeof(double);  // S, X, T
     if (!attr) {
         SVDK_CUDA(cudaFuncSetAttribute(chol_diag_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -336,3 +408,7 @@ int64_t qr_thin(Ctx* c, const double* H, int64_t ldh, int64_t m, int64_t p, doub
 }
 
 }  // namespace svdk
+
+extern "C" int svdk_debug_chol_probe(long long* out) {
+    return cudaMemcpyFromSymbol(out, svdk::g_cprobe, 4 * sizeof(long long)) == cudaSuccess ? 0 : 4;
+}

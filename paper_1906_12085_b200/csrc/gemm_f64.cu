@@ -128,6 +128,12 @@ __device__ __forceinline__ Unit decode(const Params& p, int u) {
         while ((tj + 1) * (tj + 2) / 2 <= t) ++tj;
         while (tj * (tj + 1) / 2 > t) --tj;
         ti = t - tj * (tj + 1) / 2;
+    } else if (p.b_upper) {
+        // triangular B: tile cost grows with tj, so walk column-major (all row
+        // tiles of column 0, then column 1, ...): the round-robin CTA schedule
+        // then gives every CTA an even mix of cheap and expensive tiles
+        tj = t / p.tiles_m;
+        ti = t - tj * p.tiles_m;
     } else {
         ti = t / p.tiles_n;
         tj = t - ti * p.tiles_n;

@@ -27,3 +27,8 @@ for nm in eng.ctx.timing_names():
     t = eng.ctx.timing(nm)
     print(f"  {nm}: {t['count']} launches {t['ms']:.2f} ms {t['flops'] / max(t['ms'], 1e-9) / 1e9:.1f} TF/s")
 print("orth", float((q.T @ q - torch.eye(p, dtype=torch.float64, device='cuda')).abs().max()))
+import ctypes
+from paper_1906_12085_b200 import _lib
+buf = (ctypes.c_longlong * 4)()
+_lib.load().svdk_debug_chol_probe(buf)
+print("chol_diag block 0 cycles: load", buf[0], "factor", buf[1], "inverse+store", buf[2])
