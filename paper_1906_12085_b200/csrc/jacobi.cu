@@ -29,6 +29,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <string>
 
 #include "svdk_internal.h"
 
@@ -177,8 +178,12 @@ __device__ __forceinline__ void xform2x2(double& m00, double& m01, double& m10, 
 template <int TB>
 __global__ void __launch_bounds__(solve_threads<TB>())
     jacobi_pair_solve(double* A, int64_t lda, double* Qbuf, int* active, int nb, int round,
-                      double skip_tau, int max_inner) {
-    constexpr int B = TB / 2, LD = TB + 4, NP = TB / 2, R = TB - 1;
+                      double skip_tau, int max_inner, int mode) {
+    // mode 0: all pairs of the 2b subproblem (2b-1 rounds of b rotations);
+    // mode 1: only the pairs inside block I and inside block J (b-1 rounds);
+    // mode 2: only the b^2 cross pairs (i in I, j in J) (b rounds).
+    constexpr int B = TB / 2, LD = TB + 4, NP = TB / 2, RMAX = TB - 1;
+    const int R = mode == 0 ? TB - 1 : (mode == 1 ? B - 1 : B);
     constexpr int MT = NP * NP;  // M threads
     constexpr int QT = 32;       // the Q warp: lane l holds column l of Q in registers
     extern __shared__ double sm[];
@@ -186,10 +191,10 @@ __global__ void __launch_bounds__(solve_threads<TB>())
     double* Mn = Mc + TB * LD;   // next M (double buffer)
     double* Q = Mn + TB * LD;
     double* T = Q + TB * LD;
-    __shared__ int ptab[R][NP];            // round-robin pairs, packed p | q << 8
-    __shared__ unsigned char pinv[R][TB];  // pinv[r][x] = pair of x in round r | role << 7
-    __shared__ unsigned long long look[R][NP];  // lookahead descriptors (see below)
-    __shared__ double cs[R][NP], sn[R][NP];
+    __shared__ int ptab[RMAX][NP];            // inner schedule, packed p | q << 8
+    __shared__ unsigned char pinv[RMAX][TB];  // pinv[r][x] = pair of x in round r | role << 7
+    __shared__ unsigned long long look[RMAX][NP];  // lookahead descriptors (see below)
+    __shared__ double cs[RMAX][NP], sn[RMAX][NP];
     __shared__ int any_applied;
 
     const int tid = threadIdx.x;
@@ -201,7 +206,17 @@ __global__ void __launch_bounds__(solve_threads<TB>())
     for (int e = tid; e < R * NP; e += blockDim.x) {
         int p, q;
         const int r = e / NP, i = e % NP;
-        circle_pair(TB, r, i, p, q);
+        if (mode == 0) {
+            circle_pair(TB, r, i, p, q);
+        } else if (mode == 1) {  // round robin inside each half
+            const int half = NP / 2, blk = i / half;
+            circle_pair(B, r, i % half, p, q);
+            p += blk * B;
+            q += blk * B;
+        } else {  // cross pairs: I_i with J_{(i + r) mod b}
+            p = i;
+            q = B + (i + r) % B;
+        }
         ptab[r][i] = p | (q << 8);
         pinv[r][p] = static_cast<unsigned char>(i);
         pinv[r][q] = static_cast<unsigned char>(i | 128);
@@ -595,10 +610,19 @@ void run_sweeps(Ctx* c, double* A, double* V, int64_t n_pad, int max_sweeps, dou
     const char* inner_env = std::getenv("SVDK_JACOBI_INNER");
     const int max_inner = inner_env ? std::max(1, std::atoi(inner_env)) : 1;
     const int rounds = nb - 1;
+    // Schedule: "split" (default) rotates every index pair exactly once per
+    // sweep, like the reference's cyclic sweep: a first stage diagonalises
+    // pairs inside each b-block (mode 1), then the nb-1 tournament rounds
+    // rotate only the cross pairs of each block pair (mode 2, b inner rounds
+    // instead of 2b-1). "full" (SVDK_JACOBI_SCHEME=full) re-rotates the
+    // in-block pairs in every round (mode 0).
+    const char* scheme_env = std::getenv("SVDK_JACOBI_SCHEME");
+    const bool split = !(scheme_env && std::string(scheme_env) == "full");
+    const int slots = rounds + (split ? 1 : 0);
     // Every round of a sweep keeps its own Q_p set, so the V chain on the side
     // stream can lag behind the A chain by any number of rounds.
-    DBuf qbuf(c, static_cast<size_t>(rounds) * k * TB * TB);
-    DBuf act(c, static_cast<size_t>(rounds) * k);
+    DBuf qbuf(c, static_cast<size_t>(slots) * k * TB * TB);
+    DBuf act(c, static_cast<size_t>(slots) * k);
     int* active = reinterpret_cast<int*>(act.p());
     const int a_ctas = k * (k + 1) / 2, v_ctas = static_cast<int>(n_pad / TB) * k;
     if (!c->aux_stream) {
@@ -608,11 +632,21 @@ void run_sweeps(Ctx* c, double* A, double* V, int64_t n_pad, int max_sweeps, dou
     }
     cudaStream_t S = c->stream, S2 = c->aux_stream;
     auto enqueue_sweep = [&] {
+        if (split) {  // in-block stage on the round-0 block pairing
+            double* qr = qbuf.p() + static_cast<size_t>(rounds) * k * TB * TB;
+            int* ar = active + static_cast<size_t>(rounds) * k;
+            jacobi_pair_solve<TB><<<k, nthreads_solve, smem_solve, S>>>(A, n_pad, qr, ar, nb, 0, skip_tau,
+                                                                        max_inner, 1);
+            SVDK_CUDA(cudaEventRecord(c->aux_ev[0], S));
+            SVDK_CUDA(cudaStreamWaitEvent(S2, c->aux_ev[0], 0));
+            jacobi_update_v<TB><<<v_ctas, 256, smem_v, S2>>>(V, n_pad, qr, ar, nb, 0);
+            jacobi_update_a<TB><<<a_ctas, 256, smem_a, S>>>(A, n_pad, qr, ar, nb, 0);
+        }
         for (int r = 0; r < rounds; ++r) {
             double* qr = qbuf.p() + static_cast<size_t>(r) * k * TB * TB;
             int* ar = active + static_cast<size_t>(r) * k;
             jacobi_pair_solve<TB><<<k, nthreads_solve, smem_solve, S>>>(A, n_pad, qr, ar, nb, r, skip_tau,
-                                                             max_inner);
+                                                             max_inner, split ? 2 : 0);
             SVDK_CUDA(cudaEventRecord(c->aux_ev[0], S));
             SVDK_CUDA(cudaStreamWaitEvent(S2, c->aux_ev[0], 0));
             jacobi_update_v<TB><<<v_ctas, 256, smem_v, S2>>>(V, n_pad, qr, ar, nb, r);
@@ -643,7 +677,7 @@ void run_sweeps(Ctx* c, double* A, double* V, int64_t n_pad, int max_sweeps, dou
                 enqueue_sweep();
                 SVDK_CHECK_LAUNCH();
             }
-            c->launches += 3 * rounds;
+            c->launches += 3 * slots;
             ++sweeps;
             off = std::sqrt(2.0 * device_sumsq(c, A, n_pad, 1, scratch));
         }
