@@ -42,7 +42,7 @@ __global__ void __launch_bounds__(256)
     __shared__ double dinv[NB], dref[NB];
     const int tid = threadIdx.x;
     if (tid < bs) dref[tid] = diag0[k0 + tid];  // no global load inside the pivot chain
-    const long long t_start = clock64();
+    const long long t_start = SVDK_CLOCK();
     // upper triangle is authoritative: coalesced column reads, mirrored in smem
     for (int e = tid; e < bs * bs; e += blockDim.x) {
         const int i = e % bs, j = e / bs;
@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(256)
         }
     }
     __syncthreads();
-    long long tl = clock64();
+    long long tl = SVDK_CLOCK();
     for (int j = 0; j < bs; ++j) {
         // pivot
         if (tid == 0) {
@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(256)
         }
         __syncthreads();
     }
-    long long tf = clock64();
+    long long tf = SVDK_CLOCK();
     // R out (upper, zero strictly-lower)
     for (int e = tid; e < bs * bs; e += blockDim.x) {
         const int i = e % bs, j = e / bs;
@@ -162,9 +162,9 @@ __global__ void __launch_bounds__(256)
         Rinv[i + cc * ldri] = X[i + cc * LD];
     }
     if (tid == 0 && k0 == 0) {
-        g_cprobe[0] = tl - t_start;
-        g_cprobe[1] = tf - tl;
-        g_cprobe[2] = clock64() - tf;
+        SVDK_PROBE_STORE(g_cprobe, 0, tl - t_start);
+        SVDK_PROBE_STORE(g_cprobe, 1, tf - tl);
+        SVDK_PROBE_STORE(g_cprobe, 2, SVDK_CLOCK() - tf);
     }
 }
 

@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(solve_threads<TB>())
 
     const int tid = threadIdx.x;
     const bool probe = blockIdx.x == 0 && tid == MT + QT && round == 5;
-    long long t0 = clock64();
+    long long t0 = SVDK_CLOCK();
     int I, J;
     circle_pair(nb, round, blockIdx.x, I, J);
     if (tid == 0) any_applied = 0;
@@ -249,11 +249,11 @@ __global__ void __launch_bounds__(solve_threads<TB>())
         look[rr][i] = d;
     }
     __syncthreads();
-    long long t1 = clock64();
+    long long t1 = SVDK_CLOCK();
     const bool work = any_applied != 0;
     if (probe && work) {
-        g_jprobe[0] = t0;
-        g_jprobe[1] = t1;
+        SVDK_PROBE_STORE(g_jprobe, 0, t0);
+        SVDK_PROBE_STORE(g_jprobe, 1, t1);
     }
     if (work) {
         // Roles: MT "M threads" apply round rr to one 2x2 block each
@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(solve_threads<TB>())
         for (int it = 0; it < total; ++it) {
             const int rr = it % R;
             const bool pr = probe && it == 10;
-            long long ta = pr ? clock64() : 0;
+            long long ta = pr ? SVDK_CLOCK() : 0;
             if (tid < MT) {
                 const int bi = tid % NP, bj = tid / NP;
                 const int ci_code = ptab[rr][bi], cj_code = ptab[rr][bj];
@@ -332,21 +332,21 @@ __global__ void __launch_bounds__(solve_threads<TB>())
                 const double app = rp ? a11 : a00;
                 const double aqq = rq ? b11 : b00;
                 const double x = rp ? (rq ? x11 : x10) : (rq ? x01 : x00);
-                long long t1 = pr ? clock64() : 0;
+                long long t1 = pr ? SVDK_CLOCK() : 0;
                 double c = 1.0, s = 0.0;
                 if (fabs(x) > skip_tau) rotation(app, aqq, x, c, s);
                 cs[nr][lane] = c;
                 sn[nr][lane] = s;
                 if (pr) {
-                    g_jprobe[3] = t1 - ta;
-                    g_jprobe[4] = clock64() - t1;
+                    SVDK_PROBE_STORE(g_jprobe, 3, t1 - ta);
+                    SVDK_PROBE_STORE(g_jprobe, 4, SVDK_CLOCK() - t1);
                 }
             }
-            long long tb = pr ? clock64() : 0;
+            long long tb = pr ? SVDK_CLOCK() : 0;
             __syncthreads();
             if (pr) {
-                g_jprobe[6] = tb - ta;
-                g_jprobe[7] = clock64() - tb;
+                SVDK_PROBE_STORE(g_jprobe, 6, tb - ta);
+                SVDK_PROBE_STORE(g_jprobe, 7, SVDK_CLOCK() - tb);
             }
             double* t = Mc;
             Mc = Mn;
@@ -358,7 +358,7 @@ __global__ void __launch_bounds__(solve_threads<TB>())
             for (int i = 0; i < TB; ++i) Q[i + l * LD] = qreg[i];
         }
         __syncthreads();
-        if (probe) g_jprobe[2] = clock64();
+        if (probe) SVDK_PROBE_STORE(g_jprobe, 2, SVDK_CLOCK());
         // The product of ~TB * sweeps rotations drifts from orthogonality by a
         // few hundred ulps; one Newton-Schulz step Q <- Q (3I - Q^T Q) / 2
         // restores it to working precision so that A' = Q^T A Q is a

@@ -37,6 +37,16 @@ struct Failure {
 
 #define SVDK_CHECK_LAUNCH() SVDK_CUDA(cudaGetLastError())
 
+// Development timing probes inside kernels (clock64 stamps read back by the
+// svdk_debug_* hooks); compiled out unless built with -DSVDK_PROBES.
+#ifdef SVDK_PROBES
+#define SVDK_CLOCK() clock64()
+#define SVDK_PROBE_STORE(arr, i, v) ((arr)[i] = (v))
+#else
+#define SVDK_CLOCK() 0LL
+#define SVDK_PROBE_STORE(arr, i, v) ((void)(v))
+#endif
+
 // ---------------------------------------------------------------------------
 // Device memory pool: stream-ordered reuse on the context's single stream.
 // ---------------------------------------------------------------------------

@@ -1,0 +1,25 @@
+"""Small-shape exercise of every engine path, for compute-sanitizer runs."""
+import sys
+
+import numpy as np
+
+sys.path.insert(0, ".")
+from paper_1906_12085_b200 import svdkit as sk  # noqa: E402
+
+rng = np.random.default_rng(0)
+for m, n in ((37, 13), (130, 66), (300, 129)):
+    a = np.asfortranarray(rng.standard_normal((m, n)))
+    sk.gram(a)
+    sk.matmul(a, rng.standard_normal((n, 7)))
+    sk.matmul_transposed_left(a, rng.standard_normal((m, 5)))
+    sk.qr_thin(a)
+    x = rng.standard_normal((n, n))
+    sk.eig_sym(x + x.T)
+    s = sk.truncated_svd(a)
+    sk.randomized_pca(a, sk.MethodParams(n // 2, 2, sk.RngSeed(1)))
+    sk.krylov_svd(a, sk.MethodParams(4, 2, sk.RngSeed(1)))
+    sk.lanczos_svd(a, 0, sk.RngSeed(1))
+    sk.fit_pca(a, sk.Orientation.RowsAreExamples, sk.SvdMethod.Randomized, sk.MethodParams(n, 1, sk.RngSeed(2)))
+    sk.residual_delta(a, s)
+sk.qr_thin(np.zeros((20, 4)))
+print("sanitize probe done")
