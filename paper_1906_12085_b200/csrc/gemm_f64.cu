@@ -30,6 +30,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "svdk_internal.h"
 
@@ -63,6 +64,7 @@ struct Params {
     double alpha;  // out = alpha * (op(A) B) [+ C_old when beta_one]
     int beta_one;
     int b_upper;   // B is upper triangular: tile (., col0) only needs k < col0 + BN
+    int a_tma3;    // M-major A via one 3-D box per stage (M % 16 == 0) instead of 8 2-D boxes
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -97,6 +99,16 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
         "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
         " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
         "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+// 3-D box: (m_lo 16, k 16, m_hi 8) lands as m_lo*8 + k*128 + m_hi*2048 bytes,
+// the same swizzled layout the eight 2-D 16x16 boxes produce.
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1, int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
         : "memory");
 }
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
@@ -215,7 +227,10 @@ __global__ void __launch_bounds__(THREADS, 1)
                     mbar_wait(&empty[stage], phase ^ 1);
                     mbar_expect_tx(&full[stage], w.diag ? TILE_BYTES : 2 * TILE_BYTES);
                     uint8_t* da = smA + stage * TILE_BYTES;
-                    if (AMM) {
+                    if (AMM && p.a_tma3) {
+                        tma_load_3d(da, &mapA, &full[stage], 0, static_cast<int>(k),
+                                    static_cast<int>(w.row0 >> 4));
+                    } else if (AMM) {
 #pragma unroll
                         for (int b = 0; b < BM / 16; ++b)
                             tma_load_2d(da + b * 2048, &mapA, &full[stage],
@@ -380,6 +395,23 @@ CUtensorMap make_map(const double* base, int64_t rows, int64_t cols, int64_t ld,
     return m;
 }
 
+// 3-D view of an M-major operand with rows % 16 == 0: dims (16, cols, rows/16),
+// box (16, BK, BM/16), so one TMA fills a whole BM x BK stage.
+CUtensorMap make_map_mmajor3(const double* base, int64_t rows, int64_t cols, int64_t ld) {
+    CUtensorMap m;
+    cuuint64_t dims[3] = {16, static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows / 16)};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld) * 8, 128};
+    cuuint32_t box[3] = {16, BK, BM / 16};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base),
+                             dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        fail(SVDK_E_CUDA, "cuTensorMapEncodeTiled (3d) failed: " + std::to_string(r));
+    return m;
+}
+
 // Pick the k-split count S so (tiles x S) fills whole waves of the SMs.
 int choose_splits(int n_tiles, int64_t K, int sms) {
     const int64_t k_steps = ceil_div(K, BK);
@@ -524,7 +556,14 @@ void gemm(Ctx* c, bool transa, int64_t m, int64_t n, int64_t k, const double* A,
     p.beta_one = beta_one ? 1 : 0;
     p.b_upper = b_upper ? 1 : 0;
     if (nonfinite_check) p.flag = c->d_flags;  // sticky; see raise_if_nonfinite()
-    const CUtensorMap ma = transa ? make_map(A, k, m, lda, BK, BM) : make_map(A, m, k, lda, 16, BK);
+    static const bool tma3 = [] {
+        const char* e = std::getenv("SVDK_NN_TMA3");
+        return !(e && e[0] == '0');
+    }();
+    p.a_tma3 = (!transa && tma3 && m % 16 == 0) ? 1 : 0;
+    const CUtensorMap ma = transa     ? make_map(A, k, m, lda, BK, BM)
+                           : p.a_tma3 ? make_map_mmajor3(A, m, k, lda)
+                                      : make_map(A, m, k, lda, 16, BK);
     const CUtensorMap mb = make_map(B, k, n, ldb, BK, BN);
     launch(c, p, ma, mb);
 }

@@ -119,6 +119,32 @@ __global__ void sub_colmean_kernel(const double* A, int64_t lda, int64_t m, int6
     }
 }
 
+// dst = A - mean (per column) fused with the sum of squares of the centred
+// values (pca.cpp:57-59 total variance) — one HBM pass instead of two.
+// Per-block partials, reduced afterwards in fixed order (deterministic).
+__global__ void sub_colmean_sumsq_kernel(const double* A, int64_t lda, int64_t m, int64_t n,
+                                         const double* mean, double* dst, int64_t ldd,
+                                         double* partial) {
+    __shared__ double red[32];
+    double s = 0.0;
+    for (int64_t j = blockIdx.y; j < n; j += gridDim.y) {
+        const double mu = mean[j];
+        for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < m;
+             i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+            const double x = A[i + j * lda] - mu;
+            dst[i + j * ldd] = x;
+            s = fma(x, x, s);
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (blockDim.x >> 5); ++w) s += red[w];
+        partial[blockIdx.x + static_cast<int64_t>(blockIdx.y) * gridDim.x] = s;
+    }
+}
+
 // Row means (ColumnsAreExamples): mean_i = sum_j a_ij / n, j ascending.
 __global__ void rowmean_kernel(const double* A, int64_t lda, int64_t m, int64_t n, double* mean) {
     const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
@@ -251,6 +277,23 @@ void subtract_column_means(Ctx* c, const double* A, int64_t lda, int64_t m, int6
                                                                      ldd);
     SVDK_CHECK_LAUNCH();
     c->launches++;
+}
+
+void subtract_column_means_sumsq(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n,
+                                 const double* d_mean, double* dst, int64_t ldd, double* d_sumsq) {
+    if (m <= 0 || n <= 0) {
+        fill(c, d_sumsq, 1, 0.0);
+        return;
+    }
+    // fewer column blocks than the plain subtract so the partials stay small
+    const dim3 g(static_cast<unsigned>(std::min<int64_t>(ceil_div(m, 256), 2 * c->num_sms)),
+                 static_cast<unsigned>(std::min<int64_t>(n, 256)));
+    DBuf partial(c, static_cast<size_t>(g.x) * g.y);
+    sub_colmean_sumsq_kernel<<<g, 256, 0, c->stream>>>(A, lda, m, n, d_mean, dst, ldd, partial.p());
+    SVDK_CHECK_LAUNCH();
+    sum_partials_kernel<<<1, 256, 0, c->stream>>>(partial.p(), static_cast<int>(g.x * g.y), d_sumsq);
+    SVDK_CHECK_LAUNCH();
+    c->launches += 2;
 }
 
 void center_rows_are_examples(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n,

@@ -151,17 +151,20 @@ void dev_pca(Ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, int met
         } else {
             column_sums(c, A, lda, m, n, mg, mean);
         }
+        // centring fused with the total variance (pca.cpp:57-59) in one pass
         if (center_in_place) {
-            subtract_column_means(c, A, lda, m, n, mean, const_cast<double*>(A), lda);
+            subtract_column_means_sumsq(c, A, lda, m, n, mean, const_cast<double*>(A), lda,
+                                        d_total.p());
         } else {
-            subtract_column_means(c, A, lda, m, n, mean, C.p(), ldc);
+            subtract_column_means_sumsq(c, A, lda, m, n, mean, C.p(), ldc, d_total.p());
             X = C.p();
             ldx = ldc;
         }
+        if (comm && world > 1) comm->allreduce(d_total.p(), 1);
     } else {
         fill(c, mean, n, 0.0);
+        frob_sq_rows_dev(c, X, ldx, m, n, d_total.p(), comm);  // pca.cpp:57-59
     }
-    frob_sq_rows_dev(c, X, ldx, m, n, d_total.p(), comm);  // pca.cpp:57-59
     int64_t r = 0;
     switch (method) {
         case SVDK_TRUNCATED:

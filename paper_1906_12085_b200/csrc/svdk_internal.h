@@ -193,6 +193,9 @@ void column_sums(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n, dou
                  double* d_out);
 void subtract_column_means(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n,
                            const double* d_mean, double* dst, int64_t ldd);
+// the same, fused with sum_ij dst_ij^2 into a device scalar
+void subtract_column_means_sumsq(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n,
+                                 const double* d_mean, double* dst, int64_t ldd, double* d_sumsq);
 void center_cols_are_examples(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n,
                               double* dst, int64_t ldd, double* d_mean);
 
