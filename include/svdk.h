@@ -16,6 +16,7 @@
  *      SVDK_E_DIM       -> DimensionError
  *      SVDK_E_PARAM     -> ParamError
  *      SVDK_E_NUMERICAL -> NumericalError (residual via svdk_last_residual())
+ *      SVDK_E_FORMAT    -> FormatError,  SVDK_E_IO -> IoError
  *    plus engine-only failures (CUDA, NCCL, allocation, bad state). The
  *    message is in svdk_last_error() (thread-local).
  *  - A context owns one GPU, one CUDA stream and a device memory pool. It
@@ -41,7 +42,9 @@ enum {
     SVDK_E_CUDA = 4,
     SVDK_E_NCCL = 5,
     SVDK_E_NOMEM = 6,
-    SVDK_E_STATE = 7
+    SVDK_E_STATE = 7,
+    SVDK_E_FORMAT = 8, /* -> FormatError (byte offset via the call's out-parameter) */
+    SVDK_E_IO = 9      /* -> IoError */
 };
 
 /* svd_methods.hpp:13 SvdMethod (+ Lanczos, new in this engine) */
@@ -140,6 +143,40 @@ int svdk_fit_pca(svdk_ctx* ctx, const double* data, int64_t m, int64_t n, int or
 int svdk_residual_delta(svdk_ctx* ctx, const double* a, int64_t m, int64_t n, const double* u,
                         const double* sigma, const double* v, int64_t r, double* delta);
 
+/* ---- cost model (cost_model.cpp:30-113; host-only, no context) ----
+ * Modeled flops and space (8-byte entries, input included; bytes = 8 * entries)
+ * of one factorization, the published closed forms:
+ *   SVDK_COST_TRUNCATED            truncated_cost(m, n)
+ *   SVDK_COST_RANDOMIZED           randomized_cost(m, n, l, i)        (i >= 0)
+ *   SVDK_COST_RANDOMIZED_PRACTICAL randomized_cost_practical(m, n)    (l = n/2, i = 1)
+ *   SVDK_COST_KRYLOV               krylov_cost(m, n, l, i)            (i >= 1)
+ *   SVDK_COST_KRYLOV_PRACTICAL     krylov_cost_practical(m, n)
+ *   SVDK_COST_KRYLOV_PER_STEP      krylov_cost_per_step(m, n, l, i)
+ * l and i are ignored by the models without them. Domain violations
+ * (m >= n >= l >= 1) return SVDK_E_PARAM. */
+enum {
+    SVDK_COST_TRUNCATED = 0,
+    SVDK_COST_RANDOMIZED = 1,
+    SVDK_COST_RANDOMIZED_PRACTICAL = 2,
+    SVDK_COST_KRYLOV = 3,
+    SVDK_COST_KRYLOV_PRACTICAL = 4,
+    SVDK_COST_KRYLOV_PER_STEP = 5
+};
+int svdk_cost_model(int model, uint64_t m, uint64_t n, uint64_t l, uint64_t i, double* flops,
+                    double* space_entries, double* space_bytes);
+
+/* ---- IDX image ingestion (idx_io.cpp:24-107) ----
+ * svdk_idx_parse: validate a rank-3 unsigned-byte IDX buffer (big-endian magic
+ * 0x00000803, three big-endian u32 dims, then count*height*width bytes, nothing
+ * after). On success dims = {count, height, width} and the pixels start at
+ * bytes + 16. On SVDK_E_FORMAT *error_offset is FormatError::offset(). Host-only.
+ * svdk_idx_to_matrix: images_to_matrix — count x (height*width) column-major,
+ * entry (i, p) = pixels[i * P + p] / 255 (rows are examples), expanded on the
+ * GPU from the 1-byte pixels (8x less host->device traffic than the doubles). */
+int svdk_idx_parse(const uint8_t* bytes, uint64_t len, uint64_t dims[3], uint64_t* error_offset);
+int svdk_idx_to_matrix(svdk_ctx* ctx, const uint8_t* pixels, int64_t count,
+                       int64_t pixels_per_image, double* out);
+
 /* ---- device-pointer entry points (inputs already resident in HBM) ---- */
 int svdk_dev_gemm(svdk_ctx* ctx, int transa, int64_t m, int64_t n, int64_t k, const double* a,
                   int64_t lda, const double* b, int64_t ldb, double* c, int64_t ldc);
@@ -159,6 +196,9 @@ int svdk_dev_pca(svdk_ctx* ctx, const double* a, int64_t m_local, int64_t n, int
                  int method, int64_t l, int64_t q, uint64_t seed, int center, double threshold,
                  double* u, int64_t ldu, double* sigma, double* v, int64_t ldv, double* mean,
                  int64_t* rank, int64_t* k, double* total);
+/* images_to_matrix on device buffers: out (count x P, ldo >= count) */
+int svdk_dev_idx_to_matrix(svdk_ctx* ctx, const uint8_t* pixels, int64_t count,
+                           int64_t pixels_per_image, double* out, int64_t ldo);
 
 #ifdef __cplusplus
 }

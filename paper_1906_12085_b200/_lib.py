@@ -13,7 +13,8 @@ import threading
 from .errors import EngineError, raise_for_status
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsvdk.so")
+# SVDK_LIB: development override (e.g. a -DSVDK_PROBES build under build/)
+LIB_PATH = os.environ.get("SVDK_LIB") or os.path.join(_HERE, "libsvdk.so")
 
 _i64 = C.c_int64
 _u64 = C.c_uint64

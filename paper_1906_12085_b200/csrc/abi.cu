@@ -24,6 +24,13 @@ int64_t lanczos_svd(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n, 
 int64_t qr_thin(Ctx* c, const double* H, int64_t ldh, int64_t m, int64_t p, double* Q, int64_t ldq,
                 double* R, const RowComm* comm, double* Rinv_last = nullptr);
 int64_t select_components(Ctx* c, const double* d_w, int64_t count, double total, double t);
+struct CostOut {
+    double flops = 0.0, entries = 0.0;
+};
+CostOut cost_model(int model, uint64_t m, uint64_t n, uint64_t l, uint64_t i);
+void idx_parse(const uint8_t* bytes, uint64_t len, uint64_t dims[3], uint64_t* err_offset);
+void idx_to_matrix_dev(Ctx* c, const uint8_t* px, int64_t count, int64_t P, double* out,
+                       int64_t ldo);
 }  // namespace svdk
 
 using namespace svdk;
@@ -626,6 +633,48 @@ int svdk_ctx_attach_nccl(svdk_ctx* c, const char id[128], int rank, int world) {
     return guarded([&] {
         need_ctx(c);
         attach_nccl(c, id, rank, world);
+    });
+}
+
+int svdk_cost_model(int model, uint64_t m, uint64_t n, uint64_t l, uint64_t i, double* flops,
+                    double* space_entries, double* space_bytes) {
+    return guarded([&] {
+        const CostOut c = cost_model(model, m, n, l, i);
+        if (flops) *flops = c.flops;
+        if (space_entries) *space_entries = c.entries;
+        if (space_bytes) *space_bytes = 8.0 * c.entries;
+    });
+}
+
+int svdk_idx_parse(const uint8_t* bytes, uint64_t len, uint64_t dims[3], uint64_t* error_offset) {
+    return guarded([&] {
+        if (!bytes && len > 0) fail(SVDK_E_PARAM, "idx_parse: null buffer");
+        idx_parse(bytes, len, dims, error_offset);
+    });
+}
+
+int svdk_idx_to_matrix(svdk_ctx* c, const uint8_t* pixels, int64_t count, int64_t pixels_per_image,
+                       double* out) {
+    return guarded([&] {
+        need_ctx(c);
+        if (count < 0 || pixels_per_image < 0) fail(SVDK_E_PARAM, "idx_to_matrix: negative size");
+        const int64_t bytes = count * pixels_per_image;
+        if (bytes == 0) return;
+        DBuf dpx(c, static_cast<size_t>(ceil_div(bytes, 8)));
+        DBuf dout(c, static_cast<size_t>(bytes));
+        SVDK_CUDA(cudaMemcpyAsync(dpx.p(), pixels, static_cast<size_t>(bytes),
+                                  cudaMemcpyHostToDevice, c->stream));
+        idx_to_matrix_dev(c, reinterpret_cast<const uint8_t*>(dpx.p()), count, pixels_per_image,
+                          dout.p(), count);
+        d2h(c, out, dout.p(), bytes);
+    });
+}
+
+int svdk_dev_idx_to_matrix(svdk_ctx* c, const uint8_t* pixels, int64_t count,
+                           int64_t pixels_per_image, double* out, int64_t ldo) {
+    return guarded([&] {
+        need_ctx(c);
+        idx_to_matrix_dev(c, pixels, count, pixels_per_image, out, ldo);
     });
 }
 

@@ -470,6 +470,154 @@ __global__ void __launch_bounds__(256)
     }
 }
 
+// Register-resident variants for 2b = 32 (used for every n > 64). One WARP
+// owns one 32 x 32 block and never touches shared memory: the operands are
+// loaded straight into m8n8k4 fragments (A rows: 8 consecutive doubles of a
+// column per lane quad -> full 32 B sectors), the intermediate U = Q_p^T X of
+// the two-sided product is re-laid from accumulator to A-fragment form with
+// quad shuffles, and results are stored from the accumulators. No barriers,
+// and every warp keeps its whole 8 KB tile in flight, so the kernels run at
+// HBM rate instead of the load -> sync -> compute -> sync chain of the
+// shared-memory versions above.
+//
+// Fragment maps (mma.m8n8k4.row.col, lane = 4 r + kq):
+//   A[m][k]: A[r][kq]     B[k][n]: B[kq][r]     C: C[r][2 kq], C[r][2 kq + 1]
+__device__ __forceinline__ double q_frag(const double* Qp, bool act, int k, int n) {
+    // Q[k][n] of a column-major 32 x 32 rotation, identity when inactive
+    return act ? Qp[k + n * 32] : (k == n ? 1.0 : 0.0);
+}
+
+constexpr int UPD_WARPS = 4;
+
+// A[IJ_p, IJ_q] <- Q_p^T A[IJ_p, IJ_q] Q_q for one (p <= q) per warp; the
+// mirror block gets the same values (exact symmetry); a diagonal pair block
+// copies its upper triangle to the lower one.
+__global__ void __launch_bounds__(UPD_WARPS * 32)
+    jacobi_update_a_reg(double* A, int64_t lda, const double* Qbuf, const int* active, int nb,
+                        int round) {
+    constexpr int B = 16;
+    const int lane = threadIdx.x & 31, r = lane >> 2, kq = lane & 3;
+    const int k = nb / 2;
+    const int u = blockIdx.x * UPD_WARPS + (threadIdx.x >> 5);
+    if (u >= k * (k + 1) / 2) return;
+    int q = static_cast<int>((sqrt(8.0 * u + 1.0) - 1.0) * 0.5);
+    while ((q + 1) * (q + 2) / 2 <= u) ++q;
+    while (q * (q + 1) / 2 > u) --q;
+    const int p = u - q * (q + 1) / 2;
+    const bool ap = active[p] != 0, aq = active[q] != 0;
+    if (!(ap | aq)) return;
+    int Ip, Jp, Iq, Jq;
+    circle_pair(nb, round, p, Ip, Jp);
+    circle_pair(nb, round, q, Iq, Jq);
+    const double* Qa = Qbuf + static_cast<size_t>(p) * 1024;
+    const double* Qb = Qbuf + static_cast<size_t>(q) * 1024;
+    // step 1: U = Q_p^T X. A-frags (Q_p^T)[m][k] = Q_p[k][m]; B-frags X[k][n].
+    double xa[8][4], xb[8][4];
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+        const int64_t row = gidx(B, Ip, Jp, 4 * s + kq);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            xb[s][t] = A[row + gidx(B, Iq, Jq, 8 * t + r) * lda];
+            xa[s][t] = q_frag(Qa, ap, 4 * s + kq, 8 * t + r);
+        }
+    }
+    double acc[4][4][2];
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+#pragma unroll
+        for (int t = 0; t < 4; ++t) acc[m][t][0] = acc[m][t][1] = 0.0;
+#pragma unroll
+    for (int s = 0; s < 8; ++s)
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+#pragma unroll
+            for (int t = 0; t < 4; ++t) dmma(acc[m][t][0], acc[m][t][1], xa[s][m], xb[s][t]);
+    // step 2: X' = U Q_q. U[8m + r][4s + kq] lives in lane (r, 2(s&1) + kq/2),
+    // register acc[m][s/2][kq&1].
+    double qb[8][4];
+#pragma unroll
+    for (int s = 0; s < 8; ++s)
+#pragma unroll
+        for (int t = 0; t < 4; ++t) qb[s][t] = q_frag(Qb, aq, 4 * s + kq, 8 * t + r);
+    double out[4][4][2];
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+#pragma unroll
+        for (int t = 0; t < 4; ++t) out[m][t][0] = out[m][t][1] = 0.0;
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+        const int src = (lane & ~3) | (2 * (s & 1) + (kq >> 1));
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+            const double v0 = __shfl_sync(0xffffffffu, acc[m][s >> 1][0], src);
+            const double v1 = __shfl_sync(0xffffffffu, acc[m][s >> 1][1], src);
+            const double a = (kq & 1) ? v1 : v0;
+#pragma unroll
+            for (int t = 0; t < 4; ++t) dmma(out[m][t][0], out[m][t][1], a, qb[s][t]);
+        }
+    }
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+        const int li = 8 * m + r;
+        const int64_t gi = gidx(B, Ip, Jp, li);
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const int lj = 8 * t + 2 * kq + i;
+                const int64_t gj = gidx(B, Iq, Jq, lj);
+                if (p == q && li > lj) continue;
+                A[gi + gj * lda] = out[m][t][i];
+                A[gj + gi * lda] = out[m][t][i];
+            }
+    }
+}
+
+// V[rows, IJ_q] <- V[rows, IJ_q] Q_q; one warp per (32-row tile, pair q).
+__global__ void __launch_bounds__(UPD_WARPS * 32)
+    jacobi_update_v_reg(double* V, int64_t ldv, int64_t n_rows, const double* Qbuf,
+                        const int* active, int nb, int round) {
+    constexpr int B = 16;
+    const int lane = threadIdx.x & 31, r = lane >> 2, kq = lane & 3;
+    const int k = nb / 2;
+    const int64_t u = static_cast<int64_t>(blockIdx.x) * UPD_WARPS + (threadIdx.x >> 5);
+    const int q = static_cast<int>(u % k);
+    const int64_t row0 = (u / k) * 32;
+    if (row0 >= n_rows || !active[q]) return;
+    int Iq, Jq;
+    circle_pair(nb, round, q, Iq, Jq);
+    const double* Qb = Qbuf + static_cast<size_t>(q) * 1024;
+    double va[4][8], qb[8][4];
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+        const int64_t col = gidx(B, Iq, Jq, 4 * s + kq) * ldv;
+#pragma unroll
+        for (int m = 0; m < 4; ++m) va[m][s] = V[row0 + 8 * m + r + col];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) qb[s][t] = Qb[(4 * s + kq) + (8 * t + r) * 32];
+    }
+    double acc[4][4][2];
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+#pragma unroll
+        for (int t = 0; t < 4; ++t) acc[m][t][0] = acc[m][t][1] = 0.0;
+#pragma unroll
+    for (int s = 0; s < 8; ++s)
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+#pragma unroll
+            for (int t = 0; t < 4; ++t) dmma(acc[m][t][0], acc[m][t][1], va[m][s], qb[s][t]);
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const int64_t col = gidx(B, Iq, Jq, 8 * t + 2 * kq + i) * ldv;
+#pragma unroll
+            for (int m = 0; m < 4; ++m) V[row0 + 8 * m + r + col] = acc[m][t][i];
+        }
+}
+
 // ---------------------------------------------------------------------------
 // setup / checks / finish
 // ---------------------------------------------------------------------------
@@ -631,6 +779,22 @@ void run_sweeps(Ctx* c, double* A, double* V, int64_t n_pad, int max_sweeps, dou
         SVDK_CUDA(cudaEventCreateWithFlags(&c->aux_ev[1], cudaEventDisableTiming));
     }
     cudaStream_t S = c->stream, S2 = c->aux_stream;
+    // register-resident updates for 2b = 32 (SVDK_JACOBI_UPD=smem: the
+    // shared-memory kernels, kept for TB = 16 and for comparison)
+    const char* upd_env = std::getenv("SVDK_JACOBI_UPD");
+    const bool reg_upd = TB == 32 && !(upd_env && std::string(upd_env) == "smem");
+    const int a_warp_ctas = static_cast<int>(ceil_div(static_cast<int64_t>(a_ctas), UPD_WARPS));
+    const int v_warp_ctas =
+        static_cast<int>(ceil_div(ceil_div(n_pad, static_cast<int64_t>(32)) * k, UPD_WARPS));
+    auto launch_updates = [&](const double* qr, const int* ar, int r) {
+        if (reg_upd) {
+            jacobi_update_v_reg<<<v_warp_ctas, UPD_WARPS * 32, 0, S2>>>(V, n_pad, n_pad, qr, ar, nb, r);
+            jacobi_update_a_reg<<<a_warp_ctas, UPD_WARPS * 32, 0, S>>>(A, n_pad, qr, ar, nb, r);
+        } else {
+            jacobi_update_v<TB><<<v_ctas, 256, smem_v, S2>>>(V, n_pad, qr, ar, nb, r);
+            jacobi_update_a<TB><<<a_ctas, 256, smem_a, S>>>(A, n_pad, qr, ar, nb, r);
+        }
+    };
     auto enqueue_sweep = [&] {
         if (split) {  // in-block stage on the round-0 block pairing
             double* qr = qbuf.p() + static_cast<size_t>(rounds) * k * TB * TB;
@@ -639,8 +803,7 @@ void run_sweeps(Ctx* c, double* A, double* V, int64_t n_pad, int max_sweeps, dou
                                                                         max_inner, 1);
             SVDK_CUDA(cudaEventRecord(c->aux_ev[0], S));
             SVDK_CUDA(cudaStreamWaitEvent(S2, c->aux_ev[0], 0));
-            jacobi_update_v<TB><<<v_ctas, 256, smem_v, S2>>>(V, n_pad, qr, ar, nb, 0);
-            jacobi_update_a<TB><<<a_ctas, 256, smem_a, S>>>(A, n_pad, qr, ar, nb, 0);
+            launch_updates(qr, ar, 0);
         }
         for (int r = 0; r < rounds; ++r) {
             double* qr = qbuf.p() + static_cast<size_t>(r) * k * TB * TB;
@@ -649,8 +812,7 @@ void run_sweeps(Ctx* c, double* A, double* V, int64_t n_pad, int max_sweeps, dou
                                                              max_inner, split ? 2 : 0);
             SVDK_CUDA(cudaEventRecord(c->aux_ev[0], S));
             SVDK_CUDA(cudaStreamWaitEvent(S2, c->aux_ev[0], 0));
-            jacobi_update_v<TB><<<v_ctas, 256, smem_v, S2>>>(V, n_pad, qr, ar, nb, r);
-            jacobi_update_a<TB><<<a_ctas, 256, smem_a, S>>>(A, n_pad, qr, ar, nb, r);
+            launch_updates(qr, ar, r);
         }
         // join: the sweep ends when the V chain has caught up
         SVDK_CUDA(cudaEventRecord(c->aux_ev[1], S2));
