@@ -26,9 +26,13 @@ struct CtxHolder {
     }
 };
 
-[[noreturn]] void rethrow(int code) {
+[[noreturn]] void rethrow(int code, std::size_t offset = 0) {
     const std::string msg = svdk_last_error();
     switch (code) {
+        case SVDK_E_FORMAT:
+            throw FormatError(msg, offset);
+        case SVDK_E_IO:
+            throw IoError(msg);
         case SVDK_E_DIM:
             throw DimensionError(msg);
         case SVDK_E_PARAM:
@@ -40,8 +44,8 @@ struct CtxHolder {
     }
 }
 
-void check(int code) {
-    if (code != SVDK_OK) rethrow(code);
+void check(int code, std::size_t offset = 0) {
+    if (code != SVDK_OK) rethrow(code, offset);
 }
 
 svdk_ctx* ctx() {
@@ -94,6 +98,12 @@ std::size_t width_of(SvdMethod m, std::size_t n, const MethodParams& p) {
 }
 
 }  // namespace
+
+// shared with svdkit_tools.cpp (facade-internal, not part of the API)
+namespace detail {
+svdk_ctx* engine_ctx() { return ctx(); }
+void engine_check(int code, std::size_t offset) { check(code, offset); }
+}  // namespace detail
 
 // ---------------------------------------------------------------- DenseMatrix
 DenseMatrix::DenseMatrix(std::size_t rows, std::size_t cols)

@@ -1,0 +1,4 @@
+// Forwarding header: the reference include path svdkit/idx_io.hpp maps onto the
+// B200 facade (svdkit/svdkit.hpp), so callers compile unchanged.
+#pragma once
+#include "svdkit/svdkit.hpp"

@@ -15,10 +15,13 @@
 #include <cstddef>
 #include <cstdint>
 #include <initializer_list>
+#include <iosfwd>
 #include <optional>
+#include <span>
 #include <stdexcept>
 #include <string>
 #include <string_view>
+#include <utility>
 #include <vector>
 
 namespace svdkit {
@@ -174,6 +177,94 @@ PcaModel fit_pca(const DenseMatrix& data, Orientation orientation, SvdMethod met
                  const MethodParams& params, bool center_data = true);
 DenseMatrix transform(const PcaModel& model, const DenseMatrix& a);
 double residual_delta(const DenseMatrix& a, const SvdResult& s);
+
+// ---------------------------------------------------------------- cost model
+// (reference cost_model.hpp:9-49; closed forms evaluated by svdk_cost_model)
+struct CostEstimate {
+    double flops = 0.0;
+    double space_entries = 0.0;
+    double space_bytes = 0.0;  ///< always exactly 8 * space_entries
+};
+CostEstimate krylov_cost(std::size_t m, std::size_t n, std::size_t l, std::size_t i);
+CostEstimate krylov_cost_practical(std::size_t m, std::size_t n);
+CostEstimate krylov_cost_per_step(std::size_t m, std::size_t n, std::size_t l, std::size_t i);
+CostEstimate randomized_cost(std::size_t m, std::size_t n, std::size_t l, std::size_t i);
+CostEstimate randomized_cost_practical(std::size_t m, std::size_t n);
+CostEstimate truncated_cost(std::size_t m, std::size_t n);
+
+// ---------------------------------------------------------------- CSV
+// (reference csv_io.hpp:12-27)
+std::string format_double(double value);
+DenseMatrix read_matrix_csv(std::istream& in);
+DenseMatrix read_matrix_csv_file(const std::string& path);
+void write_matrix_csv(const DenseMatrix& a, std::ostream& out);
+void write_matrix_csv_file(const DenseMatrix& a, const std::string& path);
+void write_vector_csv_file(const std::vector<double>& values, const std::string& path);
+
+// ---------------------------------------------------------------- IDX
+// (reference idx_io.hpp:12-36); images_to_matrix expands on the GPU
+struct IdxImageSet {
+    std::size_t count = 0;
+    std::size_t height = 0;
+    std::size_t width = 0;
+    std::vector<std::uint8_t> pixels;  ///< count*height*width bytes, row-major per image
+};
+IdxImageSet parse_idx_images(std::span<const std::uint8_t> bytes);
+IdxImageSet load_idx_file(const std::string& path);
+DenseMatrix images_to_matrix(const IdxImageSet& set);
+DenseMatrix image_as_matrix(const IdxImageSet& set, std::size_t index);
+
+// ---------------------------------------------------------------- bench grid
+// (reference bench.hpp:13-88); factorisations and delta run on the GPU
+struct BenchConfig {
+    std::vector<std::size_t> row_sizes;
+    std::vector<std::size_t> col_sizes;
+    std::vector<SvdMethod> methods;
+    std::size_t repeats = 10;
+    RngSeed seed{42};
+    double l_fraction = 0.5;
+    std::size_t iterations = 1;
+    double memory_cap_bytes = 2.0 * 1024 * 1024 * 1024;
+};
+struct BenchRecord {
+    SvdMethod method = SvdMethod::Truncated;
+    std::size_t m = 0;
+    std::size_t n = 0;
+    std::size_t repeats = 0;
+    double mean_seconds = 0.0;
+    double std_seconds = 0.0;
+    double delta = 0.0;
+    double model_flops = 0.0;
+    double model_space_bytes = 0.0;
+};
+struct SkippedCell {
+    SvdMethod method = SvdMethod::Truncated;
+    std::size_t m = 0;
+    std::size_t n = 0;
+    std::string reason;
+};
+struct GridResult {
+    std::vector<BenchRecord> records;
+    std::vector<SkippedCell> skipped;
+};
+std::vector<std::pair<std::size_t, std::size_t>> expand_grid(const BenchConfig& cfg);
+std::size_t sketch_width_for(const BenchConfig& cfg, std::size_t n);
+GridResult run_grid(const BenchConfig& cfg);
+std::string to_csv(const std::vector<BenchRecord>& records);
+void write_csv_file(const std::vector<BenchRecord>& records, const std::string& path);
+struct OrderingCell {
+    std::size_t m = 0;
+    std::size_t n = 0;
+    std::vector<SvdMethod> by_seconds;
+    std::vector<SvdMethod> by_flops;
+    bool agree = false;
+};
+struct OrderingReport {
+    std::vector<OrderingCell> cells;
+    double agreement = 0.0;
+};
+OrderingReport summarize_ordering(const std::vector<BenchRecord>& records);
+std::string format_report(const OrderingReport& report);
 
 }  // namespace svdkit
 

@@ -194,3 +194,97 @@ class Oracle:
         self._check(self.lib.ref_residual_delta(_p(a), _sz(a.shape[0]), _sz(a.shape[1]), _p(u), _p(s), _p(v),
                                                 _sz(len(s)), C.byref(d)))
         return d.value
+
+
+class RefTools:
+    """The reference's host-side tools (cost model, CSV / IDX formats, bench grid
+    text) through ref_shim.cpp — parity checker for the engine's versions."""
+
+    def __init__(self):
+        lib = C.CDLL(REF_PATH)
+        self.lib = lib
+        lib.ref_last_offset.restype = _sz
+        lib.ref_sketch_width_for.restype = _sz
+        lib.ref_sketch_width_for.argtypes = [C.c_double, _sz]
+        lib.ref_format_double.argtypes = [C.c_double, C.c_char_p, _sz]
+
+    def _status(self, code):
+        if code != 0:
+            err = OracleError(code)
+            err.offset = int(self.lib.ref_last_offset()) if code == 8 else 0
+            raise err
+
+    def cost(self, model, m, n, l=0, i=0):
+        f, e, b = C.c_double(), C.c_double(), C.c_double()
+        self._status(self.lib.ref_cost_model(C.c_int(model), _sz(m), _sz(n), _sz(l), _sz(i),
+                                             C.byref(f), C.byref(e), C.byref(b)))
+        return f.value, e.value, b.value
+
+    def format_double(self, v: float) -> str:
+        buf = C.create_string_buffer(64)
+        assert self.lib.ref_format_double(C.c_double(v), buf, 64) == 0
+        return buf.value.decode()
+
+    def idx_parse(self, data: bytes):
+        dims = (C.c_uint64 * 3)()
+        buf = C.create_string_buffer(data, len(data)) if data else None
+        self._status(self.lib.ref_idx_parse(buf, _sz(len(data)), dims))
+        return tuple(int(x) for x in dims)
+
+    def images_to_matrix(self, data: bytes):
+        c, h, w = self.idx_parse(data)
+        out = np.zeros((c, h * w), order="F")
+        buf = C.create_string_buffer(data, len(data))
+        self._status(self.lib.ref_images_to_matrix(buf, _sz(len(data)), _p(out)))
+        return out
+
+    def image_as_matrix(self, data: bytes, index: int):
+        c, h, w = self.idx_parse(data)
+        out = np.zeros((h, w), order="F")
+        buf = C.create_string_buffer(data, len(data))
+        self._status(self.lib.ref_image_as_matrix(buf, _sz(len(data)), _sz(index), _p(out)))
+        return out
+
+    def sketch_width_for(self, l_fraction: float, n: int) -> int:
+        return int(self.lib.ref_sketch_width_for(l_fraction, n))
+
+    def expand_grid(self, rows, cols):
+        r = (C.c_size_t * max(1, len(rows)))(*rows)
+        c = (C.c_size_t * max(1, len(cols)))(*cols)
+        out = (C.c_size_t * max(2, 2 * len(rows) * len(cols)))()
+        cells = _sz(0)
+        self._status(self.lib.ref_expand_grid(r, _sz(len(rows)), c, _sz(len(cols)), out, C.byref(cells)))
+        return [(int(out[2 * k]), int(out[2 * k + 1])) for k in range(cells.value)]
+
+    def _records(self, recs):
+        k = len(recs)
+        meth = (C.c_int * max(1, k))(*[int(r[0]) for r in recs])
+        m = (C.c_size_t * max(1, k))(*[r[1] for r in recs])
+        n = (C.c_size_t * max(1, k))(*[r[2] for r in recs])
+        rep = (C.c_size_t * max(1, k))(*[r[3] for r in recs])
+        cols = (C.c_double * max(1, 5 * k))(*[x for r in recs for x in r[4:9]])
+        return meth, m, n, rep, cols, _sz(k)
+
+    def bench_csv(self, recs) -> str:
+        """recs: tuples (method, m, n, repeats, mean, std, delta, flops, bytes)."""
+        buf = C.create_string_buffer(1 << 20)
+        assert self.lib.ref_bench_csv(*self._records(recs), buf, _sz(1 << 20)) == 0
+        return buf.value.decode()
+
+    def ordering_report(self, recs):
+        buf = C.create_string_buffer(1 << 20)
+        agree = C.c_double()
+        assert self.lib.ref_ordering_report(*self._records(recs), buf, _sz(1 << 20), C.byref(agree)) == 0
+        return buf.value.decode(), agree.value
+
+    def matrix_csv_write(self, a) -> str:
+        a = _F(a)
+        buf = C.create_string_buffer(1 << 20)
+        assert self.lib.ref_matrix_csv_write(_p(a), _sz(a.shape[0]), _sz(a.shape[1]), buf, _sz(1 << 20)) == 0
+        return buf.value.decode()
+
+    def matrix_csv_read(self, text: str):
+        out = np.zeros(1 << 16)
+        m, n = _sz(0), _sz(0)
+        self._status(self.lib.ref_matrix_csv_read(text.encode(), _p(out), _sz(out.size), C.byref(m), C.byref(n)))
+        return out[: m.value * n.value].reshape((m.value, n.value), order="F")

@@ -15,8 +15,14 @@
 #include <string>
 #include <vector>
 
+#include <sstream>
+
+#include "svdkit/bench.hpp"
+#include "svdkit/cost_model.hpp"
+#include "svdkit/csv_io.hpp"
 #include "svdkit/dense_matrix.hpp"
 #include "svdkit/errors.hpp"
+#include "svdkit/idx_io.hpp"
 #include "svdkit/kernels.hpp"
 #include "svdkit/pca.hpp"
 #include "svdkit/svd_methods.hpp"
@@ -26,6 +32,7 @@ namespace R = svdkit;  // expands to svdkit_ref under -Dsvdkit=svdkit_ref
 namespace {
 
 thread_local double g_residual = 0.0;
+thread_local std::size_t g_offset = 0;
 
 R::DenseMatrix wrap(const double* p, std::size_t r, std::size_t c) {
     return R::DenseMatrix(r, c, std::vector<double>(p, p + r * c));
@@ -47,8 +54,13 @@ int guard(F&& f) {
     } catch (const R::NumericalError& e) {
         g_residual = e.residual();
         return 3;
-    } catch (...) {
+    } catch (const R::FormatError& e) {
+        g_offset = e.offset();
+        return 8;
+    } catch (const R::IoError&) {
         return 9;
+    } catch (...) {
+        return 99;
     }
 }
 
@@ -177,6 +189,141 @@ int ref_residual_delta(const double* a, std::size_t m, std::size_t n, const doub
         s.sigma.assign(sigma, sigma + rank);
         s.rank = rank;
         *delta = R::residual_delta(wrap(a, m, n), s);
+    });
+}
+
+// ---- host-side tools: cost model, CSV / IDX formats, bench grid text ----
+std::size_t ref_last_offset() { return g_offset; }
+
+int copy_text(const std::string& t, char* out, std::size_t cap) {
+    if (t.size() + 1 > cap) return 2;
+    std::memcpy(out, t.c_str(), t.size() + 1);
+    return 0;
+}
+
+// model ids as svdk.h SVDK_COST_*
+int ref_cost_model(int model, std::size_t m, std::size_t n, std::size_t l, std::size_t i,
+                   double* flops, double* entries, double* bytes) {
+    return guard([&] {
+        R::CostEstimate c;
+        switch (model) {
+            case 0: c = R::truncated_cost(m, n); break;
+            case 1: c = R::randomized_cost(m, n, l, i); break;
+            case 2: c = R::randomized_cost_practical(m, n); break;
+            case 3: c = R::krylov_cost(m, n, l, i); break;
+            case 4: c = R::krylov_cost_practical(m, n); break;
+            case 5: c = R::krylov_cost_per_step(m, n, l, i); break;
+            default: throw R::ParamError("model");
+        }
+        *flops = c.flops;
+        *entries = c.space_entries;
+        *bytes = c.space_bytes;
+    });
+}
+
+int ref_format_double(double v, char* out, std::size_t cap) {
+    return copy_text(R::format_double(v), out, cap);
+}
+
+int ref_idx_parse(const std::uint8_t* bytes, std::size_t len, std::uint64_t* dims) {
+    return guard([&] {
+        const R::IdxImageSet s = R::parse_idx_images(std::span<const std::uint8_t>(bytes, len));
+        dims[0] = s.count;
+        dims[1] = s.height;
+        dims[2] = s.width;
+    });
+}
+
+int ref_images_to_matrix(const std::uint8_t* bytes, std::size_t len, double* out) {
+    return guard([&] {
+        put(R::images_to_matrix(R::parse_idx_images(std::span<const std::uint8_t>(bytes, len))),
+            out);
+    });
+}
+
+int ref_image_as_matrix(const std::uint8_t* bytes, std::size_t len, std::size_t index,
+                        double* out) {
+    return guard([&] {
+        put(R::image_as_matrix(R::parse_idx_images(std::span<const std::uint8_t>(bytes, len)),
+                               index),
+            out);
+    });
+}
+
+std::size_t ref_sketch_width_for(double l_fraction, std::size_t n) {
+    R::BenchConfig cfg;
+    cfg.l_fraction = l_fraction;
+    return R::sketch_width_for(cfg, n);
+}
+
+// expand_grid: out holds 2 * nr * nc sizes (m, n pairs)
+int ref_expand_grid(const std::size_t* rows, std::size_t nr, const std::size_t* cols,
+                    std::size_t nc, std::size_t* out, std::size_t* cells) {
+    return guard([&] {
+        R::BenchConfig cfg;
+        cfg.row_sizes.assign(rows, rows + nr);
+        cfg.col_sizes.assign(cols, cols + nc);
+        cfg.methods = {R::SvdMethod::Truncated};
+        const auto g = R::expand_grid(cfg);
+        for (std::size_t k = 0; k < g.size(); ++k) {
+            out[2 * k] = g[k].first;
+            out[2 * k + 1] = g[k].second;
+        }
+        *cells = g.size();
+    });
+}
+
+std::vector<R::BenchRecord> records_of(const int* method, const std::size_t* m,
+                                       const std::size_t* n, const std::size_t* repeats,
+                                       const double* cols5, std::size_t count) {
+    // cols5: count x 5 row-major {mean_seconds, std_seconds, delta, model_flops, model_space_bytes}
+    std::vector<R::BenchRecord> recs(count);
+    for (std::size_t k = 0; k < count; ++k) {
+        recs[k].method = static_cast<R::SvdMethod>(method[k]);
+        recs[k].m = m[k];
+        recs[k].n = n[k];
+        recs[k].repeats = repeats[k];
+        recs[k].mean_seconds = cols5[5 * k];
+        recs[k].std_seconds = cols5[5 * k + 1];
+        recs[k].delta = cols5[5 * k + 2];
+        recs[k].model_flops = cols5[5 * k + 3];
+        recs[k].model_space_bytes = cols5[5 * k + 4];
+    }
+    return recs;
+}
+
+int ref_bench_csv(const int* method, const std::size_t* m, const std::size_t* n,
+                  const std::size_t* repeats, const double* cols5, std::size_t count, char* out,
+                  std::size_t cap) {
+    return copy_text(R::to_csv(records_of(method, m, n, repeats, cols5, count)), out, cap);
+}
+
+int ref_ordering_report(const int* method, const std::size_t* m, const std::size_t* n,
+                        const std::size_t* repeats, const double* cols5, std::size_t count,
+                        char* out, std::size_t cap, double* agreement) {
+    const R::OrderingReport r =
+        R::summarize_ordering(records_of(method, m, n, repeats, cols5, count));
+    *agreement = r.agreement;
+    return copy_text(R::format_report(r), out, cap);
+}
+
+int ref_matrix_csv_write(const double* a, std::size_t m, std::size_t n, char* out,
+                         std::size_t cap) {
+    std::ostringstream os;
+    R::write_matrix_csv(wrap(a, m, n), os);
+    return copy_text(os.str(), out, cap);
+}
+
+// read_matrix_csv: out holds up to cap doubles (column-major)
+int ref_matrix_csv_read(const char* text, double* out, std::size_t cap, std::size_t* m,
+                        std::size_t* n) {
+    return guard([&] {
+        std::istringstream is{std::string(text)};
+        const R::DenseMatrix a = R::read_matrix_csv(is);
+        *m = a.rows();
+        *n = a.cols();
+        if (a.size() > cap) throw R::ParamError("cap");
+        put(a, out);
     });
 }
 

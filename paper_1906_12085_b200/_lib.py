@@ -64,6 +64,10 @@ SIGNATURES = {
     "svdk_dev_qr_thin": (C.c_int, [_ctxp, _vp, _i64, _i64, _i64, _vp, _i64, _vp, _ip64]),
     "svdk_dev_pca": (C.c_int, [_ctxp, _vp, _i64, _i64, _i64, C.c_int, _i64, _i64, _u64, C.c_int,
                                C.c_double, _vp, _i64, _vp, _vp, _i64, _vp, _ip64, _ip64, _dp]),
+    "svdk_dev_idx_to_matrix": (C.c_int, [_ctxp, _vp, _i64, _i64, _vp, _i64]),
+    "svdk_cost_model": (C.c_int, [C.c_int, _u64, _u64, _u64, _u64, _dp, _dp, _dp]),
+    "svdk_idx_parse": (C.c_int, [_vp, _u64, C.POINTER(_u64), C.POINTER(_u64)]),
+    "svdk_idx_to_matrix": (C.c_int, [_ctxp, _vp, _i64, _i64, _vp]),
 }
 
 _lib = None
@@ -89,11 +93,11 @@ def load() -> C.CDLL:
         return _lib
 
 
-def check(code: int) -> None:
+def check(code: int, offset: int = 0) -> None:
     if code != 0:
         lib = load()
         msg = lib.svdk_last_error().decode(errors="replace")
-        raise_for_status(code, msg, lib.svdk_last_residual())
+        raise_for_status(code, msg, lib.svdk_last_residual(), offset)
 
 
 class Context:

@@ -28,15 +28,31 @@ class NumericalError(Error):
         return self._residual
 
 
+class FormatError(Error):
+    """Malformed input bytes / text, with the byte offset or line (errors.hpp:40-49)."""
+
+    def __init__(self, what: str, offset: int = 0):
+        super().__init__(what)
+        self._offset = int(offset)
+
+    def offset(self) -> int:
+        return self._offset
+
+
+class IoError(Error):
+    """File open / read / write failure (errors.hpp:51-55)."""
+
+
 class EngineError(Error):
     """CUDA / NCCL / allocation failure inside the B200 engine (no reference analogue)."""
 
 
 SVDK_OK, SVDK_E_DIM, SVDK_E_PARAM, SVDK_E_NUMERICAL = 0, 1, 2, 3
 SVDK_E_CUDA, SVDK_E_NCCL, SVDK_E_NOMEM, SVDK_E_STATE = 4, 5, 6, 7
+SVDK_E_FORMAT, SVDK_E_IO = 8, 9
 
 
-def raise_for_status(code: int, message: str, residual: float = 0.0) -> None:
+def raise_for_status(code: int, message: str, residual: float = 0.0, offset: int = 0) -> None:
     if code == SVDK_OK:
         return
     if code == SVDK_E_DIM:
@@ -45,4 +61,8 @@ def raise_for_status(code: int, message: str, residual: float = 0.0) -> None:
         raise ParamError(message)
     if code == SVDK_E_NUMERICAL:
         raise NumericalError(message, residual)
+    if code == SVDK_E_FORMAT:
+        raise FormatError(message, offset)
+    if code == SVDK_E_IO:
+        raise IoError(message)
     raise EngineError(f"[svdk status {code}] {message}")

@@ -19,6 +19,16 @@ def test_facade_reference_caller():
     assert "facade_test: ok" in r.stdout
 
 
+def test_facade_tools_gpu():
+    """facade/tools_test gpu: images_to_matrix kernel + run_grid through the C++ API."""
+    exe = os.path.join(ROOT, "facade", "tools_test")
+    assert os.path.exists(exe), "facade not built"
+    r = subprocess.run([exe, "gpu"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "tools_test gpu: ok" in r.stdout
+    assert r.stdout.startswith("method,m,n,repeats,mean_seconds,std_seconds,delta,model_flops,")
+
+
 def test_nccl_world1_matches_local():
     import torch
 
@@ -27,7 +37,7 @@ def test_nccl_world1_matches_local():
     from tests.datagen import make_matrix
     a_np = make_matrix(6000, 128, "c2", seed=9)
     a = colmajor(*a_np.shape)
-    a.copy_(torch.from_numpy(a_np).cuda())
+    a.copy_(torch.from_numpy(np.array(a_np)).cuda())
     e_local = Engine(0)
     e_nccl = Engine(0)
     e_nccl.ctx.attach_nccl(_lib.nccl_unique_id(), 0, 1)
