@@ -175,35 +175,36 @@ __device__ __forceinline__ void xform2x2(double& m00, double& m01, double& m10, 
     }
 }
 
+// Inner schedule of a 2b subproblem for one mode (identical for every pair
+// and round, so built once per eig_sym by jacobi_tables_kernel):
+//   ptab[r][i]  rotation i of inner round r, packed p | q << 8
+//   pinv[r][x]  pair holding index x in round r | role << 7 (role 1 = q)
+//   look[r][i]  for rotation i of round r+1 = (p, q): the round-r pairs bp, bq
+//               holding p and q, their roles and their (row, col) indices —
+//               bits 0-4 bp, 5-9 bq, 10 role_p, 11 role_q, 12-16 p_bp,
+//               17-21 q_bp, 22-26 p_bq, 27-31 q_bq (one LDS for the lookahead)
 template <int TB>
-__global__ void __launch_bounds__(solve_threads<TB>())
-    jacobi_pair_solve(double* A, int64_t lda, double* Qbuf, int* active, int nb, int round,
-                      double skip_tau, int max_inner, int mode) {
-    // mode 0: all pairs of the 2b subproblem (2b-1 rounds of b rotations);
-    // mode 1: only the pairs inside block I and inside block J (b-1 rounds);
-    // mode 2: only the b^2 cross pairs (i in I, j in J) (b rounds).
-    constexpr int B = TB / 2, LD = TB + 4, NP = TB / 2, RMAX = TB - 1;
-    const int R = mode == 0 ? TB - 1 : (mode == 1 ? B - 1 : B);
-    constexpr int MT = NP * NP;  // M threads
-    constexpr int QT = 32;       // the Q warp: lane l holds column l of Q in registers
-    extern __shared__ double sm[];
-    double* Mc = sm;             // current M
-    double* Mn = Mc + TB * LD;   // next M (double buffer)
-    double* Q = Mn + TB * LD;
-    double* T = Q + TB * LD;
-    __shared__ int ptab[RMAX][NP];            // inner schedule, packed p | q << 8
-    __shared__ unsigned char pinv[RMAX][TB];  // pinv[r][x] = pair of x in round r | role << 7
-    __shared__ unsigned long long look[RMAX][NP];  // lookahead descriptors (see below)
-    __shared__ double cs[RMAX][NP], sn[RMAX][NP];
-    __shared__ int any_applied;
+struct __align__(16) SolveTables {
+    unsigned long long look[TB - 1][TB / 2];
+    int ptab[TB - 1][TB / 2];
+    unsigned char pinv[TB - 1][TB];
+};
+static_assert(sizeof(SolveTables<32>) % 16 == 0 && sizeof(SolveTables<16>) % 16 == 0, "uint4 copy");
 
-    const int tid = threadIdx.x;
-    const bool probe = blockIdx.x == 0 && tid == MT + QT && round == 5;
-    long long t0 = SVDK_CLOCK();
-    int I, J;
-    circle_pair(nb, round, blockIdx.x, I, J);
-    if (tid == 0) any_applied = 0;
-    for (int e = tid; e < R * NP; e += blockDim.x) {
+// modes 0 (all pairs), 1 (pairs inside each half), 2 (cross pairs): one CTA each
+template <int TB>
+__global__ void jacobi_tables_kernel(SolveTables<TB>* out) {
+    constexpr int B = TB / 2, NP = TB / 2;
+    const int mode = blockIdx.x;
+    const int R = mode == 0 ? TB - 1 : (mode == 1 ? B - 1 : B);
+    __shared__ SolveTables<TB> t;
+    for (int e = threadIdx.x; e < (TB - 1) * NP; e += blockDim.x) {
+        t.ptab[e / NP][e % NP] = 0;
+        t.look[e / NP][e % NP] = 0;
+    }
+    for (int e = threadIdx.x; e < (TB - 1) * TB; e += blockDim.x) t.pinv[e / TB][e % TB] = 0;
+    __syncthreads();
+    for (int e = threadIdx.x; e < R * NP; e += blockDim.x) {
         int p, q;
         const int r = e / NP, i = e % NP;
         if (mode == 0) {
@@ -217,40 +218,90 @@ __global__ void __launch_bounds__(solve_threads<TB>())
             p = i;
             q = B + (i + r) % B;
         }
-        ptab[r][i] = p | (q << 8);
-        pinv[r][p] = static_cast<unsigned char>(i);
-        pinv[r][q] = static_cast<unsigned char>(i | 128);
-    }
-    for (int e = tid; e < TB * TB; e += blockDim.x) {
-        const int i = e % TB, j = e / TB;
-        const double x = A[gidx(B, I, J, i) + gidx(B, I, J, j) * lda];
-        Mc[i + j * LD] = x;
-        Q[i + j * LD] = (i == j) ? 1.0 : 0.0;
-        if (i != j && fabs(x) > skip_tau) any_applied = 1;
+        t.ptab[r][i] = p | (q << 8);
+        t.pinv[r][p] = static_cast<unsigned char>(i);
+        t.pinv[r][q] = static_cast<unsigned char>(i | 128);
     }
     __syncthreads();
-    // look[rr][i]: for rotation i of round rr+1 = (p, q), the round-rr pairs
-    // bp, bq holding p and q, their roles, and bp's / bq's (row, col) indices:
-    // bits 0-4 bp, 5-9 bq, 10 role_p, 11 role_q, 12-16 p_bp, 17-21 q_bp,
-    // 22-26 p_bq, 27-31 q_bq — one LDS instead of a 3-level lookup chain.
-    for (int e = tid; e < R * NP; e += blockDim.x) {
+    for (int e = threadIdx.x; e < R * NP; e += blockDim.x) {
         const int rr = e / NP, i = e % NP, nr = (rr + 1) % R;
-        const int code = ptab[nr][i];
-        const int ip = pinv[rr][code & 255], iq = pinv[rr][code >> 8];
+        const int code = t.ptab[nr][i];
+        const int ip = t.pinv[rr][code & 255], iq = t.pinv[rr][code >> 8];
         const int bp = ip & 127, bq = iq & 127;
-        const unsigned long long d =
+        t.look[rr][i] =
             static_cast<unsigned long long>(bp) | (static_cast<unsigned long long>(bq) << 5) |
             (static_cast<unsigned long long>(ip >> 7) << 10) |
             (static_cast<unsigned long long>(iq >> 7) << 11) |
-            (static_cast<unsigned long long>(ptab[rr][bp] & 255) << 12) |
-            (static_cast<unsigned long long>(ptab[rr][bp] >> 8) << 17) |
-            (static_cast<unsigned long long>(ptab[rr][bq] & 255) << 22) |
-            (static_cast<unsigned long long>(ptab[rr][bq] >> 8) << 27);
-        look[rr][i] = d;
+            (static_cast<unsigned long long>(t.ptab[rr][bp] & 255) << 12) |
+            (static_cast<unsigned long long>(t.ptab[rr][bp] >> 8) << 17) |
+            (static_cast<unsigned long long>(t.ptab[rr][bq] & 255) << 22) |
+            (static_cast<unsigned long long>(t.ptab[rr][bq] >> 8) << 27);
     }
     __syncthreads();
+    const uint4* src = reinterpret_cast<const uint4*>(&t);
+    uint4* dst = reinterpret_cast<uint4*>(out + mode);
+    for (int e = threadIdx.x; e < static_cast<int>(sizeof(t) / 16); e += blockDim.x) dst[e] = src[e];
+}
+
+template <int TB>
+__device__ __forceinline__ void solve_pair(const double* A, int64_t lda, const SolveTables<TB>* tabs,
+                                           double* Qbuf, int* active, int nb, int round,
+                                           double skip_tau, int max_inner, int mode, int pair) {
+    // mode 0: all pairs of the 2b subproblem (2b-1 rounds of b rotations);
+    // mode 1: only the pairs inside block I and inside block J (b-1 rounds);
+    // mode 2: only the b^2 cross pairs (i in I, j in J) (b rounds).
+    constexpr int B = TB / 2, LD = TB + 4, NP = TB / 2, RMAX = TB - 1;
+    const int R = mode == 0 ? TB - 1 : (mode == 1 ? B - 1 : B);
+    constexpr int MT = NP * NP;  // M threads
+    constexpr int QT = 32;       // the Q warp: lane l holds column l of Q in registers
+    extern __shared__ double sm[];
+    double* Mc = sm;             // current M
+    double* Mn = Mc + TB * LD;   // next M (double buffer)
+    double* Q = Mn + TB * LD;
+    double* T = Q + TB * LD;
+    (void)RMAX;
+    __shared__ SolveTables<TB> st;  // inner schedule (see SolveTables)
+    __shared__ double cs[RMAX][NP], sn[RMAX][NP];
+
+    const int tid = threadIdx.x;
+    const bool probe = pair == 0 && tid == MT + QT && round == 5;
+    long long t0 = SVDK_CLOCK();
+    int I, J;
+    circle_pair(nb, round, pair, I, J);
+    // Everything the solve needs is fetched with all loads in flight at once:
+    // the 32 x 32 block of A (<= 4 per thread) and this mode's precomputed
+    // schedule tables (jacobi_tables_kernel, 16-byte loads).
+    constexpr int NT = solve_threads<TB>();
+    constexpr int PER = (TB * TB + NT - 1) / NT;
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(tabs) + static_cast<size_t>(mode) *
+                               (sizeof(SolveTables<TB>) / 16);
+        uint4* dst = reinterpret_cast<uint4*>(&st);
+        for (int e = tid; e < static_cast<int>(sizeof(SolveTables<TB>) / 16); e += NT) dst[e] = src[e];
+    }
+    bool big = false;
+    {
+        double xv[PER];
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int e = tid + k * NT;
+            xv[k] = e < TB * TB ? __ldcg(&A[gidx(B, I, J, e % TB) + gidx(B, I, J, e / TB) * lda]) : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int e = tid + k * NT;
+            if (e < TB * TB) {
+                const int i = e % TB, j = e / TB;
+                Mc[i + j * LD] = xv[k];
+                big |= (i != j) && fabs(xv[k]) > skip_tau;
+            }
+        }
+    }
+    const bool work = __syncthreads_or(big) != 0;
+    auto& ptab = st.ptab;
+    auto& pinv = st.pinv;
+    auto& look = st.look;
     long long t1 = SVDK_CLOCK();
-    const bool work = any_applied != 0;
     if (probe && work) {
         SVDK_PROBE_STORE(g_jprobe, 0, t0);
         SVDK_PROBE_STORE(g_jprobe, 1, t1);
@@ -373,10 +424,19 @@ __global__ void __launch_bounds__(solve_threads<TB>())
         smem_mma<TB, false>(Q, Mn, T);  // T <- Q (3I - Q^T Q) / 2
         __syncthreads();
         for (int e = tid; e < TB * TB; e += blockDim.x)
-            Qbuf[static_cast<size_t>(blockIdx.x) * TB * TB + e] = T[(e % TB) + (e / TB) * LD];
+            Qbuf[static_cast<size_t>(pair) * TB * TB + e] = T[(e % TB) + (e / TB) * LD];
     }
-    if (tid == 0) active[blockIdx.x] = work ? 1 : 0;
+    if (tid == 0) active[pair] = work ? 1 : 0;
+    __syncthreads();  // shared memory is reused by the next pair / phase
 }
+
+template <int TB>
+__global__ void __launch_bounds__(solve_threads<TB>())
+    jacobi_pair_solve(const double* A, int64_t lda, const SolveTables<TB>* tabs, double* Qbuf,
+                      int* active, int nb, int round, double skip_tau, int max_inner, int mode) {
+    solve_pair<TB>(A, lda, tabs, Qbuf, active, nb, round, skip_tau, max_inner, mode, blockIdx.x);
+}
+
 
 // ---------------------------------------------------------------------------
 // 2. the round's similarity on A, and its accumulation into V
@@ -484,7 +544,7 @@ __global__ void __launch_bounds__(256)
 //   A[m][k]: A[r][kq]     B[k][n]: B[kq][r]     C: C[r][2 kq], C[r][2 kq + 1]
 __device__ __forceinline__ double q_frag(const double* Qp, bool act, int k, int n) {
     // Q[k][n] of a column-major 32 x 32 rotation, identity when inactive
-    return act ? Qp[k + n * 32] : (k == n ? 1.0 : 0.0);
+    return act ? __ldcg(&Qp[k + n * 32]) : (k == n ? 1.0 : 0.0);
 }
 
 constexpr int UPD_WARPS = 4;
@@ -492,20 +552,18 @@ constexpr int UPD_WARPS = 4;
 // A[IJ_p, IJ_q] <- Q_p^T A[IJ_p, IJ_q] Q_q for one (p <= q) per warp; the
 // mirror block gets the same values (exact symmetry); a diagonal pair block
 // copies its upper triangle to the lower one.
-__global__ void __launch_bounds__(UPD_WARPS * 32)
-    jacobi_update_a_reg(double* A, int64_t lda, const double* Qbuf, const int* active, int nb,
-                        int round) {
+__device__ __forceinline__ void upd_a_unit(double* A, int64_t lda, const double* Qbuf,
+                                           const int* active, int nb, int round, int u) {
     constexpr int B = 16;
     const int lane = threadIdx.x & 31, r = lane >> 2, kq = lane & 3;
     const int k = nb / 2;
-    const int u = blockIdx.x * UPD_WARPS + (threadIdx.x >> 5);
     if (u >= k * (k + 1) / 2) return;
     int q = static_cast<int>((sqrt(8.0 * u + 1.0) - 1.0) * 0.5);
     while ((q + 1) * (q + 2) / 2 <= u) ++q;
     while (q * (q + 1) / 2 > u) --q;
     const int p = u - q * (q + 1) / 2;
-    const bool ap = active[p] != 0, aq = active[q] != 0;
-    if (!(ap | aq)) return;
+    const bool ap = __ldcg(&active[p]) != 0, aq = __ldcg(&active[q]) != 0;
+    if (!(ap | aq)) return;  // both rotations are the identity
     int Ip, Jp, Iq, Jq;
     circle_pair(nb, round, p, Ip, Jp);
     circle_pair(nb, round, q, Iq, Jq);
@@ -518,7 +576,7 @@ __global__ void __launch_bounds__(UPD_WARPS * 32)
         const int64_t row = gidx(B, Ip, Jp, 4 * s + kq);
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
-            xb[s][t] = A[row + gidx(B, Iq, Jq, 8 * t + r) * lda];
+            xb[s][t] = __ldcg(&A[row + gidx(B, Iq, Jq, 8 * t + r) * lda]);
             xa[s][t] = q_frag(Qa, ap, 4 * s + kq, 8 * t + r);
         }
     }
@@ -575,16 +633,15 @@ __global__ void __launch_bounds__(UPD_WARPS * 32)
 }
 
 // V[rows, IJ_q] <- V[rows, IJ_q] Q_q; one warp per (32-row tile, pair q).
-__global__ void __launch_bounds__(UPD_WARPS * 32)
-    jacobi_update_v_reg(double* V, int64_t ldv, int64_t n_rows, const double* Qbuf,
-                        const int* active, int nb, int round) {
+__device__ __forceinline__ void upd_v_unit(double* V, int64_t ldv, int64_t n_rows,
+                                           const double* Qbuf, const int* active, int nb, int round,
+                                           int64_t u) {
     constexpr int B = 16;
     const int lane = threadIdx.x & 31, r = lane >> 2, kq = lane & 3;
     const int k = nb / 2;
-    const int64_t u = static_cast<int64_t>(blockIdx.x) * UPD_WARPS + (threadIdx.x >> 5);
     const int q = static_cast<int>(u % k);
     const int64_t row0 = (u / k) * 32;
-    if (row0 >= n_rows || !active[q]) return;
+    if (row0 >= n_rows || !__ldcg(&active[q])) return;
     int Iq, Jq;
     circle_pair(nb, round, q, Iq, Jq);
     const double* Qb = Qbuf + static_cast<size_t>(q) * 1024;
@@ -593,9 +650,9 @@ __global__ void __launch_bounds__(UPD_WARPS * 32)
     for (int s = 0; s < 8; ++s) {
         const int64_t col = gidx(B, Iq, Jq, 4 * s + kq) * ldv;
 #pragma unroll
-        for (int m = 0; m < 4; ++m) va[m][s] = V[row0 + 8 * m + r + col];
+        for (int m = 0; m < 4; ++m) va[m][s] = __ldcg(&V[row0 + 8 * m + r + col]);
 #pragma unroll
-        for (int t = 0; t < 4; ++t) qb[s][t] = Qb[(4 * s + kq) + (8 * t + r) * 32];
+        for (int t = 0; t < 4; ++t) qb[s][t] = __ldcg(&Qb[(4 * s + kq) + (8 * t + r) * 32]);
     }
     double acc[4][4][2];
 #pragma unroll
@@ -616,6 +673,19 @@ __global__ void __launch_bounds__(UPD_WARPS * 32)
 #pragma unroll
             for (int m = 0; m < 4; ++m) V[row0 + 8 * m + r + col] = acc[m][t][i];
         }
+}
+
+__global__ void __launch_bounds__(UPD_WARPS * 32)
+    jacobi_update_a_reg(double* A, int64_t lda, const double* Qbuf, const int* active, int nb,
+                        int round) {
+    upd_a_unit(A, lda, Qbuf, active, nb, round, blockIdx.x * UPD_WARPS + (threadIdx.x >> 5));
+}
+
+__global__ void __launch_bounds__(UPD_WARPS * 32)
+    jacobi_update_v_reg(double* V, int64_t ldv, int64_t n_rows, const double* Qbuf,
+                        const int* active, int nb, int round) {
+    upd_v_unit(V, ldv, n_rows, Qbuf, active, nb, round,
+               static_cast<int64_t>(blockIdx.x) * UPD_WARPS + (threadIdx.x >> 5));
 }
 
 // ---------------------------------------------------------------------------
@@ -795,12 +865,20 @@ void run_sweeps(Ctx* c, double* A, double* V, int64_t n_pad, int max_sweeps, dou
             jacobi_update_a<TB><<<a_ctas, 256, smem_a, S>>>(A, n_pad, qr, ar, nb, r);
         }
     };
+    DBuf tab_buf(c, 3 * sizeof(SolveTables<TB>) / sizeof(double));
+    const auto* tabs = reinterpret_cast<const SolveTables<TB>*>(tab_buf.p());
+    jacobi_tables_kernel<TB><<<3, 256, 0, S>>>(reinterpret_cast<SolveTables<TB>*>(tab_buf.p()));
+    SVDK_CHECK_LAUNCH();
+    c->launches++;
+    auto launch_solve = [&](double* qr, int* ar, int r, int mode) {
+        jacobi_pair_solve<TB><<<k, nthreads_solve, smem_solve, S>>>(A, n_pad, tabs, qr, ar, nb, r,
+                                                                    skip_tau, max_inner, mode);
+    };
     auto enqueue_sweep = [&] {
         if (split) {  // in-block stage on the round-0 block pairing
             double* qr = qbuf.p() + static_cast<size_t>(rounds) * k * TB * TB;
             int* ar = active + static_cast<size_t>(rounds) * k;
-            jacobi_pair_solve<TB><<<k, nthreads_solve, smem_solve, S>>>(A, n_pad, qr, ar, nb, 0, skip_tau,
-                                                                        max_inner, 1);
+            launch_solve(qr, ar, 0, 1);
             SVDK_CUDA(cudaEventRecord(c->aux_ev[0], S));
             SVDK_CUDA(cudaStreamWaitEvent(S2, c->aux_ev[0], 0));
             launch_updates(qr, ar, 0);
@@ -808,8 +886,7 @@ void run_sweeps(Ctx* c, double* A, double* V, int64_t n_pad, int max_sweeps, dou
         for (int r = 0; r < rounds; ++r) {
             double* qr = qbuf.p() + static_cast<size_t>(r) * k * TB * TB;
             int* ar = active + static_cast<size_t>(r) * k;
-            jacobi_pair_solve<TB><<<k, nthreads_solve, smem_solve, S>>>(A, n_pad, qr, ar, nb, r, skip_tau,
-                                                             max_inner, split ? 2 : 0);
+            launch_solve(qr, ar, r, split ? 2 : 0);
             SVDK_CUDA(cudaEventRecord(c->aux_ev[0], S));
             SVDK_CUDA(cudaStreamWaitEvent(S2, c->aux_ev[0], 0));
             launch_updates(qr, ar, r);
