@@ -516,15 +516,20 @@ int svdk_fit_pca(svdk_ctx* c, const double* data, int64_t m, int64_t n, int orie
         DBuf dC = upload(c, data, m, n, lda);
         const int64_t ldc = lda;
         DBuf dM(c, std::max<int64_t>(nm, 1));
-        if (center) {
-            if (cols_ex)
+        if (center && !cols_ex) {
+            // column means, then centring fused with the total variance
+            // (pca.cpp:57-59) in one pass over the upload buffer
+            column_sums(c, dC.p(), ldc, m, n, static_cast<double>(m), dM.p());
+            DBuf dt(c, 1);
+            subtract_column_means_sumsq(c, dC.p(), ldc, m, n, dM.p(), dC.p(), ldc, dt.p());
+            d2h(c, total, dt.p(), 1);
+        } else {
+            if (center)
                 center_cols_are_examples(c, dC.p(), ldc, m, n, dC.p(), ldc, dM.p());
             else
-                center_rows_are_examples(c, dC.p(), ldc, m, n, dC.p(), ldc, dM.p());
-        } else {
-            fill(c, dM.p(), nm, 0.0);
+                fill(c, dM.p(), nm, 0.0);
+            *total = frob_sq(c, dC.p(), ldc, m, n);
         }
-        *total = frob_sq(c, dC.p(), ldc, m, n);
         // tall orientation for the method
         const bool wide = m < n;
         const double* dT = dC.p();

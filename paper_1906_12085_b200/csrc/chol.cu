@@ -54,21 +54,18 @@ __global__ void __launch_bounds__(256)
     }
     __syncthreads();
     long long tl = SVDK_CLOCK();
+    // Right-looking factorisation with ONE barrier per column: the pivot row
+    // is left unscaled (s_jc), the trailing update uses s_ic -= s_ji s_jc / d_j
+    // with d_j = s_jj read by every thread (no separate pivot / scaling
+    // phases), and R's row j = s_jc / sqrt(d_j) is formed after the loop.
     for (int j = 0; j < bs; ++j) {
-        // pivot
+        const double d = S[j + j * LD];
         if (tid == 0) {
-            const double d = S[j + j * LD];
-            const double ref = dref[j];
-            if (!(d > 0.0) || d <= rel_tol * ref) atomicOr(flag, 1);
-            const double r = sqrt(fmax(d, 0.0));
-            S[j + j * LD] = r;
-            dinv[j] = r > 0.0 ? 1.0 / r : 0.0;
+            if (!(d > 0.0) || d <= rel_tol * dref[j]) atomicOr(flag, 1);
+            dinv[j] = d > 0.0 ? 1.0 / sqrt(d) : 0.0;
         }
-        __syncthreads();
-        const double inv = dinv[j];
-        for (int c = j + 1 + tid; c < bs; c += blockDim.x) S[j + c * LD] *= inv;
-        __syncthreads();
-        // trailing update of the upper triangle: S[i][c] -= S[j][i] S[j][c],
+        const double dj = d > 0.0 ? 1.0 / d : 0.0;
+        // trailing update of the upper triangle: S[i][c] -= S[j][i] S[j][c] / d,
         // j < i <= c; a warp per column, lanes down the rows. Every load of
         // the step is issued before any store (explicit register staging):
         // otherwise possible smem aliasing serialises load-use-store chains.
@@ -79,7 +76,7 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
             for (int r = 0; r < 2; ++r) {
                 const int i = j + 1 + lane + 32 * r;
-                sji[r] = i < bs ? S[j + i * LD] : 0.0;
+                sji[r] = i < bs ? S[j + i * LD] * dj : 0.0;
             }
 #pragma unroll
             for (int k = 0; k < CPW; ++k) {
@@ -97,12 +94,23 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
                 for (int r = 0; r < 2; ++r) {
                     const int i = j + 1 + lane + 32 * r;
-                    if (cc < bs && i <= cc) S[i + cc * LD] = v[k][r] - sji[r] * sjc[k];
+                    if (cc < bs && i <= cc) S[i + cc * LD] = fma(-sji[r], sjc[k], v[k][r]);
                 }
             }
         }
         __syncthreads();
     }
+    // R = diag(1 / sqrt(d)) (unscaled rows): row j scaled, diagonal sqrt(d_j)
+    for (int e = tid; e < bs * bs; e += blockDim.x) {
+        const int i = e % bs, c = e / bs;
+        if (i < c) S[i + c * LD] *= dinv[i];
+    }
+    __syncthreads();
+    for (int e = tid; e < bs; e += blockDim.x) {
+        const double d = S[e + e * LD];
+        S[e + e * LD] = d > 0.0 ? sqrt(d) : 0.0;
+    }
+    __syncthreads();
     long long tf = SVDK_CLOCK();
     // R out (upper, zero strictly-lower)
     for (int e = tid; e < bs * bs; e += blockDim.x) {

@@ -33,9 +33,9 @@ __global__ void spectrum_kernel(const double* w, int64_t n, double* sigma, int* 
 
 // One warp per column j < rank: first index of max |v_ij| (strict >), then
 // sign flip of V_j and epilogue scale_j = sign_j * (1 / sigma_j) for U.
-__global__ void signs_kernel(double* V, int64_t ldv, int64_t n, const int* rank_p,
+__global__ void signs_kernel(double* V, int64_t ldv, int64_t n, const int* rank_p, int rank_val,
                              const double* sigma, double* scale, int with_scale) {
-    const int rank = *rank_p;
+    const int rank = rank_p ? *rank_p : rank_val;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (warp >= rank) return;
@@ -65,46 +65,8 @@ __global__ void signs_kernel(double* V, int64_t ldv, int64_t n, const int* rank_
         for (int64_t i = lane; i < n; i += 32) v[i] = -v[i];
     // U is formed from the already-flipped V: A(-v) = -(Av) exactly, so
     // scaling by 1/sigma reproduces the reference's flip-after-scale.
-    if (with_scale && lane == 0) scale[warp] = 1.0 / sigma[warp];
-}
-
-// Flip U columns by the sign of V's pivot entry (already-scaled U; used by
-// the sketch methods whose U comes from Q W).
-__global__ void signs_uv_kernel(double* V, int64_t ldv, int64_t n, double* U, int64_t ldu,
-                                int64_t m, int rank) {
-    const int j = blockIdx.y;
-    if (j >= rank) return;
-    double* v = V + j * ldv;
-    __shared__ double ssign;
-    if (threadIdx.x < 32) {
-        const int lane = threadIdx.x;
-        double best = 0.0;
-        int64_t arg = 0;
-        for (int64_t i = lane; i < n; i += 32) {
-            const double a = fabs(v[i]);
-            if (a > best) {
-                best = a;
-                arg = i;
-            }
-        }
-        for (int o = 16; o > 0; o >>= 1) {
-            const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-            const int64_t oa = __shfl_xor_sync(0xffffffffu, arg, o);
-            if (ob > best || (ob == best && oa < arg)) {
-                best = ob;
-                arg = oa;
-            }
-        }
-        if (lane == 0) ssign = v[arg] < 0.0 ? -1.0 : 1.0;
-    }
-    __syncthreads();
-    const double sign = ssign;
-    if (sign > 0.0) return;
-    if (blockIdx.x == 0)
-        for (int64_t i = threadIdx.x; i < n; i += blockDim.x) v[i] = -v[i];
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < m;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-        U[i + j * ldu] = -U[i + j * ldu];
+    if (with_scale == 1 && lane == 0) scale[warp] = 1.0 / sigma[warp];
+    if (with_scale == 2 && lane == 0) scale[warp] = sign;  // the sketch methods' U flip
 }
 
 }  // namespace
@@ -134,13 +96,10 @@ int64_t spectrum(Ctx* c, const double* w, int64_t n, double* sigma) {
     return rank;
 }
 
-void normalize_signs_uv(Ctx* c, double* U, int64_t ldu, int64_t m, double* V, int64_t ldv,
-                        int64_t n, int64_t rank) {
+void signs_v(Ctx* c, double* V, int64_t ldv, int64_t n, int64_t rank, double* d_sign) {
     if (rank <= 0) return;
-    const int gx = static_cast<int>(std::min<int64_t>(ceil_div(m, 256), 16));
-    signs_uv_kernel<<<dim3(gx, static_cast<unsigned>(rank)), 256, 0, c->stream>>>(V, ldv, n, U,
-                                                                                   ldu, m,
-                                                                                   static_cast<int>(rank));
+    signs_kernel<<<static_cast<unsigned>(ceil_div(rank * 32, 256)), 256, 0, c->stream>>>(
+        V, ldv, n, nullptr, static_cast<int>(rank), nullptr, d_sign, 2);
     SVDK_CHECK_LAUNCH();
     c->launches++;
 }
@@ -156,7 +115,7 @@ int64_t back_project(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n,
     DBuf scale(c, rank);
     const int warps = static_cast<int>(rank);
     signs_kernel<<<static_cast<unsigned>(ceil_div(warps * 32, 256)), 256, 0, c->stream>>>(
-        V, ldv, n, c->d_flags + 2, sigma, scale.p(), 1);
+        V, ldv, n, c->d_flags + 2, 0, sigma, scale.p(), 1);
     SVDK_CHECK_LAUNCH();
     c->launches++;
     // U = A V diag(1 / sigma) on the sign-normalised V (kernels.cpp:14-45 +

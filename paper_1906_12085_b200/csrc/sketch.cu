@@ -108,11 +108,14 @@ int64_t finish_sketch(Ctx* c, const double* Q, int64_t ldq, int64_t m, int64_t w
         DBuf iu(c, static_cast<size_t>(ldiu) * w), iv(c, static_cast<size_t>(w) * w);
         const int64_t r = truncated_svd(c, T, n, n, w, iu.p(), ldiu, sigma, iv.p(), w, nullptr);
         if (r == 0) return 0;
-        DBuf rv(c, static_cast<size_t>(w) * r);  // Rinv inner.v (w x r)
-        gemm(c, false, w, r, w, Rinv, w, iv.p(), w, rv.p(), w);
+        // normalize_signs first on V = inner.u; U's flips ride on the small
+        // factor (Q (-w) = -(Q w) exactly), so U is written once
+        copy_mat(c, iu.p(), ldiu, V, ldv, n, r);  // V = inner.u
+        DBuf sgn(c, r);
+        signs_v(c, V, ldv, n, r, sgn.p());
+        DBuf rv(c, static_cast<size_t>(w) * r);  // Rinv inner.v diag(sign) (w x r)
+        gemm(c, false, w, r, w, Rinv, w, iv.p(), w, rv.p(), w, sgn.p());
         gemm(c, false, m, r, w, Q, ldq, rv.p(), w, U, ldu, nullptr, true);  // U = Q inner.v
-        copy_mat(c, iu.p(), ldiu, V, ldv, n, r);                             // V = inner.u
-        normalize_signs_uv(c, U, ldu, m, V, ldv, n, r);
         return r;
     }
     // wide T: factor T^T (w x n) and swap (svd_methods.cpp:100-103)
@@ -122,11 +125,12 @@ int64_t finish_sketch(Ctx* c, const double* Q, int64_t ldq, int64_t m, int64_t w
     DBuf iu(c, static_cast<size_t>(ldt) * n), iv(c, static_cast<size_t>(n) * n);
     const int64_t r = truncated_svd(c, Tt.p(), ldt, w, n, iu.p(), ldt, sigma, iv.p(), n, nullptr);
     if (r == 0) return 0;
-    DBuf rv(c, static_cast<size_t>(w) * r);  // Rinv inner.v (w x r)
-    gemm(c, false, w, r, w, Rinv, w, iu.p(), ldt, rv.p(), w);
+    copy_mat(c, iv.p(), n, V, ldv, n, r);  // V = inner.u
+    DBuf sgn(c, r);
+    signs_v(c, V, ldv, n, r, sgn.p());
+    DBuf rv(c, static_cast<size_t>(w) * r);  // Rinv inner.v diag(sign) (w x r)
+    gemm(c, false, w, r, w, Rinv, w, iu.p(), ldt, rv.p(), w, sgn.p());
     gemm(c, false, m, r, w, Q, ldq, rv.p(), w, U, ldu, nullptr, true);  // U = Q inner.v
-    copy_mat(c, iv.p(), n, V, ldv, n, r);                                  // V = inner.u
-    normalize_signs_uv(c, U, ldu, m, V, ldv, n, r);
     return r;
 }
 

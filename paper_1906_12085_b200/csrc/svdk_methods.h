@@ -52,8 +52,10 @@ void reset_nonfinite(Ctx* c);
 // sigma from eigenvalues + numerical rank (svd_methods.cpp:127-135)
 int64_t spectrum(Ctx* c, const double* w, int64_t n, double* sigma);
 // normalize_signs on already-formed U, V (svd_methods.cpp:50-71)
-void normalize_signs_uv(Ctx* c, double* U, int64_t ldu, int64_t m, double* V, int64_t ldv,
-                        int64_t n, int64_t rank);
+// normalize_signs on V alone (svd_methods.cpp:50-71): flips V's columns and
+// writes d_sign[j] = +-1, the flip its U column needs (folded into a GEMM).
+void signs_v(Ctx* c, double* V, int64_t ldv, int64_t n, int64_t rank, double* d_sign);
+
 
 int64_t truncated_svd(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n, double* U,
                       int64_t ldu, double* sigma, double* V, int64_t ldv,
