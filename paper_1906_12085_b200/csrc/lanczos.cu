@@ -16,11 +16,13 @@
 // hits L2. Per-CTA column partials are reduced in fixed order.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <string>
 #include <vector>
 
 #include "svdk_methods.h"
+#include "tma_util.h"
 
 namespace svdk {
 void gaussian_fill(int64_t rows, int64_t cols, uint64_t seed, double* out);
@@ -45,9 +47,11 @@ constexpr int GV_CTAS_PER_SM = 2;  // two CTAs per SM drift out of phase, so one
 //           registers, and a 31-shuffle butterfly transposes and reduces them
 //           so lane l ends with the full column sum of column l.
 // The slab's second read (phase 2) hits L2: 296 CTAs x 32 rows x n x 8 B.
-__global__ void __launch_bounds__(GV_THREADS, GV_CTAS_PER_SM)
+template <int GV_WARPS, int CPS>
+__global__ void __launch_bounds__(GV_WARPS * 32, CPS)
     gemv_pair_kernel(const double* __restrict__ A, int64_t lda, int64_t m, int64_t n,
                      const double* __restrict__ q, double* __restrict__ partial) {
+    constexpr int GV_THREADS = GV_WARPS * 32;
     extern __shared__ double sm[];
     double* qs = sm;            // n
     double* wacc = sm + n;      // n
@@ -116,6 +120,135 @@ __global__ void __launch_bounds__(GV_THREADS, GV_CTAS_PER_SM)
     }
     __syncthreads();
     for (int64_t j = tid; j < n; j += GV_THREADS) partial[blockIdx.x * n + j] = wacc[j];
+}
+
+// Single-read GEMV pair streamed by TMA (default when n <= 2048):
+//   w_partial[cta] = sum over the CTA's 32-row slabs of A_slab^T (A_slab q).
+// One CTA per SM; one producer thread walks the CTA's slabs and issues, per
+// slab, the T = ceil(n/64) column tiles (32 rows x 64 cols = 16 KB, one TMA
+// box each) TWICE — the first pass (y = A_slab q) pulls them from HBM, the
+// second (A_slab^T y) re-reads them from L2: 148 slabs x 32 rows x n x 8 B
+// = 78 MB at n = 2048 stay resident. Consumer warp w owns ring stage w and
+// takes tiles k = w, w + NCW, ... of the CTA's tile sequence, so the ring is
+// NCW x 16 KB of loads in flight per SM with no shared-memory contention
+// between warps. Per tile, lanes are rows: pass 1 is 64 conflict-free LDS +
+// FMA per lane; pass 2 multiplies by y_lane and reduces each 32-column group
+// across lanes with a 31-shuffle butterfly (lane l ends with column l's sum).
+// The two passes of a slab are separated by one consumer-only named barrier
+// (y complete); partial y are double-buffered by slab parity.
+constexpr int GT_NCW = 8;                 // consumer warps = ring stages
+constexpr int GT_ROWS = 32, GT_COLS = 64; // TMA box
+constexpr int GT_TILE = GT_ROWS * GT_COLS;
+
+__global__ void __launch_bounds__((GT_NCW + 1) * 32, 1)
+    gemv_pair_tma_kernel(const __grid_constant__ CUtensorMap mapA, int64_t m, int64_t n,
+                         const double* __restrict__ q, double* __restrict__ partial) {
+    extern __shared__ uint8_t gt_raw[];
+    double* ring = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(gt_raw) + 127) & ~uintptr_t(127));
+    const int T = static_cast<int>((n + GT_COLS - 1) / GT_COLS);
+    const int npad = T * GT_COLS;
+    double* qs = ring + GT_NCW * GT_TILE;   // npad (zero beyond n)
+    double* wacc = qs + npad;               // npad
+    double* ypart = wacc + npad;            // 2 x GT_NCW x 32
+    uint64_t* full = reinterpret_cast<uint64_t*>(ypart + 2 * GT_NCW * 32);
+    uint64_t* empty = full + GT_NCW;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    for (int j = tid; j < npad; j += blockDim.x) {
+        qs[j] = j < n ? q[j] : 0.0;
+        wacc[j] = 0.0;
+    }
+    if (tid == 0) {
+        for (int s = 0; s < GT_NCW; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int64_t nslabs = (m + GT_ROWS - 1) / GT_ROWS;
+    if (warp == GT_NCW) {  // ---------------- producer
+        if (lane == 0) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
+            // first read: keep the tile in L2 for the second; second: drop it
+            const uint64_t keep = l2_policy_evict_last(), drop = l2_policy_evict_first();
+            int64_t k = 0;
+            for (int64_t sl = blockIdx.x; sl < nslabs; sl += gridDim.x) {
+                const int row0 = static_cast<int>(sl * GT_ROWS);
+                for (int pass = 0; pass < 2; ++pass)
+                    for (int t = 0; t < T; ++t, ++k) {
+                        const int st = static_cast<int>(k % GT_NCW);
+                        const uint32_t use = static_cast<uint32_t>(k / GT_NCW);
+                        mbar_wait(&empty[st], (use & 1) ^ 1);
+                        mbar_expect_tx(&full[st], GT_TILE * 8);
+                        tma_load_2d_hint(ring + st * GT_TILE, &mapA, &full[st], row0, t * GT_COLS,
+                                         pass == 0 ? keep : drop);
+                    }
+            }
+        }
+        return;
+    }
+    // ---------------- consumers
+    double* tile = ring + warp * GT_TILE;  // this warp's stage
+    uint32_t uses = 0;                     // completed uses of the stage
+    int64_t base = 0;                      // CTA tile index of the slab's first tile
+    int par = 0;
+    for (int64_t sl = blockIdx.x; sl < nslabs; sl += gridDim.x, base += 2 * T, par ^= 1) {
+        // pass 1: y_lane = sum_j A[row, j] q_j over this warp's tiles
+        double yacc = 0.0;
+        int t0 = static_cast<int>(((warp - base) % GT_NCW + GT_NCW) % GT_NCW);
+        for (int t = t0; t < T; t += GT_NCW) {
+            mbar_wait(&full[warp], uses & 1);
+            const double* qt = qs + t * GT_COLS;
+            double a0 = 0.0, a1 = 0.0;
+#pragma unroll 16
+            for (int c = 0; c < GT_COLS; c += 2) {
+                a0 = fma(tile[c * GT_ROWS + lane], qt[c], a0);
+                a1 = fma(tile[(c + 1) * GT_ROWS + lane], qt[c + 1], a1);
+            }
+            yacc += a0 + a1;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[warp]);
+            ++uses;
+        }
+        double* yp = ypart + par * GT_NCW * 32;
+        yp[warp * 32 + lane] = yacc;
+        asm volatile("bar.sync 1, %0;" ::"r"(GT_NCW * 32) : "memory");
+        double y = 0.0;
+#pragma unroll
+        for (int w = 0; w < GT_NCW; ++w) y += yp[w * 32 + lane];
+        // pass 2: w_j += sum_rows A[row, j] y_row over this warp's tiles
+        t0 = static_cast<int>(((warp - base - T) % GT_NCW + GT_NCW) % GT_NCW);
+        for (int t = t0; t < T; t += GT_NCW) {
+            mbar_wait(&full[warp], uses & 1);
+#pragma unroll
+            for (int g = 0; g < GT_COLS / 32; ++g) {
+                double p[32];
+#pragma unroll
+                for (int c = 0; c < 32; ++c) p[c] = tile[(g * 32 + c) * GT_ROWS + lane] * y;
+#pragma unroll
+                for (int off = 16; off >= 1; off >>= 1) {
+                    const bool upper = (lane & off) != 0;
+#pragma unroll
+                    for (int i = 0; i < off; ++i) {
+                        const double send = upper ? p[i] : p[i + off];
+                        const double keep = upper ? p[i + off] : p[i];
+                        p[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+                    }
+                }
+                wacc[t * GT_COLS + g * 32 + lane] += p[0];
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[warp]);
+            ++uses;
+        }
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(GT_NCW * 32) : "memory");
+    for (int64_t j = tid; j < n; j += GT_NCW * 32) partial[blockIdx.x * n + j] = wacc[j];
+}
+
+size_t gemv_tma_smem(int64_t n) {
+    const int64_t npad = ceil_div(n, GT_COLS) * GT_COLS;
+    return 128 + sizeof(double) * (GT_NCW * GT_TILE + 2 * npad + 2 * GT_NCW * 32) + 2 * GT_NCW * 8;
 }
 
 // Two-pass streaming form of w = A^T (A q): both passes read A along
@@ -302,10 +435,19 @@ int64_t lanczos_svd(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n, 
                     uint64_t seed, double* U, int64_t ldu, double* sigma, double* V, int64_t ldv,
                     const RowComm* comm) {
     if (steps <= 0 || steps > n) steps = n;
-    const int parts = GV_CTAS_PER_SM * c->num_sms;
-    const size_t gv_smem = (2 * n + GV_WARPS * 32) * sizeof(double);
+    // fused-GEMV geometry (development knob SVDK_GEMV_CFG = warps x CTAs/SM)
+    int gv_warps = GV_WARPS, gv_cps = GV_CTAS_PER_SM;
+    if (const char* e = std::getenv("SVDK_GEMV_CFG")) std::sscanf(e, "%dx%d", &gv_warps, &gv_cps);
+    auto gv_kernel = gemv_pair_kernel<GV_WARPS, GV_CTAS_PER_SM>;
+    if (gv_warps == 16 && gv_cps == 1) gv_kernel = gemv_pair_kernel<16, 1>;
+    else if (gv_warps == 8 && gv_cps == 1) gv_kernel = gemv_pair_kernel<8, 1>;
+    else if (gv_warps == 32 && gv_cps == 1) gv_kernel = gemv_pair_kernel<32, 1>;
+    else if (gv_warps == 4 && gv_cps == 2) gv_kernel = gemv_pair_kernel<4, 2>;
+    else { gv_warps = GV_WARPS; gv_cps = GV_CTAS_PER_SM; }
+    const int parts = gv_cps * c->num_sms;
+    const size_t gv_smem = (2 * n + gv_warps * 32) * sizeof(double);
     if (gv_smem > 200 * 1024) fail(SVDK_E_PARAM, "lanczos_svd: n too large for the fused GEMV");
-    SVDK_CUDA(cudaFuncSetAttribute(gemv_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    SVDK_CUDA(cudaFuncSetAttribute(gv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(gv_smem)));
     DBuf Q(c, static_cast<size_t>(n) * (steps + 1)), w(c, n), partial(c, static_cast<size_t>(parts) * n),
         h(c, steps + 1), scal(c, 2 * steps + 8);
@@ -313,7 +455,18 @@ int64_t lanczos_svd(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n, 
     // A^T y (one HBM read, short DRAM runs); "two-pass" streams A twice along
     // its columns. SVDK_GEMV=fused|twopass overrides the default.
     const char* gv_env = std::getenv("SVDK_GEMV");
-    const bool two_pass = gv_env ? std::string(gv_env) == "twopass" : true;
+    const size_t tma_smem = gemv_tma_smem(n);
+    const bool tma_ok = tma_smem <= 220 * 1024 && n <= 2048 && (lda % 2 == 0) &&
+                        (reinterpret_cast<uintptr_t>(A) % 16 == 0);
+    const std::string gv_mode = gv_env ? std::string(gv_env) : (tma_ok ? "tma" : "twopass");
+    const bool use_tma = gv_mode == "tma" && tma_ok;
+    const bool two_pass = !use_tma && gv_mode != "fused";
+    CUtensorMap mapA{};
+    if (use_tma) {
+        mapA = tensor_map_2d(A, m, n, lda, GT_ROWS, GT_COLS, CU_TENSOR_MAP_SWIZZLE_NONE);
+        SVDK_CUDA(cudaFuncSetAttribute(gemv_pair_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(tma_smem)));
+    }
     const int64_t row_blocks = ceil_div(std::max<int64_t>(m, 1), GN_THREADS * GN_ROWS);
     const int64_t chunks = std::min<int64_t>(std::max<int64_t>(1, ceil_div(2 * c->num_sms, row_blocks)),
                                              std::max<int64_t>(1, n / 16));
@@ -348,12 +501,16 @@ int64_t lanczos_svd(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n, 
         } else {
             {
                 PhaseTimer timer(c, "gemv_pair", 4.0 * m * n, 8.0 * m * n);
-                gemv_pair_kernel<<<parts, GV_THREADS, gv_smem, c->stream>>>(A, lda, m, n, qj,
+                if (use_tma)
+                    gemv_pair_tma_kernel<<<c->num_sms, (GT_NCW + 1) * 32, tma_smem, c->stream>>>(
+                        mapA, m, n, qj, partial.p());
+                else
+                    gv_kernel<<<parts, gv_warps * 32, gv_smem, c->stream>>>(A, lda, m, n, qj,
                                                                             partial.p());
                 SVDK_CHECK_LAUNCH();
             }
             reduce_parts_kernel<<<static_cast<unsigned>(ceil_div(n, 256)), 256, 0, c->stream>>>(
-                partial.p(), parts, n, w.p());
+                partial.p(), use_tma ? c->num_sms : parts, n, w.p());
             SVDK_CHECK_LAUNCH();
         }
         if (comm) comm->allreduce(w.p(), static_cast<size_t>(n));
