@@ -182,6 +182,11 @@ int svdk_dev_gemm(svdk_ctx* ctx, int transa, int64_t m, int64_t n, int64_t k, co
                   int64_t lda, const double* b, int64_t ldb, double* c, int64_t ldc);
 int svdk_dev_gram(svdk_ctx* ctx, const double* a, int64_t m, int64_t n, int64_t lda, double* g,
                   int64_t ldg);
+/* w = A^T (A q), A m x n column-major (device pointers): the Lanczos matvec
+ * pair on its own (engine-internal; no reference counterpart — the reference
+ * has no Lanczos). Exposed for kernel-level parity tests. */
+int svdk_dev_gemv_pair(svdk_ctx* ctx, const double* a, int64_t m, int64_t n, int64_t lda,
+                       const double* q, double* w);
 int svdk_dev_eig_sym(svdk_ctx* ctx, const double* s, int64_t n, int64_t lds, int max_sweeps,
                      double* w, double* v, int64_t ldv);
 int svdk_dev_qr_thin(svdk_ctx* ctx, const double* h, int64_t m, int64_t p, int64_t ldh, double* q,

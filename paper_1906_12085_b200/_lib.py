@@ -60,6 +60,7 @@ SIGNATURES = {
     "svdk_residual_delta": (C.c_int, [_ctxp, _vp, _i64, _i64, _vp, _vp, _vp, _i64, _dp]),
     "svdk_dev_gemm": (C.c_int, [_ctxp, C.c_int, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64]),
     "svdk_dev_gram": (C.c_int, [_ctxp, _vp, _i64, _i64, _i64, _vp, _i64]),
+    "svdk_dev_gemv_pair": (C.c_int, [_ctxp, _vp, _i64, _i64, _i64, _vp, _vp]),
     "svdk_dev_eig_sym": (C.c_int, [_ctxp, _vp, _i64, _i64, C.c_int, _vp, _vp, _i64]),
     "svdk_dev_qr_thin": (C.c_int, [_ctxp, _vp, _i64, _i64, _i64, _vp, _i64, _vp, _ip64]),
     "svdk_dev_pca": (C.c_int, [_ctxp, _vp, _i64, _i64, _i64, C.c_int, _i64, _i64, _u64, C.c_int,

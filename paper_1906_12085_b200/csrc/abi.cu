@@ -601,6 +601,16 @@ int svdk_dev_gram(svdk_ctx* c, const double* a, int64_t m, int64_t n, int64_t ld
     });
 }
 
+int svdk_dev_gemv_pair(svdk_ctx* c, const double* a, int64_t m, int64_t n, int64_t lda, const double* q,
+                       double* w) {
+    return guarded([&] {
+        need_ctx(c);
+        if (m < 0 || n < 0 || lda < std::max<int64_t>(m, 1)) fail(SVDK_E_DIM, "gemv_pair: bad shape");
+        GemvPair g(c, a, lda, m, n);
+        g.run(q, w);
+    });
+}
+
 int svdk_dev_eig_sym(svdk_ctx* c, const double* s, int64_t n, int64_t lds, int max_sweeps,
                      double* w, double* v, int64_t ldv) {
     return guarded([&] {

@@ -4,6 +4,7 @@
 #include <functional>
 
 #include "svdk_internal.h"
+#include "tma_util.h"
 
 namespace svdk {
 
@@ -56,6 +57,32 @@ int64_t spectrum(Ctx* c, const double* w, int64_t n, double* sigma);
 // writes d_sign[j] = +-1, the flip its U column needs (folded into a GEMM).
 void signs_v(Ctx* c, double* V, int64_t ldv, int64_t n, int64_t rank, double* d_sign);
 
+
+// w = A^T (A q) (n x 1) for a fixed A: the Lanczos matvec pair (lanczos.cu).
+// Construction picks the kernel form and prepares its tensor map/workspace;
+// run() enqueues one product on the context stream (no host sync).
+class GemvPair {
+public:
+    GemvPair(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n);
+    // reduce = false leaves the cluster form's per-cluster column partials
+    // unsummed (partials()/parts(); the caller fuses the sum) — parts() is 0
+    // when w was written directly.
+    void run(const double* q, double* w, bool reduce = true);
+    bool one_read() const { return cluster_; }
+    int parts() const { return cluster_ && m_ > 0 && n_ > 0 ? nclusters_ : 0; }
+    const double* partials() const { return partial_.p(); }
+
+private:
+    Ctx* c_;
+    const double* A_;
+    int64_t lda_, m_, n_;
+    bool cluster_ = false, la_ = true;
+    int cs_ = 4, nclusters_ = 1, ncta_ = 0;
+    size_t smem_ = 0;
+    int64_t chunks_ = 1;
+    CUtensorMap map_{};
+    DBuf partial_, yv_;
+};
 
 int64_t truncated_svd(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n, double* U,
                       int64_t ldu, double* sigma, double* V, int64_t ldv,

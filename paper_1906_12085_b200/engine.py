@@ -85,6 +85,13 @@ class Engine:
                                           _p(b), _ld(b), _p(c), _ld(c)))
         return c
 
+    def gemv_pair(self, a, q, w=None):
+        """w = A^T (A q) (the Lanczos matvec pair)."""
+        m, n = a.shape
+        w = torch.empty(n, dtype=torch.float64, device=a.device) if w is None else w
+        _lib.check(self.lib.svdk_dev_gemv_pair(self.ctx.handle, _p(a), m, n, _ld(a), _p(q), _p(w)))
+        return w
+
     def eig_sym(self, s, max_sweeps: int = 30):
         n = s.shape[0]
         w = torch.empty(n, dtype=torch.float64, device=s.device)

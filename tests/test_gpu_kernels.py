@@ -163,3 +163,37 @@ def test_center_matches_reference(sk, ref):
         cr, mr = ref.center(a, o)
         assert np.max(np.abs(c.mean - mr)) <= 1e-14 * (np.abs(mr).max() + 1)
         assert np.max(np.abs(c.centered - cr)) <= 1e-13
+
+
+@pytest.mark.parametrize("form", ["cluster:1", "cluster:2", "cluster:4", "cluster:8", "twopass:4"])
+def test_gemv_pair_vs_numpy(form, monkeypatch):
+    """w = A^T (A q), the Lanczos matvec pair, in every kernel form, on ragged
+    shapes: partial 64-row slabs, partial 32-column tiles, m < 64, clusters
+    with fewer slabs than others and CTAs owning no columns. Error bound is
+    relative to |A|^T (|A| |q|); repeated runs are bit-identical (fixed-order
+    reductions)."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_1906_12085_b200.engine import Engine, colmajor
+    mode, cs = form.split(":")
+    monkeypatch.setenv("SVDK_GEMV", mode)
+    monkeypatch.setenv("SVDK_GEMV_CS", cs)
+    eng = Engine(0)
+    torch.cuda.set_stream(eng.stream)
+    rng = np.random.default_rng(77)
+    for m, n in ((1, 1), (5, 3), (63, 40), (64, 32), (1000, 130), (4099, 257), (20000, 256), (9473, 1031)):
+        a_np = rng.standard_normal((m, n))
+        q_np = rng.standard_normal(n)
+        a = colmajor(m, n)
+        a.copy_(torch.from_numpy(a_np))
+        q = torch.from_numpy(q_np).cuda()
+        torch.cuda.synchronize()
+        w1 = eng.gemv_pair(a, q).cpu().numpy()
+        w2 = eng.gemv_pair(a, q).cpu().numpy()
+        torch.cuda.synchronize()
+        ref = a_np.T @ (a_np @ q_np)
+        scale = np.abs(a_np).T @ (np.abs(a_np) @ np.abs(q_np))
+        assert np.max(np.abs(w1 - ref) / scale) < 1e-14, (m, n)
+        assert np.array_equal(w1, w2), (m, n)
+    torch.cuda.set_stream(torch.cuda.default_stream())

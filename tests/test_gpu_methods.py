@@ -158,3 +158,38 @@ def test_residual_delta_transform_truncate(sk, ref):
     c = sk.center(a, sk.Orientation.RowsAreExamples).centered
     y = sk.transform(model, c)
     assert np.allclose(y, c @ model.basis, rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("gemv", ["cluster:1", "cluster:2", "cluster:4", "cluster:8", "twopass:4"])
+def test_lanczos_gemv_forms_ragged(sk, ref, monkeypatch, gemv):
+    """Every GEMV-pair form (cluster size 1/2/4/8, two-pass fallback) on shapes
+    with partial 64-row slabs, partial 32-column tiles, m < 64 and CTAs that own
+    no columns (n < cluster x 32) — all against the reference truncated_svd."""
+    mode, cs = gemv.split(":")
+    monkeypatch.setenv("SVDK_GEMV", mode)
+    monkeypatch.setenv("SVDK_GEMV_CS", cs)
+    rng = np.random.default_rng(31)
+    for m, n in ((50, 7), (63, 40), (1000, 130), (4099, 257)):
+        a = np.asfortranarray(rng.standard_normal((m, n)))
+        r = ref.truncated_svd(a)
+        s = sk.lanczos_svd(a, 0, sk.RngSeed(2))
+        check_svd(s, r.sigma, r.v)
+
+
+def test_lanczos_breakdown_restart(sk, ref):
+    """Rank-deficient A: the Krylov space is invariant after rank(A) steps, the
+    device-side breakdown test fires and every later step restarts inside the
+    numerical null space. The true spectrum and subspace must match the
+    reference; the remaining Ritz values sit at the rounding floor (the
+    reference's own rank cut also keeps such noise: its Gram eigenvalues are
+    +-1e-16 ||A||^2, so sigma ~ 1e-8 sigma_1 passes the 1e-12 cut)."""
+    rng = np.random.default_rng(12)
+    for rank, (m, n) in ((5, (400, 40)), (17, (3000, 96))):
+        a = np.asfortranarray(rng.standard_normal((m, rank)) @ rng.standard_normal((rank, n)))
+        r = ref.truncated_svd(a)
+        s = sk.lanczos_svd(a, 0, sk.RngSeed(9))
+        assert r.rank >= rank and s.rank >= rank
+        assert eig_rel_err(s.sigma[:rank] ** 2, r.sigma[:rank] ** 2) <= 1e-10
+        assert np.all(s.sigma[rank:] <= 1e-6 * s.sigma[0])
+        assert subspace_sine(s.v[:, :rank], r.v[:, :rank]) <= 1e-8
+        assert orthogonality(s.v) <= 1e-10 and orthogonality(s.u[:, :rank]) <= 1e-8
