@@ -412,8 +412,8 @@ def ours(args, cfg):
             except Exception:
                 traffic = None
         roofline = {"bound": "hbm",
-                    "kernel": "gemv_pair_tma_kernel (Lanczos w = A^T (A q): one HBM read of A by TMA, "
-                              "second pass from L2)",
+                    "kernel": "gemv_pair_cluster_kernel (Lanczos w = A^T (A q): one HBM read of A by TMA, 4-CTA clusters, "
+                              "second pass from L2, y exchanged over DSMEM)",
                     "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                     "algorithmic_bytes_per_launch": gv["bytes"] / max(gv["count"], 1),
                     "traffic": traffic, "launches": gv["count"], "share_of_step": gv["ms"] / ms if ms else None,
