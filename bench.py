@@ -165,12 +165,16 @@ def generate(cfg, m, device, rank, seed=42):
 def reference_arm(args, cfg):
     """The reference's own CPU implementation (oracle/_ref: the unmodified
     reference sources compiled in place) on a bounded row sample of the same
-    workload, single-threaded (the reference is single-threaded by design,
-    SPEC.md:115). Work that scales with m (centering, the tall GEMMs,
-    Householder QR, U = Q W) is timed every step on m_s rows and scaled by
-    m / m_s; the m-independent small problem (Gram of T + eig_sym(l) +
-    T W, or eig_sym(n) for the Gram route) is timed once per process at the
-    full size n and added to every step."""
+    workload, on all the host threads it can use. Each reference call is
+    single-threaded by design, but callers may run independent calls in
+    parallel, so the work that scales with m (centering, the
+    tall GEMMs, Householder QR, U = Q W) runs as `threads` concurrent
+    reference pipelines on independent m_s-row samples: the step time for m
+    rows is the concurrent wall time x m / (threads x m_s), which includes
+    the cores' shared memory-bandwidth contention. The m-independent small
+    problem (Gram of T + eig_sym(l) + T W, or eig_sym(n) for the Gram route)
+    is one sequential reference call, timed once per process at full size n
+    and added to every step."""
     import numpy as np
 
     from oracle.pyoracle import Oracle, available
@@ -178,12 +182,16 @@ def reference_arm(args, cfg):
         raise SystemExit(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
     ref = Oracle("ref")
     m, n, l, q = cfg["m"] * args.gpus, cfg["n"], cfg["l"], cfg["q"]
-    rng = np.random.default_rng(7)
     full = cfg["m"] * cfg["n"] <= 20000 * 256  # c1 runs whole
     ms = m if full else max(n, 1024)
-    a = np.asfortranarray(rng.standard_normal((ms, n)) * np.array([SPECTRA[cfg["spec"]](i) for i in range(1, n + 1)]))
+    threads = max(1, int(getattr(args, "ref_threads", 0) or len(os.sched_getaffinity(0))))
+    threads = min(threads, 128)
+    scale = np.array([SPECTRA[cfg["spec"]](i) for i in range(1, n + 1)])
+    samples = [np.asfortranarray(np.random.default_rng(7 + i).standard_normal((ms, n)) * scale)
+               for i in range(threads if not full else 1)]
+    a = samples[0]
 
-    def rows_part():
+    def rows_part(a=a):
         t0 = time.perf_counter()
         c, _ = ref.center(a, 1)
         ref.frobenius_norm_sq(c)
@@ -209,6 +217,7 @@ def reference_arm(args, cfg):
             ref.frobenius_norm_sq(c)
             ref.truncated_svd(c)
             return time.perf_counter() - t0
+        threads = 1  # one whole-matrix reference call: nothing independent to run beside it
         sample = f"full reference fit_pca (center, total, truncated_svd) on {m}x{n}"
     else:
         _, small = rows_part()
@@ -230,11 +239,21 @@ def reference_arm(args, cfg):
         if extrap:
             fixed *= 12.0 ** math.log2(n / 512)
 
+        from concurrent.futures import ThreadPoolExecutor
+        pool = ThreadPoolExecutor(max_workers=threads) if threads > 1 else None
+
         def step():
-            t, _ = rows_part()
-            return t * (m / ms) + fixed
-        sample = (f"reference kernels on {ms} of {m} rows (x{m / ms:.0f}, m-proportional phases) + "
-                  f"m-independent small problem timed once ({fixed:.1f} s{extrap})")
+            # ctypes releases the GIL for the duration of each reference call
+            t0 = time.perf_counter()
+            if pool is None:
+                rows_part(samples[0])
+            else:
+                list(pool.map(rows_part, samples))
+            t = time.perf_counter() - t0
+            return t * (m / (ms * threads)) + fixed
+        sample = (f"{threads} concurrent reference pipelines, each on its own {ms}-row sample (x{m / (ms * threads):.1f}"
+                  f" to {m} rows, m-proportional phases) + m-independent small problem (one sequential reference "
+                  f"call) timed once ({fixed:.1f} s{extrap})")
     for _ in range(args.warmup):
         step()
     ts = [step() for _ in range(args.steps)]
@@ -245,7 +264,7 @@ def reference_arm(args, cfg):
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded Gaussian sample)",
             "impl": "reference",
             "config": {"workload": cfg["desc"], "m": m, "n": n, "method": cfg["method"], "l": l, "q": q},
-            "cpu_baseline": {"value": value, "unit": "rows/s", "cores": 1, "kind": "reference", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": "rows/s", "cores": threads, "kind": "reference", "sample": sample},
             "e2e": {"value": value, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
@@ -282,8 +301,10 @@ def ours(args, cfg):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         ncpu = os.cpu_count() or 1
         env = dict(os.environ, CUDA_VISIBLE_DEVICES="")
+        # the in-run baseline stays on ONE pinned core so it cannot disturb the
+        # GPU run's host thread; `--impl reference` alone uses every core
         cmd = [sys.executable, os.path.abspath(__file__), "--impl", "reference", "--config", args.config,
-               "--steps", "1", "--warmup", "0"]
+               "--steps", "1", "--warmup", "0", "--ref-threads", "1"]
         if ncpu > 2:
             cmd = ["taskset", "-c", str(ncpu - 1)] + cmd
             os.sched_setaffinity(0, set(range(ncpu - 1)))
@@ -479,6 +500,8 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-threads", type=int, default=0,
+                    help="--impl reference: concurrent reference pipelines (default: every usable core)")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.config == "c4":
