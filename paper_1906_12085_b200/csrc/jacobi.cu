@@ -148,9 +148,15 @@ __device__ __forceinline__ void smem_mma(const double* A, const double* Bm, doub
 __device__ long long g_jprobe[8];
 
 template <int TB>
+constexpr int solve_q_warps() {
+    // Q <- Q J is split over warps by rows (TB = 32: 4 warps x 8 rows): one warp
+    // doing all 32 rows was a ~1k-cycle shuffle/FP64 chain per inner round
+    return TB == 32 ? 4 : 1;
+}
+template <int TB>
 constexpr int solve_threads() {
-    // M threads (one 2x2 block each) + 1 Q warp (Q in registers) + 1 lookahead warp
-    return (TB / 2) * (TB / 2) + 32 + 32;
+    // M threads (one 2x2 block each) + the Q warps (Q in registers) + 1 lookahead warp
+    return (TB / 2) * (TB / 2) + 32 * solve_q_warps<TB>() + 32;
 }
 
 // R_i^T B R_j on the 2x2 block B = [[m00, m01], [m10, m11]] of rows (p_i, q_i)
@@ -173,6 +179,19 @@ __device__ __forceinline__ void xform2x2(double& m00, double& m01, double& m10, 
             m10 = 0.0;
         }
     }
+}
+
+// Entry (u, v) of R_i^T B R_j alone, in xform2x2's operation order (columns
+// first, then rows; a skipped rotation (s == 0) passes values through).
+__device__ __forceinline__ double xform_entry(double m00, double m01, double m10, double m11, double ci,
+                                              double si, double cj, double sj, int u, int v) {
+    double t0 = v ? m01 : m00, t1 = v ? m11 : m10;
+    if (sj != 0.0) {
+        t0 = v ? fma(sj, m00, cj * m01) : fma(cj, m00, -(sj * m01));
+        t1 = v ? fma(sj, m10, cj * m11) : fma(cj, m10, -(sj * m11));
+    }
+    if (si == 0.0) return u ? t1 : t0;
+    return u ? fma(si, t0, ci * t1) : fma(ci, t0, -(si * t1));
 }
 
 // Inner schedule of a 2b subproblem for one mode (identical for every pair
@@ -253,7 +272,8 @@ __device__ __forceinline__ void solve_pair(const double* A, int64_t lda, const S
     constexpr int B = TB / 2, LD = TB + 4, NP = TB / 2, RMAX = TB - 1;
     const int R = mode == 0 ? TB - 1 : (mode == 1 ? B - 1 : B);
     constexpr int MT = NP * NP;  // M threads
-    constexpr int QT = 32;       // the Q warp: lane l holds column l of Q in registers
+    constexpr int QW = solve_q_warps<TB>(), QR = TB / QW;
+    constexpr int QT = 32 * QW;  // Q warps: lane l of warp h holds rows [h QR, (h+1) QR) of column l
     extern __shared__ double sm[];
     double* Mc = sm;             // current M
     double* Mn = Mc + TB * LD;   // next M (double buffer)
@@ -325,9 +345,10 @@ __device__ __forceinline__ void solve_pair(const double* A, int64_t lda, const S
             sn[r][i] = s;
         };
         if (lane >= 0 && lane < NP) rot_of(0, lane, Mc);
-        double qreg[TB];  // the Q warp's column (lane < TB)
+        double qreg[QR];  // the Q warps' column slices (lane < TB)
+        const int qrow0 = ((tid - MT) >> 5) * QR;
 #pragma unroll
-        for (int i = 0; i < TB; ++i) qreg[i] = (i == ((tid - MT) & 31)) ? 1.0 : 0.0;
+        for (int i = 0; i < QR; ++i) qreg[i] = (qrow0 + i == ((tid - MT) & 31)) ? 1.0 : 0.0;
         __syncthreads();
         const int total = max_inner * R;
         for (int it = 0; it < total; ++it) {
@@ -349,7 +370,7 @@ __device__ __forceinline__ void solve_pair(const double* A, int64_t lda, const S
             } else if (tid < MT + QT) {
                 // Q <- Q J: columns p, q of a rotation mix; partner columns are
                 // exchanged by warp shuffles (no shared-memory traffic)
-                const int l = tid - MT;
+                const int l = (tid - MT) & 31;
                 const int code = pinv[rr][l & (TB - 1)];
                 const int j = code & 127, role = code >> 7;
                 const int pq = ptab[rr][j];
@@ -357,7 +378,7 @@ __device__ __forceinline__ void solve_pair(const double* A, int64_t lda, const S
                 // branch-free: a skipped pair has (c, s) = (1, 0)
                 const double c = cs[rr][j], b = role ? sn[rr][j] : -sn[rr][j];
 #pragma unroll
-                for (int i = 0; i < TB; ++i) {
+                for (int i = 0; i < QR; ++i) {
                     const double other = __shfl_sync(0xffffffffu, qreg[i], partner);
                     qreg[i] = fma(b, other, c * qreg[i]);
                 }
@@ -377,12 +398,11 @@ __device__ __forceinline__ void solve_pair(const double* A, int64_t lda, const S
                 double b10 = Mc[q2 + p2 * LD], b11 = Mc[q2 + q2 * LD];
                 double x00 = Mc[p1 + p2 * LD], x01 = Mc[p1 + q2 * LD];
                 double x10 = Mc[q1 + p2 * LD], x11 = Mc[q1 + q2 * LD];
-                xform2x2(a00, a01, a10, a11, cp, sp, cp, sp, true);
-                xform2x2(b00, b01, b10, b11, cq, sq, cq, sq, true);
-                xform2x2(x00, x01, x10, x11, cp, sp, cq, sq, false);
-                const double app = rp ? a11 : a00;
-                const double aqq = rq ? b11 : b00;
-                const double x = rp ? (rq ? x11 : x10) : (rq ? x01 : x00);
+                // only the three entries the new rotation needs, each with the
+                // operation order of xform2x2 (same bits as the M threads)
+                const double app = xform_entry(a00, a01, a10, a11, cp, sp, cp, sp, rp, rp);
+                const double aqq = xform_entry(b00, b01, b10, b11, cq, sq, cq, sq, rq, rq);
+                const double x = xform_entry(x00, x01, x10, x11, cp, sp, cq, sq, rp, rq);
                 long long t1 = pr ? SVDK_CLOCK() : 0;
                 double c = 1.0, s = 0.0;
                 if (fabs(x) > skip_tau) rotation(app, aqq, x, c, s);
@@ -403,10 +423,10 @@ __device__ __forceinline__ void solve_pair(const double* A, int64_t lda, const S
             Mc = Mn;
             Mn = t;
         }
-        if (tid >= MT && tid < MT + TB) {  // Q columns back to shared memory
-            const int l = tid - MT;
+        if (tid >= MT && tid < MT + QT && ((tid - MT) & 31) < TB) {  // Q slices back to shared memory
+            const int l = (tid - MT) & 31;
 #pragma unroll
-            for (int i = 0; i < TB; ++i) Q[i + l * LD] = qreg[i];
+            for (int i = 0; i < QR; ++i) Q[(qrow0 + i) + l * LD] = qreg[i];
         }
         __syncthreads();
         if (probe) SVDK_PROBE_STORE(g_jprobe, 2, SVDK_CLOCK());
