@@ -567,6 +567,18 @@ __device__ __forceinline__ double q_frag(const double* Qp, bool act, int k, int 
     return act ? __ldcg(&Qp[k + n * 32]) : (k == n ? 1.0 : 0.0);
 }
 
+// 32-byte global accesses (one full sector; LDG/STG.E.ENL2.256 on sm_100)
+__device__ __forceinline__ double4 ld_cg4(const double* p) {
+    double4 v;
+    asm volatile("ld.global.cg.v4.f64 {%0, %1, %2, %3}, [%4];"
+                 : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w)
+                 : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void st4(double* p, double a, double b, double c, double d) {
+    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+}
+
 constexpr int UPD_WARPS = 4;
 
 // A[IJ_p, IJ_q] <- Q_p^T A[IJ_p, IJ_q] Q_q for one (p <= q) per warp; the
@@ -652,7 +664,15 @@ __device__ __forceinline__ void upd_a_unit(double* A, int64_t lda, const double*
     }
 }
 
-// V[rows, IJ_q] <- V[rows, IJ_q] Q_q; one warp per (32-row tile, pair q).
+// V[rows, IJ_q] <- V[rows, IJ_q] Q_q; one warp per (pair q, VT_ROWS-row chunk).
+// Rows inside a 32-row tile are permuted so that m8n8k4 row r of m-tile m is
+// tile row 4r + m (each output row depends only on its own input row): lane
+// (r, kq) then owns 4 CONSECUTIVE rows of a column, and every access is one
+// 32-byte load/store (8 + 8 per tile instead of 32 + 32 scattered 8-byte
+// ones). Q_q's fragments are loaded once per warp; the next tile's loads are
+// in flight while the current tile's DMMAs run.
+constexpr int VT_ROWS = 128;
+
 __device__ __forceinline__ void upd_v_unit(double* V, int64_t ldv, int64_t n_rows,
                                            const double* Qbuf, const int* active, int nb, int round,
                                            int64_t u) {
@@ -660,39 +680,52 @@ __device__ __forceinline__ void upd_v_unit(double* V, int64_t ldv, int64_t n_row
     const int lane = threadIdx.x & 31, r = lane >> 2, kq = lane & 3;
     const int k = nb / 2;
     const int q = static_cast<int>(u % k);
-    const int64_t row0 = (u / k) * 32;
-    if (row0 >= n_rows || !__ldcg(&active[q])) return;
+    const int64_t row_begin = (u / k) * VT_ROWS;
+    if (row_begin >= n_rows || !__ldcg(&active[q])) return;
+    const int64_t row_end = min(n_rows, row_begin + VT_ROWS);
     int Iq, Jq;
     circle_pair(nb, round, q, Iq, Jq);
     const double* Qb = Qbuf + static_cast<size_t>(q) * 1024;
-    double va[4][8], qb[8][4];
-#pragma unroll
-    for (int s = 0; s < 8; ++s) {
-        const int64_t col = gidx(B, Iq, Jq, 4 * s + kq) * ldv;
-#pragma unroll
-        for (int m = 0; m < 4; ++m) va[m][s] = __ldcg(&V[row0 + 8 * m + r + col]);
-#pragma unroll
-        for (int t = 0; t < 4; ++t) qb[s][t] = __ldcg(&Qb[(4 * s + kq) + (8 * t + r) * 32]);
-    }
-    double acc[4][4][2];
-#pragma unroll
-    for (int m = 0; m < 4; ++m)
-#pragma unroll
-        for (int t = 0; t < 4; ++t) acc[m][t][0] = acc[m][t][1] = 0.0;
+    double qb[8][4];
 #pragma unroll
     for (int s = 0; s < 8; ++s)
 #pragma unroll
+        for (int t = 0; t < 4; ++t) qb[s][t] = __ldcg(&Qb[(4 * s + kq) + (8 * t + r) * 32]);
+    double* vb = V + 4 * r;
+    double4 va[8];
+#pragma unroll
+    for (int s = 0; s < 8; ++s) va[s] = ld_cg4(vb + row_begin + gidx(B, Iq, Jq, 4 * s + kq) * ldv);
+    for (int64_t row0 = row_begin; row0 < row_end; row0 += 32) {
+        const bool more = row0 + 32 < row_end;
+        double4 vn[8];
+        if (more) {
+#pragma unroll
+            for (int s = 0; s < 8; ++s) vn[s] = ld_cg4(vb + row0 + 32 + gidx(B, Iq, Jq, 4 * s + kq) * ldv);
+        }
+        double acc[4][4][2];
+#pragma unroll
         for (int m = 0; m < 4; ++m)
 #pragma unroll
-            for (int t = 0; t < 4; ++t) dmma(acc[m][t][0], acc[m][t][1], va[m][s], qb[s][t]);
+            for (int t = 0; t < 4; ++t) acc[m][t][0] = acc[m][t][1] = 0.0;
 #pragma unroll
-    for (int t = 0; t < 4; ++t)
+        for (int s = 0; s < 8; ++s) {
+            const double am[4] = {va[s].x, va[s].y, va[s].z, va[s].w};
 #pragma unroll
-        for (int i = 0; i < 2; ++i) {
-            const int64_t col = gidx(B, Iq, Jq, 8 * t + 2 * kq + i) * ldv;
+            for (int m = 0; m < 4; ++m)
 #pragma unroll
-            for (int m = 0; m < 4; ++m) V[row0 + 8 * m + r + col] = acc[m][t][i];
+                for (int t = 0; t < 4; ++t) dmma(acc[m][t][0], acc[m][t][1], am[m], qb[s][t]);
         }
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+                st4(vb + row0 + gidx(B, Iq, Jq, 8 * t + 2 * kq + i) * ldv, acc[0][t][i], acc[1][t][i],
+                    acc[2][t][i], acc[3][t][i]);
+        if (more) {
+#pragma unroll
+            for (int s = 0; s < 8; ++s) va[s] = vn[s];
+        }
+    }
 }
 
 __global__ void __launch_bounds__(UPD_WARPS * 32)
@@ -875,7 +908,7 @@ void run_sweeps(Ctx* c, double* A, double* V, int64_t n_pad, int max_sweeps, dou
     const bool reg_upd = TB == 32 && !(upd_env && std::string(upd_env) == "smem");
     const int a_warp_ctas = static_cast<int>(ceil_div(static_cast<int64_t>(a_ctas), UPD_WARPS));
     const int v_warp_ctas =
-        static_cast<int>(ceil_div(ceil_div(n_pad, static_cast<int64_t>(32)) * k, UPD_WARPS));
+        static_cast<int>(ceil_div(ceil_div(n_pad, static_cast<int64_t>(VT_ROWS)) * k, UPD_WARPS));
     auto launch_updates = [&](const double* qr, const int* ar, int r) {
         if (reg_upd) {
             jacobi_update_v_reg<<<v_warp_ctas, UPD_WARPS * 32, 0, S2>>>(V, n_pad, n_pad, qr, ar, nb, r);
