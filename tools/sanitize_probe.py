@@ -22,4 +22,13 @@ for m, n in ((37, 13), (130, 66), (300, 129)):
     sk.fit_pca(a, sk.Orientation.RowsAreExamples, sk.SvdMethod.Randomized, sk.MethodParams(n, 1, sk.RngSeed(2)))
     sk.residual_delta(a, s)
 sk.qr_thin(np.zeros((20, 4)))
+# Lanczos GEMV pair in every cluster size (1/2/4 CTAs exchanging y over DSMEM)
+# and the device-side breakdown/restart path (rank-deficient A)
+import os  # noqa: E402
+b = np.asfortranarray(rng.standard_normal((300, 3)) @ rng.standard_normal((3, 40)))
+for cs in ("1", "2", "4"):
+    os.environ["SVDK_GEMV_CS"] = cs
+    sk.lanczos_svd(np.asfortranarray(rng.standard_normal((333, 150))), 0, sk.RngSeed(3))
+    sk.lanczos_svd(b, 0, sk.RngSeed(4))
+os.environ.pop("SVDK_GEMV_CS")
 print("sanitize probe done")
