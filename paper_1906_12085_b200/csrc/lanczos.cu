@@ -426,12 +426,38 @@ __global__ void __launch_bounds__(GT_THREADS)
     }
 }
 
+// s + sum_{b < count} p[b * stride], added in index order (bit-identical to
+// the plain loop) with 8 loads in flight instead of one
+__device__ __forceinline__ double ordered_sum(double s, const double* p, int count, int64_t stride) {
+    int b = 0;
+    for (; b + 8 <= count; b += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldcg(p + (b + u) * stride);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s += v[u];
+    }
+    for (; b < count; ++b) s += __ldcg(p + b * stride);
+    return s;
+}
+// x - sum in the same order: x -= p[0], x -= p[stride], ...
+__device__ __forceinline__ double ordered_sub(double x, const double* p, int count, int64_t stride) {
+    int b = 0;
+    for (; b + 8 <= count; b += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldcg(p + (b + u) * stride);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) x -= v[u];
+    }
+    for (; b < count; ++b) x -= __ldcg(p + b * stride);
+    return x;
+}
+
 __global__ void reduce_parts_kernel(const double* partial, int parts, int64_t n, double* w) {
     const int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (j >= n) return;
-    double s = 0.0;
-    for (int b = 0; b < parts; ++b) s += partial[b * n + j];
-    w[j] = s;
+    w[j] = ordered_sum(0.0, partial + j, parts, n);
 }
 
 __device__ double block_sum(double v, double* red) {
@@ -468,15 +494,14 @@ __device__ __forceinline__ bool last_cta_done(unsigned* counter, unsigned total)
 __global__ void __launch_bounds__(256) reduce_alpha_kernel(const double* partial, int parts, int64_t n,
                                                             double* w, const double* q, const double* qprev,
                                                             const double* beta_prev, double* alpha_out,
-                                                            double* dots, unsigned* counter) {
+                                                            double* dots, unsigned* counter, double* nrm0) {
     __shared__ double red[32];
     const int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     double d = 0.0;
     if (j < n) {
         double s;
         if (parts > 0) {
-            s = 0.0;
-            for (int b = 0; b < parts; ++b) s += partial[b * n + j];
+            s = ordered_sum(0.0, partial + j, parts, n);
             w[j] = s;
         } else {
             s = w[j];
@@ -489,18 +514,25 @@ __global__ void __launch_bounds__(256) reduce_alpha_kernel(const double* partial
     double a = 0.0;
     for (unsigned b = 0; b < gridDim.x; ++b) a += __ldcg(dots + b);
     const double bp = beta_prev ? *beta_prev : 0.0;
+    double ss = 0.0;
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
         double x = __ldcg(w + i) - a * q[i];
         if (qprev) x -= bp * qprev[i];
         w[i] = x;
+        ss = fma(x, x, ss);
     }
-    if (threadIdx.x == 0) *alpha_out = a;
+    ss = block_sum(ss, red);
+    if (threadIdx.x == 0) {
+        *alpha_out = a;
+        *nrm0 = sqrt(ss);  // ||w|| before reorthogonalisation
+    }
 }
 
 // h_k = Q[:, k]^T w for k < cols (one warp per column, 8 independent chains:
 // Q_j is L2-resident and this is load-latency bound)
 __global__ void __launch_bounds__(256) cgs_dot_kernel(const double* Q, int64_t ldq, int64_t n, int64_t cols,
-                                                       const double* w, double* h) {
+                                                       const double* w, double* h, const double* skip) {
+    if (skip && *skip != 0.0) return;  // second pass not needed this step
     const int64_t k = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (k >= cols) return;
@@ -531,10 +563,17 @@ __global__ void __launch_bounds__(256) cgs_dot_kernel(const double* Q, int64_t l
 // the last row block finishes ||w|| (fixed order throughout).
 constexpr int CGS_ROWS = 256;
 constexpr int CGS_MAXKC = 48;  // column chunks: ~a wave of CTAs at n = 2048
+// Pass 1 (decide != nullptr) also applies "twice is enough" (Kahan-Parlett):
+// if ||w1|| >= ||w0|| / sqrt(2) the projection removed only rounding-level
+// components, w1 is orthogonal to Q_j to working precision, and pass 2 is
+// skipped (its kernels see *skip != 0 and return; nrm[1] = nrm[0]). When it
+// removed more (loss of orthogonality, or a true breakdown), pass 2 runs.
 __global__ void __launch_bounds__(CGS_ROWS) cgs_update_norm_kernel(const double* Q, int64_t ldq, int64_t n,
                                                                    int64_t cols, int64_t kw, const double* h,
                                                                    double* w, double* part, double* sq,
-                                                                   unsigned* counters, double* nrm_out) {
+                                                                   unsigned* counters, double* nrm_out,
+                                                                   const double* nrm0, double* skip) {
+    if (!nrm0 && skip && *skip != 0.0) return;  // pass 2, not needed this step
     __shared__ double hs[512];
     __shared__ double red[32];
     const int rb = blockIdx.x, kc = blockIdx.y, nkc = gridDim.y, nrb = gridDim.x;
@@ -567,8 +606,7 @@ __global__ void __launch_bounds__(CGS_ROWS) cgs_update_norm_kernel(const double*
     if (!last_cta_done(counters + rb, nkc)) return;
     double ss = 0.0;
     if (i < n) {
-        double x = __ldcg(w + i);
-        for (int c = 0; c < nkc; ++c) x -= __ldcg(part + c * n + i);
+        const double x = ordered_sub(__ldcg(w + i), part + i, nkc, n);
         w[i] = x;
         ss = x * x;
     }
@@ -578,7 +616,13 @@ __global__ void __launch_bounds__(CGS_ROWS) cgs_update_norm_kernel(const double*
     if (threadIdx.x == 0) {
         double t = 0.0;
         for (int b = 0; b < nrb; ++b) t += __ldcg(sq + b);
-        *nrm_out = sqrt(t);
+        const double nw = sqrt(t);
+        *nrm_out = nw;
+        if (nrm0) {  // pass 1: decide whether pass 2 is needed
+            const bool enough = nw >= 0.70710678118654752 * *nrm0;
+            *skip = enough ? 1.0 : 0.0;
+            if (enough) nrm_out[1] = nw;
+        }
     }
 }
 
@@ -804,8 +848,8 @@ int64_t lanczos_svd(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n, 
     double* alpha = scal.p();
     double* beta = scal.p() + steps;
     double* nrm = scal.p() + 2 * steps;    // [0] after CGS pass 1, [1] after pass 2
-    double* state = scal.p() + 2 * steps + 2;  // gnorm, prev_beta, restart flag
-    fill(c, state, 3, 0.0);
+    double* state = scal.p() + 2 * steps + 2;  // gnorm, prev_beta, restart flag, ||w0||, skip pass 2
+    fill(c, state, 5, 0.0);
     // step-tail workspaces: per-CTA partials and last-CTA counters (zeroed once;
     // every kernel resets the counters it used)
     const int64_t nb256 = ceil_div(n, 256);
@@ -829,18 +873,19 @@ int64_t lanczos_svd(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n, 
         const int parts = comm ? 0 : gemv.parts();
         reduce_alpha_kernel<<<static_cast<unsigned>(nb256), 256, 0, c->stream>>>(
             gemv.partials(), parts, n, w.p(), qj, j > 0 ? Q.p() + (j - 1) * n : nullptr,
-            j > 0 ? beta + (j - 1) : nullptr, alpha + j, red.p(), cnt);
+            j > 0 ? beta + (j - 1) : nullptr, alpha + j, red.p(), cnt, state + 3);
         SVDK_CHECK_LAUNCH();
         const int64_t cols = j + 1;
         const int64_t nkc = std::min<int64_t>(CGS_MAXKC, ceil_div(cols, 32));
         const int64_t kw = ceil_div(cols, nkc);
         for (int pass = 0; pass < 2; ++pass) {
+            double* skip = state + 4;  // set by pass 1, read by pass 2
             cgs_dot_kernel<<<static_cast<unsigned>(ceil_div(cols * 32, 256)), 256, 0, c->stream>>>(
-                Q.p(), n, n, cols, w.p(), h.p());
+                Q.p(), n, n, cols, w.p(), h.p(), pass == 1 ? skip : nullptr);
             SVDK_CHECK_LAUNCH();
             cgs_update_norm_kernel<<<dim3(static_cast<unsigned>(nb256), static_cast<unsigned>(nkc)), CGS_ROWS,
                                      0, c->stream>>>(Q.p(), n, n, cols, kw, h.p(), w.p(), part.p(), red.p(),
-                                                     cnt + 1, nrm + pass);
+                                                     cnt + 1, nrm + pass, pass == 0 ? state + 3 : nullptr, skip);
             SVDK_CHECK_LAUNCH();
         }
         const bool last = j + 1 == steps;
