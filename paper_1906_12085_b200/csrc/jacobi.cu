@@ -82,17 +82,19 @@ __device__ __forceinline__ int64_t gidx(int B, int I, int J, int i) {
 
 // C = op(A) * B on TB x TB shared-memory matrices (col-major, ld TB+4) with
 // FP64 DMMA; result is written to C (same layout). No block barrier inside.
+// smem_mma_t: the same, run by the `nthr` threads tid in [0, nthr) of a
+// thread group (warp-aligned) instead of the whole block.
 template <int TB, bool TRANS_A>
-__device__ __forceinline__ void smem_mma(const double* A, const double* Bm, double* C) {
+__device__ __forceinline__ void smem_mma_t(const double* A, const double* Bm, double* C, int tid, int nthr) {
     constexpr int LD = TB + 4;
     constexpr int NT = TB / 8;
     constexpr int WTM = NT >= 8 ? 2 : 1;
     constexpr int WTN = NT >= 8 ? 4 : (NT >= 4 ? 2 : 1);
     constexpr int WARPS_M = NT / WTM, WARPS_N = NT / WTN;
     static_assert(WARPS_M * WARPS_N <= 8, "tile split");
-    const int lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+    const int lane = tid & 31, nwarps = nthr >> 5;
     const int r = lane >> 2, kq = lane & 3;
-    for (int wt = threadIdx.x >> 5; wt < WARPS_M * WARPS_N; wt += nwarps) {
+    for (int wt = tid >> 5; wt < WARPS_M * WARPS_N; wt += nwarps) {
         const int wm = wt % WARPS_M, wn = wt / WARPS_M;
         double acc[WTM][WTN][2];
 #pragma unroll
@@ -128,6 +130,11 @@ __device__ __forceinline__ void smem_mma(const double* A, const double* Bm, doub
                 C[row + (col + 1) * LD] = acc[a][b][1];
             }
     }
+}
+
+template <int TB, bool TRANS_A>
+__device__ __forceinline__ void smem_mma(const double* A, const double* Bm, double* C) {
+    smem_mma_t<TB, TRANS_A>(A, Bm, C, threadIdx.x, blockDim.x);
 }
 
 // ---------------------------------------------------------------------------
@@ -980,7 +987,553 @@ void run_sweeps(Ctx* c, double* A, double* V, int64_t n_pad, int max_sweeps, dou
     if (exec) cudaGraphExecDestroy(exec);
 }
 
+// ---------------------------------------------------------------------------
+// 3. quad scheme: 64-wide updates (two 16-block rounds per similarity)
+// ---------------------------------------------------------------------------
+// The indices are cut into blocks of 16 and SUPER-blocks of 32 (blocks 2s,
+// 2s+1). A sweep is the ns-1 rounds of a round-robin tournament over the ns
+// super-blocks; in round r, super-pair (S, T) = ({I, J}, {K, L}) owns the
+// 64 x 64 subproblem A[S T, S T] and rotates, as two 16-block "sub-stages"
+// of two disjoint 32 x 32 cross solves each,
+//     sub-stage B: (I, K) and (J, L)        sub-stage C: (I, L) and (J, K),
+// i.e. all S x T cross pairs. Round 0 first runs sub-stage A: (I, J) and
+// (K, L) with all pairs (mode 0), which covers every pair inside each super-
+// block. So a sweep still rotates every index pair exactly once, like the
+// reference's cyclic sweep, with the same 32 x 32 solve (and rotation
+// formulas) as the 2b = 32 scheme; what changes is that the two sub-stages'
+// rotations are composed into ONE 64 x 64 Q per super-pair inside the solve
+// CTA (the second sub-stage sees the first one's similarity, applied to the
+// 64 x 64 block in shared memory), so the full-matrix A and V updates run
+// once per two 16-block rounds: half the HBM traffic for the same DMMA work
+// (arithmetic intensity 8 instead of 4 flop/B, above the B200 FP64 ridge).
+constexpr int L64 = 68;  // ld of 64 x 64 shared tiles (== 4 mod 16: conflict-free fragment loads)
+constexpr int L32 = 36;
+constexpr int QH = 256 + 128 + 32;  // threads per 32 x 32 solve: M threads, 4 Q warps, lookahead warp
+constexpr int Q_THREADS = 2 * QH;  // two concurrent solves per CTA
+constexpr int SUB32 = 32 * L32;
+static_assert(QH == solve_threads<32>(), "solve roles");
+constexpr size_t QUAD_SMEM =
+    (3 * 64 * L64 + 8 * SUB32 + 4 * 31 * 16) * sizeof(double) + sizeof(SolveTables<32>) + 16;
+
+__device__ __forceinline__ void named_bar(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// Local-64 index (blocks I J K L = 16-index groups 0..3) of local index i of
+// half h's 32 x 32 subproblem in sub-stage `kind` (0 = A, 1 = B, 2 = C).
+__device__ __forceinline__ int quad_idx(int kind, int h, int i) {
+    if (kind == 0) return 32 * h + i;                    // {I, J} | {K, L}
+    if (kind == 1) return (i < 16 ? i : i + 16) + 16 * h;  // {I, K} | {J, L}
+    return h ? 16 + i : (i < 16 ? i : i + 32);           // {I, L} | {J, K}
+}
+
+// One 32 x 32 solve of a quad sub-stage, run by the QH threads of one half
+// (ltid in [0, QH)) and synchronised by named barrier `bar`: the inner rounds
+// of solve_pair (same roles, same operation order), then the Newton-Schulz
+// step. Mc holds the subproblem on entry; Ts holds the rotation on exit
+// (identity when !work).
+__device__ __forceinline__ void quad_sub_solve(double* Mc, double* Mn, double* Qs, double* Ts,
+                                               const SolveTables<32>& st, double (*cs)[16],
+                                               double (*sn)[16], int R, int ltid, int bar, bool work,
+                                               double skip_tau) {
+    constexpr int TB = 32, LD = L32, NP = 16, MT = 256, QR = 8, QT = 128;
+    if (!work) {
+        for (int e = ltid; e < TB * TB; e += QH) Ts[(e & 31) + (e >> 5) * LD] = (e & 31) == (e >> 5) ? 1.0 : 0.0;
+        named_bar(bar, QH);
+        return;
+    }
+    const auto& ptab = st.ptab;
+    const auto& pinv = st.pinv;
+    const auto& look = st.look;
+    const int lane = ltid - (MT + QT);
+    if (lane >= 0 && lane < NP) {
+        const int code = ptab[0][lane];
+        const int p = code & 255, q = code >> 8;
+        const double x = Mc[p + q * LD];
+        double c = 1.0, s = 0.0;
+        if (fabs(x) > skip_tau) rotation(Mc[p + p * LD], Mc[q + q * LD], x, c, s);
+        cs[0][lane] = c;
+        sn[0][lane] = s;
+    }
+    double qreg[QR];
+    const int qrow0 = ((ltid - MT) >> 5) * QR;
+#pragma unroll
+    for (int i = 0; i < QR; ++i) qreg[i] = (qrow0 + i == ((ltid - MT) & 31)) ? 1.0 : 0.0;
+    named_bar(bar, QH);
+    for (int rr = 0; rr < R; ++rr) {
+        if (ltid < MT) {
+            const int bi = ltid % NP, bj = ltid / NP;
+            const int ci_code = ptab[rr][bi], cj_code = ptab[rr][bj];
+            const int pi = ci_code & 255, qi = ci_code >> 8;
+            const int pj = cj_code & 255, qj = cj_code >> 8;
+            double m00 = Mc[pi + pj * LD], m01 = Mc[pi + qj * LD];
+            double m10 = Mc[qi + pj * LD], m11 = Mc[qi + qj * LD];
+            xform2x2(m00, m01, m10, m11, cs[rr][bi], sn[rr][bi], cs[rr][bj], sn[rr][bj], bi == bj);
+            Mn[pi + pj * LD] = m00;
+            Mn[pi + qj * LD] = m01;
+            Mn[qi + pj * LD] = m10;
+            Mn[qi + qj * LD] = m11;
+        } else if (ltid < MT + QT) {
+            const int l = (ltid - MT) & 31;
+            const int code = pinv[rr][l];
+            const int j = code & 127, role = code >> 7;
+            const int pq = ptab[rr][j];
+            const int partner = role ? (pq & 255) : (pq >> 8);
+            const double c = cs[rr][j], b = role ? sn[rr][j] : -sn[rr][j];
+#pragma unroll
+            for (int i = 0; i < QR; ++i) {
+                const double other = __shfl_sync(0xffffffffu, qreg[i], partner);
+                qreg[i] = fma(b, other, c * qreg[i]);
+            }
+        } else if (lane < NP && rr + 1 < R) {
+            const int nr = rr + 1;
+            const unsigned long long d = look[rr][lane];
+            const int bp = d & 31, bq = (d >> 5) & 31;
+            const int rp = (d >> 10) & 1, rq = (d >> 11) & 1;
+            const int p1 = (d >> 12) & 31, q1 = (d >> 17) & 31;
+            const int p2 = (d >> 22) & 31, q2 = (d >> 27) & 31;
+            const double cp = cs[rr][bp], sp = sn[rr][bp], cq = cs[rr][bq], sq = sn[rr][bq];
+            const double app = xform_entry(Mc[p1 + p1 * LD], Mc[p1 + q1 * LD], Mc[q1 + p1 * LD],
+                                           Mc[q1 + q1 * LD], cp, sp, cp, sp, rp, rp);
+            const double aqq = xform_entry(Mc[p2 + p2 * LD], Mc[p2 + q2 * LD], Mc[q2 + p2 * LD],
+                                           Mc[q2 + q2 * LD], cq, sq, cq, sq, rq, rq);
+            const double x = xform_entry(Mc[p1 + p2 * LD], Mc[p1 + q2 * LD], Mc[q1 + p2 * LD],
+                                         Mc[q1 + q2 * LD], cp, sp, cq, sq, rp, rq);
+            double c = 1.0, s = 0.0;
+            if (fabs(x) > skip_tau) rotation(app, aqq, x, c, s);
+            cs[nr][lane] = c;
+            sn[nr][lane] = s;
+        }
+        named_bar(bar, QH);
+        double* t = Mc;
+        Mc = Mn;
+        Mn = t;
+    }
+    if (ltid >= MT && ltid < MT + QT) {
+        const int l = (ltid - MT) & 31;
+#pragma unroll
+        for (int i = 0; i < QR; ++i) Qs[(qrow0 + i) + l * LD] = qreg[i];
+    }
+    named_bar(bar, QH);
+    // Newton-Schulz: Ts <- Q (3I - Q^T Q) / 2 (see solve_pair)
+    smem_mma_t<TB, true>(Qs, Qs, Mn, ltid, QH);
+    named_bar(bar, QH);
+    for (int e = ltid; e < TB * TB; e += QH) {
+        const int i = e % TB, j = e / TB;
+        Mn[i + j * LD] = (i == j ? 1.5 : 0.0) - 0.5 * Mn[i + j * LD];
+    }
+    named_bar(bar, QH);
+    smem_mma_t<TB, false>(Qs, Mn, Ts, ltid, QH);
+    named_bar(bar, QH);
+}
+
+// One warp computes a 16 x 32 tile C = A B with K = 32 (m8n8k4 DMMA, 8 k-steps);
+// a_at(m, k), b_at(k, n) read the operands, store(m, n, v) writes the result.
+template <class FA, class FB, class FC>
+__device__ __forceinline__ void warp_tile_16x32(FA a_at, FB b_at, FC store) {
+    const int lane = threadIdx.x & 31, r = lane >> 2, kq = lane & 3;
+    double acc[2][4][2];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int t = 0; t < 4; ++t) acc[mt][t][0] = acc[mt][t][1] = 0.0;
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+        double af[2], bf[4];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) af[mt] = a_at(8 * mt + r, 4 * s + kq);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) bf[t] = b_at(4 * s + kq, 8 * t + r);
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int t = 0; t < 4; ++t) dmma(acc[mt][t][0], acc[mt][t][1], af[mt], bf[t]);
+    }
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+#pragma unroll
+            for (int i = 0; i < 2; ++i) store(8 * mt + r, 8 * t + 2 * kq + i, acc[mt][t][i]);
+}
+
+// One CTA per super-pair of round `round`: composes the round's sub-stages into
+// the 64 x 64 rotation Qbuf[pair] (column-major, ld 64); active[pair] = 0 when
+// no sub-stage found an entry above skip_tau (Q = I, updates skipped).
+__global__ void __launch_bounds__(Q_THREADS, 1)
+    jacobi_quad_solve(const double* A, int64_t lda, const SolveTables<32>* tabs, double* Qbuf,
+                      int* active, int ns, int round, double skip_tau, int stage0) {
+    extern __shared__ double sm[];
+    double* M64 = sm;             // the subproblem, transformed by each sub-stage
+    double* Qa = M64 + 64 * L64;  // accumulated 64 x 64 rotation
+    double* P = Qa + 64 * L64;    // this sub-stage's two 32 x 32 rotations Q_0, Q_1 (ld L32)
+    double* H = P + 64 * L64;     // the halves' solve buffers; Y / Qn temporaries after the solves
+    const int tid = threadIdx.x, h = tid >= QH ? 1 : 0, ltid = tid - h * QH;
+    double* Mc = H + h * 4 * SUB32;
+    double* Mn = Mc + SUB32;
+    double* Qs = Mn + SUB32;
+    double* csb = H + 8 * SUB32 + h * 2 * 31 * 16;
+    auto cs = reinterpret_cast<double(*)[16]>(csb);
+    auto sn = reinterpret_cast<double(*)[16]>(csb + 31 * 16);
+    auto* st = reinterpret_cast<SolveTables<32>*>(H + 8 * SUB32 + 4 * 31 * 16);
+    int a, b;
+    circle_pair(ns, round, blockIdx.x, a, b);
+    auto g = [&](int i) -> int64_t {
+        return i < 32 ? static_cast<int64_t>(a) * 32 + i : static_cast<int64_t>(b) * 32 + (i - 32);
+    };
+    for (int e = tid; e < 64 * 64; e += Q_THREADS) {
+        const int i = e & 63, j = e >> 6;
+        M64[i + j * L64] = __ldcg(&A[g(i) + g(j) * lda]);
+        Qa[i + j * L64] = i == j ? 1.0 : 0.0;
+    }
+    bool any = false;
+    const int nsub = stage0 ? 3 : 2;
+    for (int s = 0; s < nsub; ++s) {
+        const int kind = stage0 ? s : s + 1;
+        const int mode = kind == 0 ? 0 : 2;
+        const int R = mode == 0 ? 31 : 16;
+        {
+            const uint4* src = reinterpret_cast<const uint4*>(tabs + mode);
+            uint4* dst = reinterpret_cast<uint4*>(st);
+            for (int e = tid; e < static_cast<int>(sizeof(SolveTables<32>) / 16); e += Q_THREADS) dst[e] = src[e];
+        }
+        __syncthreads();  // M64 and the tables ready
+        bool big = false;
+        for (int e = ltid; e < 32 * 32; e += QH) {
+            const int i = e & 31, j = e >> 5;
+            const double v = M64[quad_idx(kind, h, i) + quad_idx(kind, h, j) * L64];
+            Mc[i + j * L32] = v;
+            big |= i != j && fabs(v) > skip_tau;
+        }
+        const int w0 = __syncthreads_or(big && h == 0);
+        const int w1 = __syncthreads_or(big && h == 1);
+        if (!(w0 | w1)) continue;  // uniform: nothing to rotate in this sub-stage
+        any = true;
+        // each half's rotation Q_h (32 x 32, ld L32) lands in the P region
+        quad_sub_solve(Mc, Mn, Qs, P + h * SUB32, *st, cs, sn, R, ltid, 1 + h, h ? w1 != 0 : w0 != 0,
+                       skip_tau);
+        __syncthreads();
+        // M <- P^T M P and Qa <- Qa P with P = Q_0 (+) Q_1 on the two index
+        // sets, as 16 x 32 warp tiles: T1 forms Y_{h1 h2} = M[h1, h2] Q_h2 for
+        // the three blocks h1 <= h2 and Qa[:, h] Q_h; T2 forms Q_h1^T Y_{h1 h2},
+        // written with its mirror (M stays exactly symmetric).
+        const double* Qh = P;
+        double* Y = H;                 // Y_00, Y_01, Y_11 (ld L32)
+        double* Qn = H + 4 * SUB32;    // Qa[:, h] Q_h: two 64 x 32 (ld L64)
+        const int wi = tid >> 5;
+        if (wi < 6) {
+            const int blk = wi >> 1, r0 = 16 * (wi & 1);
+            const int h1 = blk == 2 ? 1 : 0, h2 = blk == 0 ? 0 : 1;
+            warp_tile_16x32(
+                [&](int m, int k) { return M64[quad_idx(kind, h1, r0 + m) + quad_idx(kind, h2, k) * L64]; },
+                [&](int k, int n) { return Qh[h2 * SUB32 + k + n * L32]; },
+                [&](int m, int n, double v) { Y[blk * SUB32 + (r0 + m) + n * L32] = v; });
+        } else if (wi < 14) {
+            const int hq = (wi - 6) >> 2, r0 = 16 * ((wi - 6) & 3);
+            warp_tile_16x32([&](int m, int k) { return Qa[(r0 + m) + quad_idx(kind, hq, k) * L64]; },
+                            [&](int k, int n) { return Qh[hq * SUB32 + k + n * L32]; },
+                            [&](int m, int n, double v) { Qn[hq * 32 * L64 + (r0 + m) + n * L64] = v; });
+        }
+        __syncthreads();
+        if (wi < 6) {
+            const int blk = wi >> 1, r0 = 16 * (wi & 1);
+            const int h1 = blk == 2 ? 1 : 0, h2 = blk == 0 ? 0 : 1;
+            warp_tile_16x32([&](int m, int k) { return Qh[h1 * SUB32 + k + (r0 + m) * L32]; },
+                            [&](int k, int n) { return Y[blk * SUB32 + k + n * L32]; },
+                            [&](int m, int n, double v) {
+                                if (h1 == h2 && r0 + m > n) return;
+                                const int i = quad_idx(kind, h1, r0 + m), j = quad_idx(kind, h2, n);
+                                M64[i + j * L64] = v;
+                                M64[j + i * L64] = v;
+                            });
+        } else {
+            for (int e = tid - 6 * 32; e < 64 * 64; e += Q_THREADS - 6 * 32) {
+                const int row = e & 63, col = (e >> 6) & 31, hq = e >> 11;
+                Qa[row + quad_idx(kind, hq, col) * L64] = Qn[hq * 32 * L64 + row + col * L64];
+            }
+        }
+    }
+    __syncthreads();
+    if (any) {
+        double* out = Qbuf + static_cast<size_t>(blockIdx.x) * 4096;
+        for (int e = tid; e < 64 * 64; e += Q_THREADS) out[e] = Qa[(e & 63) + (e >> 6) * L64];
+    }
+    if (tid == 0) active[blockIdx.x] = any ? 1 : 0;
+}
+
+// A[ST_p, ST_q] <- Q_p^T A[ST_p, ST_q] Q_q for one super-pair block (p <= q)
+// per CTA of 4 warps; X and Q_q are staged in shared memory, warp w computes
+// rows [16 w, 16 w + 16) of U = Q_p^T X (its Q_p fragments in registers) and
+// then of X' = U Q_q (U re-laid by quad shuffles). X' goes back through shared
+// memory with an odd leading dimension (L_OUT = 65), so that both the column
+// runs of X' and those of its mirror are read without bank conflicts and
+// written to HBM as full 256-byte runs. (Measured alternatives, n = 4096: 8
+// warps x 8 rows 114 us, persistent CTAs with a cp.async double buffer and
+// Q_q through L1 112 us, this one 105 us.)
+constexpr size_t A64_SMEM = 2 * 64 * L64 * sizeof(double);
+constexpr int A64_THREADS = 128;
+constexpr int L_OUT = 65;
+
+__global__ void __launch_bounds__(A64_THREADS)
+    jacobi_update_a64(double* A, int64_t lda, const double* Qbuf, const int* active, int ns, int round) {
+    extern __shared__ double sm[];
+    double* Xs = sm;
+    double* Qs = sm + 64 * L64;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, r = lane >> 2, kq = lane & 3;
+    const int u = blockIdx.x;
+    int q = static_cast<int>((sqrt(8.0 * u + 1.0) - 1.0) * 0.5);
+    while ((q + 1) * (q + 2) / 2 <= u) ++q;
+    while (q * (q + 1) / 2 > u) --q;
+    const int p = u - q * (q + 1) / 2;
+    const bool ap = __ldcg(&active[p]) != 0, aq = __ldcg(&active[q]) != 0;
+    if (!(ap | aq)) return;
+    int pa, pb, qa, qb;
+    circle_pair(ns, round, p, pa, pb);
+    circle_pair(ns, round, q, qa, qb);
+    auto gp = [&](int i) -> int64_t {
+        return i < 32 ? static_cast<int64_t>(pa) * 32 + i : static_cast<int64_t>(pb) * 32 + (i - 32);
+    };
+    auto gq = [&](int i) -> int64_t {
+        return i < 32 ? static_cast<int64_t>(qa) * 32 + i : static_cast<int64_t>(qb) * 32 + (i - 32);
+    };
+    const double* Qp = Qbuf + static_cast<size_t>(p) * 4096;
+    const double* Qq = Qbuf + static_cast<size_t>(q) * 4096;
+#pragma unroll 8
+    for (int it = 0; it < 2048 / A64_THREADS; ++it) {
+        const int e = tid + it * A64_THREADS;
+        const int i = (e & 31) * 2, j = e >> 5;
+        const double2 x = __ldcg(reinterpret_cast<const double2*>(&A[gp(i) + gq(j) * lda]));
+        const double2 y = aq ? __ldcg(reinterpret_cast<const double2*>(&Qq[i + j * 64]))
+                             : make_double2(i == j ? 1.0 : 0.0, i + 1 == j ? 1.0 : 0.0);
+        *reinterpret_cast<double2*>(&Xs[i + j * L64]) = x;
+        *reinterpret_cast<double2*>(&Qs[i + j * L64]) = y;
+    }
+    // A-fragments of Q_p^T: (Q_p^T)[m][k] = Q_p[k][m], m = 16 w + 8 mt + r, k = 4 s + kq
+    double qpf[16][2];
+#pragma unroll
+    for (int s = 0; s < 16; ++s)
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+            const int k = 4 * s + kq, m = 16 * w + 8 * mt + r;
+            qpf[s][mt] = ap ? __ldcg(&Qp[k + m * 64]) : (k == m ? 1.0 : 0.0);
+        }
+    __syncthreads();
+    double U[2][8][2];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int t = 0; t < 8; ++t) U[mt][t][0] = U[mt][t][1] = 0.0;
+#pragma unroll
+    for (int s = 0; s < 16; ++s) {
+        double bx[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) bx[t] = Xs[(4 * s + kq) + (8 * t + r) * L64];
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt) dmma(U[mt][t][0], U[mt][t][1], qpf[s][mt], bx[t]);
+    }
+    double O[2][8][2];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int t = 0; t < 8; ++t) O[mt][t][0] = O[mt][t][1] = 0.0;
+#pragma unroll
+    for (int s = 0; s < 16; ++s) {
+        // U[8 mt + r][4 s + kq] lives in lane (r, 2 (s & 1) + kq / 2), register U[mt][s / 2][kq & 1]
+        const int src = (lane & ~3) | (2 * (s & 1) + (kq >> 1));
+        double bq[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) bq[t] = Qs[(4 * s + kq) + (8 * t + r) * L64];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+            const double v0 = __shfl_sync(0xffffffffu, U[mt][s >> 1][0], src);
+            const double v1 = __shfl_sync(0xffffffffu, U[mt][s >> 1][1], src);
+            const double av = (kq & 1) ? v1 : v0;
+#pragma unroll
+            for (int t = 0; t < 8; ++t) dmma(O[mt][t][0], O[mt][t][1], av, bq[t]);
+        }
+    }
+    __syncthreads();  // every warp is done reading Xs
+    double* Xo = Xs;  // X' with leading dimension L_OUT
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+#pragma unroll
+            for (int i = 0; i < 2; ++i) Xo[(16 * w + 8 * mt + r) + (8 * t + 2 * kq + i) * L_OUT] = O[mt][t][i];
+    __syncthreads();
+    if (p == q) {  // diagonal super-pair block: upper triangle mirrored (exact symmetry)
+#pragma unroll 4
+        for (int e = tid; e < 4096; e += A64_THREADS) {
+            const int i = e & 63, j = e >> 6;
+            A[gp(i) + gp(j) * lda] = i <= j ? Xo[i + j * L_OUT] : Xo[j + i * L_OUT];
+        }
+        return;
+    }
+#pragma unroll 4
+    for (int e = tid; e < 4096; e += A64_THREADS) {  // X': lanes walk a column of X'
+        const int i = e & 63, j = e >> 6;
+        A[gp(i) + gq(j) * lda] = Xo[i + j * L_OUT];
+    }
+#pragma unroll 4
+    for (int e = tid; e < 4096; e += A64_THREADS) {  // mirror: lanes walk a row of X'
+        const int jj = e & 63, ii = e >> 6;
+        A[gq(jj) + gp(ii) * lda] = Xo[ii + jj * L_OUT];
+    }
+}
+
+// V[rows, ST_q] <- V[rows, ST_q] Q_q: one CTA of 4 warps per (super-pair q,
+// V64_ROWS-row chunk), Q_q staged in shared memory; a warp walks 16-row tiles
+// with the rows permuted so that m8n8k4 row r of m-tile m is tile row 2 r + m
+// (each lane owns 2 consecutive rows: every V access is a 16-byte LDG/STG and
+// 8 lanes cover a full 128-byte column run). Four CTAs per SM keep loads of
+// one warp in flight under the DMMAs of the others.
+constexpr int V64_ROWS = 256;
+
+__device__ __forceinline__ double2 ld_cg2(const double* p) {
+    return __ldcg(reinterpret_cast<const double2*>(p));
+}
+
+__global__ void __launch_bounds__(128, 4)
+    jacobi_update_v64(double* V, int64_t ldv, int64_t n_rows, const double* Qbuf, const int* active,
+                      int ns, int round) {
+    __shared__ double Qs[64 * L64];
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, r = lane >> 2, kq = lane & 3;
+    const int ks = ns / 2;
+    const int q = static_cast<int>(blockIdx.x % ks);
+    const int64_t row_begin = static_cast<int64_t>(blockIdx.x / ks) * V64_ROWS;
+    if (row_begin >= n_rows || !__ldcg(&active[q])) return;
+    int qa, qb;
+    circle_pair(ns, round, q, qa, qb);
+    auto gq = [&](int i) -> int64_t {
+        return i < 32 ? static_cast<int64_t>(qa) * 32 + i : static_cast<int64_t>(qb) * 32 + (i - 32);
+    };
+    const double* Qq = Qbuf + static_cast<size_t>(q) * 4096;
+#pragma unroll
+    for (int it = 0; it < 16; ++it) {
+        const int e = tid + it * 128;
+        const int i = (e & 31) * 2, j = e >> 5;
+        const double2 y = __ldcg(reinterpret_cast<const double2*>(&Qq[i + j * 64]));
+        Qs[i + j * L64] = y.x;
+        Qs[i + 1 + j * L64] = y.y;
+    }
+    const int64_t row_end = min(n_rows, row_begin + V64_ROWS);
+    // column bases: k-step s reads column gq(4 s + kq), t-tile stores gq(8 t + 2 kq + i)
+    const int64_t step = 4 * ldv;
+    const double* ca = V + 2 * r + (static_cast<int64_t>(qa) * 32 + kq) * ldv;
+    const double* cb = V + 2 * r + (static_cast<int64_t>(qb) * 32 + kq) * ldv;
+    double* sa = V + 2 * r + (static_cast<int64_t>(qa) * 32 + 2 * kq) * ldv;
+    double* sb = V + 2 * r + (static_cast<int64_t>(qb) * 32 + 2 * kq) * ldv;
+    __syncthreads();
+    for (int64_t row0 = row_begin + 16 * w; row0 < row_end; row0 += 64) {
+        double2 va[16];
+#pragma unroll
+        for (int s = 0; s < 16; ++s) va[s] = ld_cg2((s < 8 ? ca : cb) + row0 + (s & 7) * step);
+        double acc[2][8][2];
+#pragma unroll
+        for (int m = 0; m < 2; ++m)
+#pragma unroll
+            for (int t = 0; t < 8; ++t) acc[m][t][0] = acc[m][t][1] = 0.0;
+#pragma unroll
+        for (int s = 0; s < 16; ++s) {
+            double bq[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) bq[t] = Qs[(4 * s + kq) + (8 * t + r) * L64];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                dmma(acc[0][t][0], acc[0][t][1], va[s].x, bq[t]);
+                dmma(acc[1][t][0], acc[1][t][1], va[s].y, bq[t]);
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+                *reinterpret_cast<double2*>((t < 4 ? sa : sb) + row0 + (t & 3) * 2 * step + i * ldv) =
+                    make_double2(acc[0][t][i], acc[1][t][i]);
+    }
+}
+
+void run_sweeps_quad(Ctx* c, double* A, double* V, int64_t n_pad, int max_sweeps, double thr, double fro,
+                     DBuf& scratch, int& sweeps, double& off) {
+    const int ns = static_cast<int>(n_pad / 32), ks = ns / 2, rounds = ns - 1;
+    static bool attr = false;
+    if (!attr) {
+        SVDK_CUDA(cudaFuncSetAttribute(jacobi_quad_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(QUAD_SMEM)));
+        SVDK_CUDA(cudaFuncSetAttribute(jacobi_update_a64, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(A64_SMEM)));
+        attr = true;
+    }
+    const double skip_tau = 1e-13 * fro / static_cast<double>(n_pad);  // as run_sweeps
+    DBuf qbuf(c, static_cast<size_t>(rounds) * ks * 4096);
+    DBuf act(c, static_cast<size_t>(rounds) * ks);
+    int* active = reinterpret_cast<int*>(act.p());
+    if (!c->aux_stream) {
+        SVDK_CUDA(cudaStreamCreateWithFlags(&c->aux_stream, cudaStreamNonBlocking));
+        SVDK_CUDA(cudaEventCreateWithFlags(&c->aux_ev[0], cudaEventDisableTiming));
+        SVDK_CUDA(cudaEventCreateWithFlags(&c->aux_ev[1], cudaEventDisableTiming));
+    }
+    cudaStream_t S = c->stream, S2 = c->aux_stream;
+    DBuf tab_buf(c, 3 * sizeof(SolveTables<32>) / sizeof(double));
+    const auto* tabs = reinterpret_cast<const SolveTables<32>*>(tab_buf.p());
+    jacobi_tables_kernel<32><<<3, 256, 0, S>>>(reinterpret_cast<SolveTables<32>*>(tab_buf.p()));
+    SVDK_CHECK_LAUNCH();
+    c->launches++;
+    const int a_ctas = ks * (ks + 1) / 2;
+    const int v_ctas = static_cast<int>(ceil_div(n_pad, static_cast<int64_t>(V64_ROWS))) * ks;
+    auto enqueue_sweep = [&] {
+        for (int r = 0; r < rounds; ++r) {
+            double* qr = qbuf.p() + static_cast<size_t>(r) * ks * 4096;
+            int* ar = active + static_cast<size_t>(r) * ks;
+            jacobi_quad_solve<<<ks, Q_THREADS, QUAD_SMEM, S>>>(A, n_pad, tabs, qr, ar, ns, r, skip_tau,
+                                                              r == 0 ? 1 : 0);
+            SVDK_CUDA(cudaEventRecord(c->aux_ev[0], S));
+            SVDK_CUDA(cudaStreamWaitEvent(S2, c->aux_ev[0], 0));
+            jacobi_update_v64<<<v_ctas, 128, 0, S2>>>(V, n_pad, n_pad, qr, ar, ns, r);
+            jacobi_update_a64<<<a_ctas, A64_THREADS, A64_SMEM, S>>>(A, n_pad, qr, ar, ns, r);
+        }
+        SVDK_CUDA(cudaEventRecord(c->aux_ev[1], S2));
+        SVDK_CUDA(cudaStreamWaitEvent(S, c->aux_ev[1], 0));
+    };
+    cudaGraphExec_t exec = nullptr;
+    const bool use_graph = S != nullptr;
+    if (use_graph) {
+        cudaGraph_t graph;
+        SVDK_CUDA(cudaStreamBeginCapture(S, cudaStreamCaptureModeThreadLocal));
+        enqueue_sweep();
+        SVDK_CUDA(cudaStreamEndCapture(S, &graph));
+        SVDK_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+        cudaGraphDestroy(graph);
+    }
+    sweeps = 0;
+    try {
+        while (off > thr && sweeps < max_sweeps) {
+            if (use_graph) {
+                SVDK_CUDA(cudaGraphLaunch(exec, S));
+            } else {
+                enqueue_sweep();
+                SVDK_CHECK_LAUNCH();
+            }
+            c->launches += 3 * rounds;
+            ++sweeps;
+            off = std::sqrt(2.0 * device_sumsq(c, A, n_pad, 1, scratch));
+        }
+    } catch (...) {
+        if (exec) cudaGraphExecDestroy(exec);
+        throw;
+    }
+    if (exec) cudaGraphExecDestroy(exec);
+}
+
 }  // namespace
+
+// Smallest n that uses the quad scheme by default. Measured on B200
+// (tools/jacobi_eval.sh, Gram spectra): n = 1024 / 2048 / 4096 take 17.2 / 61.1
+// / 396 ms with 2b = 32 and 20.5 / 68.7 / 338 ms with the quad scheme — below
+// n ~ 3000 the solve chain (not the update traffic) bounds a sweep.
+constexpr int64_t kQuadMinN = 3072;
 
 void eig_sym(Ctx* c, const double* S, int64_t lds, int64_t n, int max_sweeps, double* w,
              double* Vout, int64_t ldv) {
@@ -1016,10 +1569,12 @@ void eig_sym(Ctx* c, const double* S, int64_t lds, int64_t n, int max_sweeps, do
     // Block size: measured on B200 (tools/eig_sweep.sh): 2b = 32 with ONE
     // inner sweep per round is fastest for n in [256, 2048]; the outer sweep
     // count (9-12) does not depend on how far each subproblem is pushed.
-    int TB = n <= 64 ? 16 : 32;
+    // TB = 64: the quad scheme (64-wide updates, section 3 above) for large n,
+    // where the per-round A/V updates dominate.
+    int TB = n <= 64 ? 16 : (n >= kQuadMinN ? 64 : 32);
     if (const char* e = std::getenv("SVDK_JACOBI_TB")) {  // tuning override
         const int t = std::atoi(e);
-        if (t == 16 || t == 32) TB = t;
+        if (t == 16 || t == 32 || t == 64) TB = t;
     }
     const int64_t n_pad = round_up(n, TB);
     DBuf A(c, static_cast<size_t>(n_pad) * n_pad), V(c, static_cast<size_t>(n_pad) * n_pad);
@@ -1040,6 +1595,8 @@ void eig_sym(Ctx* c, const double* S, int64_t lds, int64_t n, int max_sweeps, do
     if (n == 1) off = 0.0;
     if (TB == 16)
         run_sweeps<16>(c, A.p(), V.p(), n_pad, max_sweeps, thr, fro, scratch, sweeps, off);
+    else if (TB == 64)
+        run_sweeps_quad(c, A.p(), V.p(), n_pad, max_sweeps, thr, fro, scratch, sweeps, off);
     else
         run_sweeps<32>(c, A.p(), V.p(), n_pad, max_sweeps, thr, fro, scratch, sweeps, off);
     c->jacobi_sweeps = sweeps;

@@ -97,6 +97,31 @@ def test_eig_matches_reference_gram(sk, ref):
     assert single < 1e-10 and cluster < 1e-10
 
 
+@pytest.mark.parametrize("tb", [32, 64])
+@pytest.mark.parametrize("n", [5, 64, 100, 256, 700])
+def test_eig_block_schemes(sk, ref, monkeypatch, tb, n):
+    """Both block schemes (2b = 32 per-round updates, and the quad scheme's 64-wide
+    updates composing two 16-block rounds) against LAPACK and the compiled
+    reference eig_sym on a Gram spectrum, with the same sweep-count behaviour."""
+    monkeypatch.setenv("SVDK_JACOBI_TB", str(tb))
+    rng = np.random.default_rng(100 + n)
+    x = rng.standard_normal((2 * n + 3, n))
+    s = np.asfortranarray(x.T @ x)
+    e = sk.eig_sym(s)
+    w, v = e.eigenvalues, e.eigenvectors
+    fro = np.linalg.norm(s)
+    assert np.all(np.diff(w) <= 0)
+    assert np.max(np.abs(w - np.linalg.eigvalsh(s)[::-1])) <= 1e-13 * fro
+    assert np.linalg.norm(s @ v - v * w) <= 1e-10 * fro
+    assert np.max(np.abs(v.T @ v - np.eye(n))) <= 1e-12
+    if n <= 256:
+        w_ref, v_ref = ref.eig_sym(s)
+        assert np.max(np.abs(w - w_ref) / w_ref) < 1e-11
+        from tests.parity import per_vector_sines
+        single, cluster = per_vector_sines(v, w_ref, v_ref)
+        assert single < 1e-9 and cluster < 1e-9
+
+
 def test_eig_errors(sk):
     with pytest.raises(errors.DimensionError):
         sk.eig_sym(np.ones((2, 3)))
