@@ -515,11 +515,28 @@ __global__ void __launch_bounds__(256) reduce_alpha_kernel(const double* partial
     for (unsigned b = 0; b < gridDim.x; ++b) a += __ldcg(dots + b);
     const double bp = beta_prev ? *beta_prev : 0.0;
     double ss = 0.0;
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-        double x = __ldcg(w + i) - a * q[i];
-        if (qprev) x -= bp * qprev[i];
-        w[i] = x;
-        ss = fma(x, x, ss);
+    // one CTA walks all of w: 8 entries per thread in flight at a time (the
+    // plain loop was a chain of dependent L2 round trips, ~16 us at n = 4096)
+    constexpr int U = 8;
+    for (int64_t i0 = threadIdx.x; i0 < n; i0 += U * static_cast<int64_t>(blockDim.x)) {
+        double xw[U], xq[U], xp[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t i = i0 + u * static_cast<int64_t>(blockDim.x);
+            xw[u] = i < n ? __ldcg(w + i) : 0.0;
+            xq[u] = i < n ? q[i] : 0.0;
+            xp[u] = (qprev && i < n) ? qprev[i] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t i = i0 + u * static_cast<int64_t>(blockDim.x);
+            if (i < n) {
+                double x = xw[u] - a * xq[u];
+                if (qprev) x -= bp * xp[u];
+                w[i] = x;
+                ss = fma(x, x, ss);
+            }
+        }
     }
     ss = block_sum(ss, red);
     if (threadIdx.x == 0) {
@@ -652,13 +669,18 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
 // nrm = {||w|| before, after} the second CGS pass, state = {gnorm, prev_beta,
 // restart flag}. gnorm is the running Gershgorin bound on ||T||. Breakdown
 // (an invariant subspace: the second reorthogonalisation pass removed more
-// than half of w, or ||w|| <= 1e-14 ||T||) sets b_j = 0 and a restart flag
-// with w = a fresh Gaussian vector (counter hash of (seed, j), identical on
-// every rank); otherwise b_j = ||w|| and q_{j+1} = w / b_j.
-__global__ void lanczos_finish_kernel(double* w, int64_t n, const double* nrm, const double* alpha_j,
-                                      double* beta_j, double* state, double* qn, int last, uint64_t seed,
-                                      int64_t j) {
+// than half of w, or ||w|| <= 1e-14 ||T||) sets b_j = 0 and restarts with a
+// fresh Gaussian vector (counter hash of (seed, j), identical on every rank),
+// orthogonalised twice against Q_cols (CGS2) and normalised into q_{j+1} —
+// by this same CTA: breakdowns are rare and Q_cols is read 4 times, so no
+// grid-wide synchronisation is needed. Otherwise b_j = ||w|| and
+// q_{j+1} = w / b_j.
+__global__ void __launch_bounds__(1024) lanczos_finish_kernel(double* w, int64_t n, const double* nrm,
+                                                              const double* alpha_j, double* beta_j,
+                                                              double* state, double* qn, int last, uint64_t seed,
+                                                              int64_t j, const double* Q, int64_t cols, double* h) {
     __shared__ int brk;
+    __shared__ double red[32];
     const double n1 = nrm[0], n2 = nrm[1];
     const double gnorm = fmax(state[0], fabs(*alpha_j) + state[1] + n2);
     if (threadIdx.x == 0) brk = !last && (!(n2 > 0.5 * n1) || !(n2 > 1e-14 * gnorm));
@@ -667,32 +689,35 @@ __global__ void lanczos_finish_kernel(double* w, int64_t n, const double* nrm, c
         state[0] = gnorm;
         *beta_j = brk ? 0.0 : n2;
         state[1] = brk ? 0.0 : n2;
-        state[2] = brk ? 1.0 : 0.0;
     }
     if (last) return;
     if (!brk) {
         const double inv = 1.0 / n2;
-        for (int64_t i = threadIdx.x; i < n; i += blockDim.x) qn[i] = w[i] * inv;
-    } else {
-        const uint64_t key = splitmix64(seed ^ (0x9e3779b97f4a7c15ull * static_cast<uint64_t>(j + 1)));
-        for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-            const uint64_t h1 = splitmix64(key + 2 * static_cast<uint64_t>(i));
-            const uint64_t h2 = splitmix64(key + 2 * static_cast<uint64_t>(i) + 1);
-            const double u1 = static_cast<double>((h1 >> 11) + 1) * 0x1.0p-53;
-            const double u2 = static_cast<double>(h2 >> 11) * 0x1.0p-53;
-            w[i] = sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
+        constexpr int U = 4;
+        for (int64_t i0 = threadIdx.x; i0 < n; i0 += U * static_cast<int64_t>(blockDim.x)) {
+            double x[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int64_t i = i0 + u * static_cast<int64_t>(blockDim.x);
+                x[u] = i < n ? __ldcg(w + i) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int64_t i = i0 + u * static_cast<int64_t>(blockDim.x);
+                if (i < n) qn[i] = x[u] * inv;
+            }
         }
+        return;
     }
-}
-
-// Restart after breakdown (runs only when state[2] is set; a no-op launch
-// otherwise): orthogonalise the random w twice against Q_cols (CGS2) and
-// normalise it into q_{j+1}. One CTA: breakdowns are rare and Q_cols is read
-// 4 times, so no grid-wide synchronisation is needed.
-__global__ void lanczos_restart_kernel(const double* Q, int64_t n, int64_t cols, double* w, double* h,
-                                       double* state, double* qn) {
-    if (state[2] == 0.0) return;
-    __shared__ double red[32];
+    const uint64_t key = splitmix64(seed ^ (0x9e3779b97f4a7c15ull * static_cast<uint64_t>(j + 1)));
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const uint64_t h1 = splitmix64(key + 2 * static_cast<uint64_t>(i));
+        const uint64_t h2 = splitmix64(key + 2 * static_cast<uint64_t>(i) + 1);
+        const double u1 = static_cast<double>((h1 >> 11) + 1) * 0x1.0p-53;
+        const double u2 = static_cast<double>(h2 >> 11) * 0x1.0p-53;
+        w[i] = sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
+    }
+    __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     for (int pass = 0; pass < 2; ++pass) {
         for (int64_t k = warp; k < cols; k += nw) {
@@ -713,8 +738,6 @@ __global__ void lanczos_restart_kernel(const double* Q, int64_t n, int64_t cols,
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s = fma(w[i], w[i], s);
     const double inv = 1.0 / sqrt(block_sum(s, red));
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x) qn[i] = w[i] * inv;
-    __syncthreads();
-    if (threadIdx.x == 0) state[2] = 0.0;
 }
 
 // Dense tridiagonal T (k x k) from alpha, beta.
@@ -848,7 +871,7 @@ int64_t lanczos_svd(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n, 
     double* alpha = scal.p();
     double* beta = scal.p() + steps;
     double* nrm = scal.p() + 2 * steps;    // [0] after CGS pass 1, [1] after pass 2
-    double* state = scal.p() + 2 * steps + 2;  // gnorm, prev_beta, restart flag, ||w0||, skip pass 2
+    double* state = scal.p() + 2 * steps + 2;  // gnorm, prev_beta, (unused), ||w0||, skip pass 2
     fill(c, state, 5, 0.0);
     // step-tail workspaces: per-CTA partials and last-CTA counters (zeroed once;
     // every kernel resets the counters it used)
@@ -863,7 +886,7 @@ int64_t lanczos_svd(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n, 
     SVDK_CHECK_LAUNCH();
     c->launches += 2;
     // Every step is enqueued without a host round trip: the breakdown decision
-    // and the restart run on the device (lanczos_finish/restart_kernel).
+    // and the restart run on the device (lanczos_finish_kernel).
     for (int64_t j = 0; j < steps; ++j) {
         const double* qj = Q.p() + j * n;
         // w = A^T A q_j (GEMV partials reduced in reduce_alpha unless an
@@ -891,14 +914,9 @@ int64_t lanczos_svd(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n, 
         const bool last = j + 1 == steps;
         double* qn = last ? nullptr : Q.p() + (j + 1) * n;
         lanczos_finish_kernel<<<1, 1024, 0, c->stream>>>(w.p(), n, nrm, alpha + j, beta + j, state, qn,
-                                                         last ? 1 : 0, seed, j);
+                                                         last ? 1 : 0, seed, j, Q.p(), cols, h.p());
         SVDK_CHECK_LAUNCH();
         c->launches += 6;
-        if (!last) {
-            lanczos_restart_kernel<<<1, 1024, 0, c->stream>>>(Q.p(), n, cols, w.p(), h.p(), state, qn);
-            SVDK_CHECK_LAUNCH();
-            c->launches++;
-        }
     }
     // Ritz pairs: eig(T), V = Q_L S
     DBuf T(c, static_cast<size_t>(steps) * steps), theta(c, steps), S(c, static_cast<size_t>(steps) * steps);
