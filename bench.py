@@ -431,16 +431,19 @@ def ours(args, cfg):
         eflops = ej["count"] * sweeps * 8.0 * n_eig ** 3
         achieved = eflops / (ej["ms"] / 1e3) / 1e12 if ej["ms"] > 0 else 0.0
         roofline = {"bound": "tensor",
-                    "kernel": "Jacobi sweep (jacobi_pair_solve + jacobi_update_a_reg/_v_reg DMMA, one CUDA graph "
-                              "per sweep)",
+                    "kernel": ("Jacobi sweep (quad scheme: jacobi_quad_solve + jacobi_update_a64/_v64 DMMA, one "
+                               "CUDA graph per sweep)" if n_eig >= 3072 else
+                               "Jacobi sweep (jacobi_pair_solve + jacobi_update_a_reg/_v_reg DMMA, one CUDA graph "
+                               "per sweep)"),
                     "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                     "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None, "launches": ej["count"],
                     "share_of_step": ej["ms"] / ms if ms else None,
                     "algorithmic_flops_per_launch": eflops / max(ej["count"], 1),
                     "peak_source": "measured cuBLAS DGEMM 8192^3 sustained on B200 (profiles/fp64_peaks.json)",
                     "note": f"{sweeps} sweeps x 8 n^3 (n = {n_eig}); at small n the sweep is latency-bound "
-                            "(~n dependent inner rotation rounds per sweep), at n = 4096 the per-round A/V "
-                            "block updates run at ~half of the DMMA and HBM rooflines"}
+                            "(~n dependent inner rotation rounds per sweep); at n = 4096 the 64-wide A/V updates "
+                            "are DMMA-bound (pipe 64% / 77% active, profiles/r1_jacobi_quad_ncu.txt) behind the "
+                            "latency-bound 64x64 solves"}
     elif gv["ms"] > g["ms"]:
         achieved = gv["bytes"] / (gv["ms"] / 1e3) / 1e9 if gv["ms"] > 0 else 0.0
         peak = HBM_PEAK_GBS
