@@ -671,6 +671,76 @@ __device__ __forceinline__ void upd_a_unit(double* A, int64_t lda, const double*
     }
 }
 
+// The same update split over the four warps of a CTA (one unit per CTA):
+// warp w4 produces rows [8 w4, 8 w4 + 8) of Q_p^T X Q_q. Its rows of
+// U = Q_p^T X stay in its own accumulators, so no data crosses warps; each
+// warp reads all of X and Q_q (L2-resident) and issues 64 instead of 256
+// DMMAs, so a round's update takes the latency of a quarter of the work. The
+// CTA meets at a barrier between the last read of X and the first store
+// (every warp reads all of X and writes a quarter of it). Same accumulation
+// order per output entry as upd_a_unit: bit-identical results. Used for
+// n <= 768, where a round is a short latency chain (solve -> update -> solve).
+__global__ void __launch_bounds__(128)
+    jacobi_update_a_q4(double* A, int64_t lda, const double* Qbuf, const int* active, int nb, int round) {
+    constexpr int B = 16;
+    const int lane = threadIdx.x & 31, r = lane >> 2, kq = lane & 3, w4 = threadIdx.x >> 5;
+    const int u = blockIdx.x;
+    int q = static_cast<int>((sqrt(8.0 * u + 1.0) - 1.0) * 0.5);
+    while ((q + 1) * (q + 2) / 2 <= u) ++q;
+    while (q * (q + 1) / 2 > u) --q;
+    const int p = u - q * (q + 1) / 2;
+    const bool ap = __ldcg(&active[p]) != 0, aq = __ldcg(&active[q]) != 0;
+    if (!(ap | aq)) return;
+    int Ip, Jp, Iq, Jq;
+    circle_pair(nb, round, p, Ip, Jp);
+    circle_pair(nb, round, q, Iq, Jq);
+    const double* Qa = Qbuf + static_cast<size_t>(p) * 1024;
+    const double* Qb = Qbuf + static_cast<size_t>(q) * 1024;
+    double xa[8], xb[8][4], qb[8][4];
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+        const int64_t row = gidx(B, Ip, Jp, 4 * s + kq);
+        xa[s] = q_frag(Qa, ap, 4 * s + kq, 8 * w4 + r);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            xb[s][t] = __ldcg(&A[row + gidx(B, Iq, Jq, 8 * t + r) * lda]);
+            qb[s][t] = q_frag(Qb, aq, 4 * s + kq, 8 * t + r);
+        }
+    }
+    double acc[4][2];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) acc[t][0] = acc[t][1] = 0.0;
+#pragma unroll
+    for (int s = 0; s < 8; ++s)
+#pragma unroll
+        for (int t = 0; t < 4; ++t) dmma(acc[t][0], acc[t][1], xa[s], xb[s][t]);
+    double out[4][2];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) out[t][0] = out[t][1] = 0.0;
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+        const int src = (lane & ~3) | (2 * (s & 1) + (kq >> 1));
+        const double v0 = __shfl_sync(0xffffffffu, acc[s >> 1][0], src);
+        const double v1 = __shfl_sync(0xffffffffu, acc[s >> 1][1], src);
+        const double a = (kq & 1) ? v1 : v0;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) dmma(out[t][0], out[t][1], a, qb[s][t]);
+    }
+    __syncthreads();  // all of X has been read by every warp
+    const int li = 8 * w4 + r;
+    const int64_t gi = gidx(B, Ip, Jp, li);
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const int lj = 8 * t + 2 * kq + i;
+            const int64_t gj = gidx(B, Iq, Jq, lj);
+            if (p == q && li > lj) continue;
+            A[gi + gj * lda] = out[t][i];
+            A[gj + gi * lda] = out[t][i];
+        }
+}
+
 // V[rows, IJ_q] <- V[rows, IJ_q] Q_q; one warp per (pair q, VT_ROWS-row chunk).
 // Rows inside a 32-row tile are permuted so that m8n8k4 row r of m-tile m is
 // tile row 4r + m (each output row depends only on its own input row): lane
@@ -914,12 +984,20 @@ void run_sweeps(Ctx* c, double* A, double* V, int64_t n_pad, int max_sweeps, dou
     const char* upd_env = std::getenv("SVDK_JACOBI_UPD");
     const bool reg_upd = TB == 32 && !(upd_env && std::string(upd_env) == "smem");
     const int a_warp_ctas = static_cast<int>(ceil_div(static_cast<int64_t>(a_ctas), UPD_WARPS));
+    // latency-bound rounds (small n): each A block unit split over four warps.
+    // Measured (tools/eig_time.py): n = 256 / 512 3.71 -> 3.36 / 7.25 -> 6.80 ms;
+    // n = 1024 / 2048 17.2 -> 17.7 / 61.2 -> 74.2 ms (4x the warps, more L2 reads)
+    const char* q4_env = std::getenv("SVDK_JACOBI_AQ4");
+    const bool a_q4 = q4_env ? std::atoi(q4_env) != 0 : n_pad <= 768;
     const int v_warp_ctas =
         static_cast<int>(ceil_div(ceil_div(n_pad, static_cast<int64_t>(VT_ROWS)) * k, UPD_WARPS));
     auto launch_updates = [&](const double* qr, const int* ar, int r) {
         if (reg_upd) {
             jacobi_update_v_reg<<<v_warp_ctas, UPD_WARPS * 32, 0, S2>>>(V, n_pad, n_pad, qr, ar, nb, r);
-            jacobi_update_a_reg<<<a_warp_ctas, UPD_WARPS * 32, 0, S>>>(A, n_pad, qr, ar, nb, r);
+            if (a_q4)
+                jacobi_update_a_q4<<<a_ctas, 128, 0, S>>>(A, n_pad, qr, ar, nb, r);
+            else
+                jacobi_update_a_reg<<<a_warp_ctas, UPD_WARPS * 32, 0, S>>>(A, n_pad, qr, ar, nb, r);
         } else {
             jacobi_update_v<TB><<<v_ctas, 256, smem_v, S2>>>(V, n_pad, qr, ar, nb, r);
             jacobi_update_a<TB><<<a_ctas, 256, smem_a, S>>>(A, n_pad, qr, ar, nb, r);
