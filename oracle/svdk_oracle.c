@@ -235,8 +235,8 @@ int orc_eig_sym(const double* s, size_t n, int max_sweeps, double* w, double* v,
         }
     }
     if (max_asym > 1e-8 * max_abs) return ORC_E_PARAM;
-    double* a = (double*)malloc((n * n ? n * n : 1) * sizeof(double));
-    double* vv = (double*)calloc(n * n ? n * n : 1, sizeof(double));
+    double* a = (double*)malloc((n > 0 ? n * n : 1) * sizeof(double));
+    double* vv = (double*)calloc(n > 0 ? n * n : 1, sizeof(double));
     for (size_t j = 0; j < n; ++j)
         for (size_t i = 0; i < n; ++i) AT(a, n, i, j) = 0.5 * (AT(s, n, i, j) + AT(s, n, j, i));
     const double threshold = 1e-12 * sqrt(orc_frobenius_norm_sq(a, n * n));
