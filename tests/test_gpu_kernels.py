@@ -122,6 +122,22 @@ def test_eig_block_schemes(sk, ref, monkeypatch, tb, n):
         assert single < 1e-9 and cluster < 1e-9
 
 
+def test_eig_quad_default_ragged(sk):
+    """Default scheme selection at large n: n = 3100 (quad scheme, padded to 3136)
+    against LAPACK on a Gram spectrum: eigenvalues, residual, orthogonality."""
+    n = 3100
+    rng = np.random.default_rng(31)
+    x = rng.standard_normal((n + 500, n))
+    s = np.asfortranarray(x.T @ x)
+    e = sk.eig_sym(s)
+    w, v = e.eigenvalues, e.eigenvectors
+    fro = np.linalg.norm(s)
+    assert np.all(np.diff(w) <= 0)
+    assert np.max(np.abs(w - np.linalg.eigvalsh(s)[::-1])) <= 1e-13 * fro
+    assert np.linalg.norm(s @ v - v * w) <= 1e-10 * fro
+    assert np.max(np.abs(v.T @ v - np.eye(n))) <= 1e-12
+
+
 def test_eig_errors(sk):
     with pytest.raises(errors.DimensionError):
         sk.eig_sym(np.ones((2, 3)))
