@@ -212,14 +212,8 @@ int read_flag(Ctx* c, int idx) {
 // nblk x NB x NB). Returns false on a pivot breakdown.
 bool potrf_upper(Ctx* c, double* G, int64_t ldg, int64_t p, double* R, int64_t ldr,
                  double* Rinv_blocks, double rel_tol) {
-    static bool attr = false;
     const size_t smem = 3 * static_cast<size_t>(NB) * (NB + 1) * sizeof(double);  // S, X, T
-    if (!attr) {
-        SVDK_CUDA(cudaFuncSetAttribute(chol_diag_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem)));
-        attr = true;
-    }
+    ensure_smem_attr(reinterpret_cast<const void*>(chol_diag_kernel), smem);
     DBuf diag(c, p);
     diag_copy_kernel<<<static_cast<unsigned>(ceil_div(p, 256)), 256, 0, c->stream>>>(
         G, ldg, p, 0.0, diag.p(), nullptr, 0);

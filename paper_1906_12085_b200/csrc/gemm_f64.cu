@@ -402,14 +402,8 @@ bool tma_ok(const void* p, int64_t ld) {
 }
 
 void launch(Ctx* c, Params& p, const CUtensorMap& ma, const CUtensorMap& mb) {
-    static bool attr_set = false;
-    if (!attr_set) {
-        SVDK_CUDA(cudaFuncSetAttribute(gemm_kernel<false>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-        SVDK_CUDA(cudaFuncSetAttribute(gemm_kernel<true>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-        attr_set = true;
-    }
+    ensure_smem_attr(reinterpret_cast<const void*>(gemm_kernel<false>), SMEM_BYTES);
+    ensure_smem_attr(reinterpret_cast<const void*>(gemm_kernel<true>), SMEM_BYTES);
     DBuf partial;
     if (p.splits > 1) {
         partial = DBuf(c, static_cast<size_t>(p.units) * TILE_ELEMS);

@@ -939,19 +939,9 @@ void run_sweeps(Ctx* c, double* A, double* V, int64_t n_pad, int max_sweeps, dou
     constexpr int nthreads_solve = solve_threads<TB>();
     const size_t smem_a = 4 * TB * (TB + 4) * sizeof(double);
     const size_t smem_v = 3 * TB * (TB + 4) * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-        SVDK_CUDA(cudaFuncSetAttribute(jacobi_pair_solve<TB>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem_solve)));
-        SVDK_CUDA(cudaFuncSetAttribute(jacobi_update_a<TB>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem_a)));
-        SVDK_CUDA(cudaFuncSetAttribute(jacobi_update_v<TB>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem_v)));
-        attr = true;
-    }
+    ensure_smem_attr(reinterpret_cast<const void*>(jacobi_pair_solve<TB>), smem_solve);
+    ensure_smem_attr(reinterpret_cast<const void*>(jacobi_update_a<TB>), smem_a);
+    ensure_smem_attr(reinterpret_cast<const void*>(jacobi_update_v<TB>), smem_v);
     // Inner skip threshold: if every off-diagonal entry were this small the
     // outer test off <= 1e-12 ||A||_F would hold with a 10x margin.
     const double skip_tau = 1e-13 * fro / static_cast<double>(n_pad);
@@ -1484,9 +1474,6 @@ __global__ void __launch_bounds__(128, 4)
     if (row_begin >= n_rows || !__ldcg(&active[q])) return;
     int qa, qb;
     circle_pair(ns, round, q, qa, qb);
-    auto gq = [&](int i) -> int64_t {
-        return i < 32 ? static_cast<int64_t>(qa) * 32 + i : static_cast<int64_t>(qb) * 32 + (i - 32);
-    };
     const double* Qq = Qbuf + static_cast<size_t>(q) * 4096;
 #pragma unroll
     for (int it = 0; it < 16; ++it) {
@@ -1536,14 +1523,8 @@ __global__ void __launch_bounds__(128, 4)
 void run_sweeps_quad(Ctx* c, double* A, double* V, int64_t n_pad, int max_sweeps, double thr, double fro,
                      DBuf& scratch, int& sweeps, double& off) {
     const int ns = static_cast<int>(n_pad / 32), ks = ns / 2, rounds = ns - 1;
-    static bool attr = false;
-    if (!attr) {
-        SVDK_CUDA(cudaFuncSetAttribute(jacobi_quad_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(QUAD_SMEM)));
-        SVDK_CUDA(cudaFuncSetAttribute(jacobi_update_a64, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(A64_SMEM)));
-        attr = true;
-    }
+    ensure_smem_attr(reinterpret_cast<const void*>(jacobi_quad_solve), QUAD_SMEM);
+    ensure_smem_attr(reinterpret_cast<const void*>(jacobi_update_a64), A64_SMEM);
     const double skip_tau = 1e-13 * fro / static_cast<double>(n_pad);  // as run_sweeps
     DBuf qbuf(c, static_cast<size_t>(rounds) * ks * 4096);
     DBuf act(c, static_cast<size_t>(rounds) * ks);

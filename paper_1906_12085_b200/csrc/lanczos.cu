@@ -324,8 +324,7 @@ void launch_gemv_cluster(Ctx* c, const CUtensorMap& map, const double* A, int64_
 // would run the remainder as a second wave.
 template <int CS, bool LA>
 int prepare_gemv_cluster(const GcLayout& L, int num_sms) {
-    SVDK_CUDA(cudaFuncSetAttribute(gemv_pair_cluster_kernel<CS, LA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(L.smem)));
+    ensure_smem_attr(reinterpret_cast<const void*>(gemv_pair_cluster_kernel<CS, LA>), L.smem);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(num_sms / CS * CS));
     cfg.blockDim = dim3((GC_NCW + 1) * 32);

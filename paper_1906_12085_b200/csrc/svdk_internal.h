@@ -10,7 +10,10 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <map>
+#include <mutex>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "svdk.h"
@@ -153,6 +156,23 @@ private:
 
 inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 inline int64_t ceil_div(int64_t x, int64_t m) { return (x + m - 1) / m; }
+
+// Raise a kernel's MaxDynamicSharedMemorySize to at least `bytes` on the
+// current device (set once per (kernel, device, larger size)): function
+// attributes are per device, one process may drive several GPUs, and contexts
+// may be used from several host threads.
+inline void ensure_smem_attr(const void* func, size_t bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, size_t> set_to;
+    int dev = 0;
+    SVDK_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(mu);
+    size_t& cur = set_to[{func, dev}];
+    if (bytes > cur) {
+        SVDK_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
+        cur = bytes;
+    }
+}
 
 // ---------------------------------------------------------------------------
 // Engine entry points shared across translation units (device pointers,
