@@ -64,6 +64,11 @@ void need_ctx(svdk_ctx* c) {
     if (!c) fail(SVDK_E_STATE, "null svdk_ctx");
 }
 
+}  // namespace
+
+// Host-buffer and method-dispatch helpers (shared with stream_fit.cu).
+namespace svdk {
+
 // Host column-major (ld = rows) -> device with an even leading dimension
 // (TMA needs 16-byte strides).
 DBuf upload(Ctx* c, const double* h, int64_t rows, int64_t cols, int64_t& ld) {
@@ -169,6 +174,10 @@ void validate_method(int method, int64_t m, int64_t n, int64_t l, int64_t q, con
     if (method < 0 || method > SVDK_LANCZOS) fail(SVDK_E_PARAM, "compute_svd: unknown method");
 }
 
+}  // namespace svdk
+
+namespace {
+
 // Host-pointer method call: H2D, run, D2H (u m x rank, sigma, v n x rank).
 void host_method(svdk_ctx* c, int method, const double* a, int64_t m, int64_t n, int64_t l,
                  int64_t q, uint64_t seed, double* u, double* sigma, double* v, int64_t* rank,
@@ -231,6 +240,8 @@ int svdk_ctx_destroy(svdk_ctx* ctx) {
         for (cudaEvent_t e : ctx->event_pool) cudaEventDestroy(e);
         if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
         if (ctx->aux_stream) cudaStreamDestroy(ctx->aux_stream);
+        if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+        if (ctx->copy_ev) cudaEventDestroy(ctx->copy_ev);
         for (cudaEvent_t e : ctx->aux_ev)
             if (e) cudaEventDestroy(e);
         delete ctx;
@@ -510,6 +521,11 @@ int svdk_fit_pca(svdk_ctx* c, const double* data, int64_t m, int64_t n, int orie
             else if (method == SVDK_LANCZOS)
                 omega_prefetch(c, tn, 1, seed);
         }
+        // Truncated / randomized on a tall centred RowsAreExamples matrix: the
+        // upload streams in row chunks under the Gram / sketch (stream_fit.cu).
+        if (!cols_ex && center &&
+            fit_pca_streamed(c, data, m, n, method, l, q, seed, basis, eigenvalues, total, mean, rank))
+            return;
         // The upload buffer is ours: centre it in place (no second m x n copy,
         // which is what lets the 64 GB c4 matrix fit one GPU).
         int64_t lda;

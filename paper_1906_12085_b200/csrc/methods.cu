@@ -129,8 +129,17 @@ int64_t back_project(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n,
 // V (n x rank, ldv). Returns rank.
 int64_t truncated_svd(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n, double* U,
                       int64_t ldu, double* sigma, double* V, int64_t ldv, const RowComm* comm) {
-    DBuf G(c, static_cast<size_t>(n) * n), w(c, n), Vfull(c, static_cast<size_t>(n) * n);
+    DBuf G(c, static_cast<size_t>(n) * n);
     gram_rows(c, A, lda, m, n, G.p(), n, comm);
+    return truncated_from_gram(c, A, lda, m, n, std::move(G), U, ldu, sigma, V, ldv, comm);
+}
+
+// The rest of truncated_svd once G = A^T A (n x n, ld n) is formed (also the
+// entry of the streamed host-buffer path, which accumulates G chunk by chunk).
+int64_t truncated_from_gram(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n, DBuf G,
+                            double* U, int64_t ldu, double* sigma, double* V, int64_t ldv,
+                            const RowComm* comm) {
+    DBuf w(c, n), Vfull(c, static_cast<size_t>(n) * n);
     eig_sym_rows(c, G.p(), n, n, w.p(), Vfull.p(), n, comm);
     G.reset();
     return back_project(c, A, lda, m, n, w.p(), Vfull.p(), n, n, U, ldu, sigma, V, ldv);

@@ -138,15 +138,25 @@ int64_t randomized_pca(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t 
                        int64_t q, uint64_t seed, double* U, int64_t ldu, double* sigma, double* V,
                        int64_t ldv, const RowComm* comm) {
     const int64_t ldh = round_up(std::max<int64_t>(m, 1), 2);
-    DBuf Om(c, static_cast<size_t>(n) * l), H(c, static_cast<size_t>(ldh) * l),
-        H2(c, static_cast<size_t>(ldh) * l), Z(c, static_cast<size_t>(n) * l);
-    omega_upload(c, n, l, seed, Om.p());
-    gemm(c, false, m, l, n, A, lda, Om.p(), n, H.p(), ldh, nullptr, true);  // H = A Omega
+    DBuf H(c, static_cast<size_t>(ldh) * l);
+    {
+        DBuf Om(c, static_cast<size_t>(n) * l);
+        omega_upload(c, n, l, seed, Om.p());
+        gemm(c, false, m, l, n, A, lda, Om.p(), n, H.p(), ldh, nullptr, true);  // H = A Omega
+    }
+    return randomized_from_sketch(c, A, lda, m, n, l, q, std::move(H), ldh, U, ldu, sigma, V, ldv, comm);
+}
+
+// The rest of randomized_pca once H = A Omega (m x l, ld ldh) is formed (also
+// the entry of the streamed host-buffer path, which forms H chunk by chunk).
+int64_t randomized_from_sketch(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n, int64_t l,
+                               int64_t q, DBuf H, int64_t ldh, double* U, int64_t ldu, double* sigma,
+                               double* V, int64_t ldv, const RowComm* comm) {
+    DBuf H2(c, static_cast<size_t>(ldh) * l), Z(c, static_cast<size_t>(n) * l);
     for (int64_t j = 0; j < q; ++j) {
         power_step(c, A, lda, m, n, H.p(), ldh, l, H2.p(), ldh, Z.p(), comm);
         std::swap(H, H2);
     }
-    Om.reset();
     // Q = qr_thin(H).q = Q1 Rinv  (H2 reused as Q1)
     DBuf Rinv(c, static_cast<size_t>(l) * l), T(c, static_cast<size_t>(n) * l);
     qr_thin(c, H.p(), ldh, m, l, H2.p(), ldh, nullptr, comm, Rinv.p());

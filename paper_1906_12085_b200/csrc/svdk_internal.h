@@ -115,6 +115,8 @@ struct Ctx {
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     cudaStream_t aux_stream = nullptr;  // side stream for off-critical-path work
+    cudaStream_t copy_stream = nullptr;  // host-buffer uploads streamed under compute
+    cudaEvent_t copy_ev = nullptr;
     cudaEvent_t aux_ev[2] = {nullptr, nullptr};
     Pool pool;
     // scratch: small pinned host buffer for scalars / flags

@@ -89,6 +89,27 @@ int64_t truncated_svd(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n
                       const RowComm* comm = nullptr);
 
 // Full PCA pipeline on a device-resident (local shard of) A; see svdk.h.
+// Host-buffer / dispatch helpers (abi.cu)
+DBuf upload(Ctx* c, const double* h, int64_t rows, int64_t cols, int64_t& ld);
+DBuf alloc_mat(Ctx* c, int64_t rows, int64_t cols, int64_t& ld);
+void download(Ctx* c, double* h, const double* d, int64_t ld, int64_t rows, int64_t cols);
+int64_t run_method(Ctx* c, int method, const double* dA, int64_t lda, int64_t m, int64_t n, int64_t l,
+                   int64_t q, uint64_t seed, double* dU, int64_t ldu, double* dS, double* dV, int64_t ldv,
+                   const RowComm* comm);
+int64_t method_width(int method, int64_t m, int64_t n, int64_t l, int64_t q);
+void validate_method(int method, int64_t m, int64_t n, int64_t l, int64_t q, const char* name);
+int64_t truncated_from_gram(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n, DBuf G,
+                            double* U, int64_t ldu, double* sigma, double* V, int64_t ldv,
+                            const RowComm* comm);
+int64_t randomized_from_sketch(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n, int64_t l,
+                               int64_t q, DBuf H, int64_t ldh, double* U, int64_t ldu, double* sigma,
+                               double* V, int64_t ldv, const RowComm* comm);
+// Host-buffer fit_pca (RowsAreExamples, centred, tall, truncated/randomized)
+// with the H2D copy streamed in column chunks under the Gram / sketch; returns
+// false (nothing done) when the shape does not qualify.
+bool fit_pca_streamed(Ctx* c, const double* host, int64_t m, int64_t n, int method, int64_t l, int64_t q,
+                      uint64_t seed, double* basis, double* eigenvalues, double* total, double* mean,
+                      int64_t* rank);
 void dev_pca(Ctx* c, const double* A, int64_t m_local, int64_t n, int64_t lda, int method,
              int64_t l, int64_t q, uint64_t seed, int center_mode, double threshold, double* U,
              int64_t ldu, double* sigma, double* V, int64_t ldv, double* mean, int64_t* rank,

@@ -94,6 +94,43 @@ def test_c1_fit_pca_vs_reference(sk, method):
     assert single <= 1e-8 and cluster <= 1e-8
 
 
+@pytest.mark.parametrize("method", ["truncated", "randomized"])
+def test_fit_pca_streamed_upload(sk, monkeypatch, method):
+    """Host-buffer fit_pca with the upload streamed in column chunks under the
+    Gram / sketch (stream_fit.cu) on c1 in two chunks (192 + 64 columns): same
+    golden bars as the plain path; then a matrix with large
+    column means (|mu| ~ 1e3 x the spread) against the plain path."""
+    gz = golden("c1.npz")
+    a = make_matrix(20000, 256, "c1", seed=int(gz["seed"]))
+    l, q, rs = (int(x) for x in gz[f"{method}_params"])
+    enum = sk.SvdMethod.Truncated if method == "truncated" else sk.SvdMethod.Randomized
+    params = sk.MethodParams(l, q, sk.RngSeed(rs))
+    monkeypatch.setenv("SVDK_STREAM_COLS", "192")
+    monkeypatch.setenv("SVDK_STREAM", "2")  # randomized streams only on request
+    model = sk.fit_pca(a, sk.Orientation.RowsAreExamples, enum, params, True)
+    lam_ref, v_ref = gz[f"{method}_lambda"], gz[f"{method}_v"]
+    assert abs(model.total_variance - float(gz["total"])) <= 1e-12 * float(gz["total"])
+    assert eig_rel_err(model.eigenvalues, lam_ref) <= 1e-10
+    k = sk.select_components(model.eigenvalues, model.total_variance, float(gz["threshold"]))
+    assert k == int(gz[f"{method}_k"]) == 214
+    assert subspace_sine(model.basis[:, :k], v_ref[:, :k]) <= 1e-8
+    single, cluster = per_vector_sines(model.basis, lam_ref, v_ref)
+    assert single <= 1e-8 and cluster <= 1e-8
+    # large, chunk-varying column means
+    rng = np.random.default_rng(5)
+    spread = float(np.sqrt(gz["total"] / a.size))
+    shifted = np.asfortranarray(a + 1e3 * spread * (1.0 + rng.standard_normal(256))[None, :]
+                                + spread * np.linspace(0.0, 5.0, 20000)[:, None])
+    streamed = sk.fit_pca(shifted, sk.Orientation.RowsAreExamples, enum, params, True)
+    monkeypatch.setenv("SVDK_STREAM", "0")
+    plain = sk.fit_pca(shifted, sk.Orientation.RowsAreExamples, enum, params, True)
+    assert np.max(np.abs(streamed.mean - plain.mean)) <= 1e-12 * np.max(np.abs(plain.mean))
+    assert abs(streamed.total_variance - plain.total_variance) <= 1e-11 * plain.total_variance
+    assert eig_rel_err(streamed.eigenvalues, plain.eigenvalues) <= 1e-10
+    kk = sk.select_components(plain.eigenvalues, plain.total_variance, 0.95)
+    assert subspace_sine(streamed.basis[:, :kk], plain.basis[:, :kk]) <= 1e-8
+
+
 def test_c2mid_golden(sk):
     """c2's spectrum/method (l = n = 1024, q = 2, t = 0.99) at 20000 rows vs the reference."""
     gz = golden("c2mid.npz")
