@@ -61,7 +61,8 @@ void omega_prefetch(Ctx* c, int64_t rows, int64_t cols, uint64_t seed) {
     c->omega_job = job;
 }
 
-void omega_upload(Ctx* c, int64_t rows, int64_t cols, uint64_t seed, double* d_out) {
+void omega_upload(Ctx* c, int64_t rows, int64_t cols, uint64_t seed, double* d_out, cudaStream_t stream) {
+    if (!stream) stream = c->stream;
     const bool ready = c->omega_job && c->omega_job->rows == rows && c->omega_job->cols == cols &&
                        c->omega_job->seed == seed;
     if (ready) {
@@ -71,8 +72,8 @@ void omega_upload(Ctx* c, int64_t rows, int64_t cols, uint64_t seed, double* d_o
         gaussian_fill(rows, cols, seed, staging(c, static_cast<size_t>(rows) * cols));
     }
     SVDK_CUDA(cudaMemcpyAsync(d_out, c->pinned, sizeof(double) * rows * cols,
-                              cudaMemcpyHostToDevice, c->stream));
-    SVDK_CUDA(cudaEventRecord(c->pinned_ev, c->stream));
+                              cudaMemcpyHostToDevice, stream));
+    SVDK_CUDA(cudaEventRecord(c->pinned_ev, stream));
 }
 
 void release_host_staging(Ctx* c) {

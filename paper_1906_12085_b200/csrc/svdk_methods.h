@@ -41,9 +41,10 @@ void frob_sq_rows_dev(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n
 // Reference Gaussian sampler (host, bit-identical) staged through pinned
 // memory. omega_prefetch starts filling it on a host thread so the sample is
 // ready when the first GEMM needs it; omega_upload joins (or generates) and
-// issues the H2D copy on the context stream.
+// issues the H2D copy on `stream` (default: the context stream).
 void omega_prefetch(Ctx* c, int64_t rows, int64_t cols, uint64_t seed);
-void omega_upload(Ctx* c, int64_t rows, int64_t cols, uint64_t seed, double* d_out);
+void omega_upload(Ctx* c, int64_t rows, int64_t cols, uint64_t seed, double* d_out,
+                  cudaStream_t stream = nullptr);
 void release_host_staging(Ctx* c);
 
 // Non-finite GEMM results (kernels.cpp:39-43) set a sticky device flag; the

@@ -96,17 +96,18 @@ def test_c1_fit_pca_vs_reference(sk, method):
 
 @pytest.mark.parametrize("method", ["truncated", "randomized"])
 def test_fit_pca_streamed_upload(sk, monkeypatch, method):
-    """Host-buffer fit_pca with the upload streamed in column chunks under the
-    Gram / sketch (stream_fit.cu) on c1 in two chunks (192 + 64 columns): same
-    golden bars as the plain path; then a matrix with large
+    """Host-buffer fit_pca with the upload streamed under the first pass
+    (stream_fit.cu) on c1: truncated in two column chunks (192 + 64 columns),
+    randomized in 7 row chunks (each centred by its own means, closed-form
+    correction to the global mean); same golden bars as the plain path; then a matrix with large
     column means (|mu| ~ 1e3 x the spread) against the plain path."""
     gz = golden("c1.npz")
     a = make_matrix(20000, 256, "c1", seed=int(gz["seed"]))
     l, q, rs = (int(x) for x in gz[f"{method}_params"])
     enum = sk.SvdMethod.Truncated if method == "truncated" else sk.SvdMethod.Randomized
     params = sk.MethodParams(l, q, sk.RngSeed(rs))
-    monkeypatch.setenv("SVDK_STREAM_COLS", "192")
-    monkeypatch.setenv("SVDK_STREAM", "2")  # randomized streams only on request
+    monkeypatch.setenv("SVDK_STREAM_COLS", "192")  # truncated: column chunks
+    monkeypatch.setenv("SVDK_STREAM_ROWS", "3000")  # randomized: row chunks (7, last partial)
     model = sk.fit_pca(a, sk.Orientation.RowsAreExamples, enum, params, True)
     lam_ref, v_ref = gz[f"{method}_lambda"], gz[f"{method}_v"]
     assert abs(model.total_variance - float(gz["total"])) <= 1e-12 * float(gz["total"])

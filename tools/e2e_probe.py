@@ -44,6 +44,17 @@ for mode in ["1", "0", "1", "0"]:
         torch.cuda.synchronize()
         ts.append(time.perf_counter() - t0)
     print(f"fit_pca stream={mode}: {min(ts) * 1e3:.1f} ms (best of 3), all {[round(t * 1e3, 1) for t in ts]}", flush=True)
+    eng.ctx.set_timing(True)
+    eng.ctx.timing_reset()
+    t0 = time.perf_counter()
+    _lib.check(lib.svdk_fit_pca(eng.ctx.handle, C.c_void_p(host.data_ptr()), m, n, 1, mid, cfg["l"], cfg["q"],
+                                4242, 1, C.c_void_p(basis.data_ptr()), C.c_void_p(eig.data_ptr()), C.byref(total),
+                                C.c_void_p(mean.data_ptr()), C.byref(rank)))
+    torch.cuda.synchronize()
+    wall = (time.perf_counter() - t0) * 1e3
+    print("   phases (device ms):", {k: round(eng.ctx.timing(k)["ms"], 2) for k in eng.ctx.timing_names()},
+          f"wall {wall:.1f} ms", flush=True)
+    eng.ctx.set_timing(False)
 dev = torch.empty(n, m, dtype=torch.float64, device="cuda").t()
 for label, chunk in (("contiguous", m), ("2-D chunks of 32768 rows", 32768)):
     ts = []
