@@ -149,13 +149,17 @@ int64_t randomized_pca(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t 
 }
 
 // The rest of randomized_pca once H = A Omega (m x l, ld ldh) is formed (also
-// the entry of the streamed host-buffer path, which forms H chunk by chunk).
+// the entry of the streamed host-buffer path, which forms H chunk by chunk,
+// and with Z_first != nullptr the first power iteration's A^T H as well).
 int64_t randomized_from_sketch(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n, int64_t l,
                                int64_t q, DBuf H, int64_t ldh, double* U, int64_t ldu, double* sigma,
-                               double* V, int64_t ldv, const RowComm* comm) {
+                               double* V, int64_t ldv, const RowComm* comm, const double* Z_first) {
     DBuf H2(c, static_cast<size_t>(ldh) * l), Z(c, static_cast<size_t>(n) * l);
     for (int64_t j = 0; j < q; ++j) {
-        power_step(c, A, lda, m, n, H.p(), ldh, l, H2.p(), ldh, Z.p(), comm);
+        if (j == 0 && Z_first)  // A^T H already formed by the caller (n x l, ld n)
+            gemm(c, false, m, l, n, A, lda, Z_first, n, H2.p(), ldh, nullptr, true);  // H = A Z
+        else
+            power_step(c, A, lda, m, n, H.p(), ldh, l, H2.p(), ldh, Z.p(), comm);
         std::swap(H, H2);
     }
     // Q = qr_thin(H).q = Q1 Rinv  (H2 reused as Q1)

@@ -75,6 +75,19 @@ __global__ void add_chunk_rows_kernel(double* X, int64_t ldx, int64_t m, int64_t
     }
 }
 
+// E[k, j] = SH[k][j] + cnt_k W[k, j] (C x l, ld ldd; padding rows zero): the
+// chunk-sum term of the first power iteration's correction (see below).
+__global__ void sketch_corr_kernel(const double* SH /* [C][l] */, const double* W, int C, int64_t l,
+                                   int64_t rows, int64_t m, int64_t ldd, double* E) {
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < ldd * l;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t j = e / ldd, k = e - j * ldd;
+        double v = 0.0;
+        if (k < C) v = fma(static_cast<double>(min(rows, m - k * rows)), W[k + j * ldd], SH[k * l + j]);
+        E[k + j * ldd] = v;
+    }
+}
+
 __global__ void sum_fixed_order_kernel(const double* partial, int count, double* out) {
     if (threadIdx.x == 0 && blockIdx.x == 0) {
         double s = 0.0;
@@ -114,8 +127,12 @@ int64_t chunk_rows(int64_t m, int64_t n) {
 //   A^c rows of chunk k = (A_k - 1 mu_k^T) + 1 d_k^T,  d_k = mu_k - mu,
 //   H rows of chunk k   = (A_k - 1 mu_k^T) Omega + 1 (Omega^T d_k)^T.
 // d_k is the spread of the chunk means, so the correction introduces no
-// cancellation. One more pass adds d_k to the stored chunks (A becomes the
-// globally centred matrix the power iterations read), fused with the total.
+// cancellation. With power iterations (q >= 1) the first A^T H is accumulated
+// per chunk as well, Z = sum_k (A_k - 1 mu_k^T)^T H_k^raw, and corrected with
+//   A^c^T H = Z + sum_k d_k (s_k + cnt_k w_k)^T,  s_k = H_k^raw^T 1, w_k = Omega^T d_k
+// (the (A_k - 1 mu_k^T)^T 1 terms vanish: each chunk is centred by its own
+// mean). One more pass adds d_k to the stored chunks (A becomes the globally
+// centred matrix the remaining iterations read), fused with the total.
 bool streamed_sketch_rows(Ctx* c, const double* host, int64_t m, int64_t n, int64_t l, int64_t q, uint64_t seed,
                           double* basis, double* eigenvalues, double* total, double* mean, int64_t* rank) {
     const int64_t rows = chunk_rows(m, n);
@@ -128,6 +145,8 @@ bool streamed_sketch_rows(Ctx* c, const double* host, int64_t m, int64_t n, int6
     DBuf mu_k(c, static_cast<size_t>(C) * n), mu(c, n);
     const int64_t ldh = round_up(m, 2);
     DBuf H(c, static_cast<size_t>(ldh) * l), Om(c, static_cast<size_t>(n) * l);
+    const bool with_z = q >= 1;
+    DBuf Z(c, with_z ? static_cast<size_t>(n) * l : 1), SH(c, with_z ? static_cast<size_t>(C) * l : 1);
     reset_nonfinite(c);
     {
         PhaseTimer timer(c, "streamed_upload");
@@ -171,6 +190,10 @@ bool streamed_sketch_rows(Ctx* c, const double* host, int64_t m, int64_t n, int6
             column_sums(c, Ak, lda, mk, n, static_cast<double>(mk), muk);
             subtract_column_means(c, Ak, lda, mk, n, muk, Ak, lda);
             gemm(c, false, mk, l, n, Ak, lda, Om.p(), n, H.p() + r0, ldh, nullptr, true);  // H_k = A_k^c Omega
+            if (with_z) {  // s_k and Z += A_k^c^T H_k
+                column_sums(c, H.p() + r0, ldh, mk, l, 1.0, SH.p() + k * l);
+                gemm(c, true, n, l, mk, Ak, lda, H.p() + r0, ldh, Z.p(), n, nullptr, false, 1.0, k > 0);
+            }
             mark(S);
         }
         if (trace) {
@@ -193,6 +216,14 @@ bool streamed_sketch_rows(Ctx* c, const double* host, int64_t m, int64_t n, int6
     SVDK_CHECK_LAUNCH();
     gemm(c, false, ldd, l, n, d.p(), ldd, Om.p(), n, Wd.p(), ldd);  // row k = (Omega^T d_k)^T
     Om.reset();
+    if (with_z) {  // Z += D^T E, E row k = s_k + cnt_k w_k
+        DBuf E(c, static_cast<size_t>(ldd) * l);
+        sketch_corr_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(ldd * l, 256), 4 * c->num_sms)), 256,
+                             0, S>>>(SH.p(), Wd.p(), static_cast<int>(C), l, rows, m, ldd, E.p());
+        SVDK_CHECK_LAUNCH();
+        c->launches++;
+        gemm(c, true, n, l, ldd, d.p(), ldd, E.p(), ldd, Z.p(), n, nullptr, false, 1.0, true);
+    }
     {
         const dim3 gh(static_cast<unsigned>(std::min<int64_t>(ceil_div(m, 256), 2 * c->num_sms)),
                       static_cast<unsigned>(std::min<int64_t>(l, 256)));
@@ -212,7 +243,7 @@ bool streamed_sketch_rows(Ctx* c, const double* host, int64_t m, int64_t n, int6
     int64_t ldu, ldv;
     DBuf dU = alloc_mat(c, m, l, ldu), dV = alloc_mat(c, n, l, ldv), dS(c, std::max(l, n));
     const int64_t r = randomized_from_sketch(c, dA.p(), lda, m, n, l, q, std::move(H), ldh, dU.p(), ldu, dS.p(),
-                                             dV.p(), ldv, nullptr);
+                                             dV.p(), ldv, nullptr, with_z ? Z.p() : nullptr);
     raise_if_nonfinite(c);
     download(c, basis, dV.p(), ldv, n, r);  // RowsAreExamples: basis = V
     std::vector<double> sv(r);

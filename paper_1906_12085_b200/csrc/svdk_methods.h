@@ -104,7 +104,7 @@ int64_t truncated_from_gram(Ctx* c, const double* A, int64_t lda, int64_t m, int
                             const RowComm* comm);
 int64_t randomized_from_sketch(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n, int64_t l,
                                int64_t q, DBuf H, int64_t ldh, double* U, int64_t ldu, double* sigma,
-                               double* V, int64_t ldv, const RowComm* comm);
+                               double* V, int64_t ldv, const RowComm* comm, const double* Z_first = nullptr);
 // Host-buffer fit_pca (RowsAreExamples, centred, tall, truncated/randomized)
 // with the H2D copy streamed in column chunks under the Gram / sketch; returns
 // false (nothing done) when the shape does not qualify.
