@@ -1249,6 +1249,8 @@ __global__ void __launch_bounds__(Q_THREADS, 1)
     auto g = [&](int i) -> int64_t {
         return i < 32 ? static_cast<int64_t>(a) * 32 + i : static_cast<int64_t>(b) * 32 + (i - 32);
     };
+    const bool probe = blockIdx.x == 0 && tid == 0 && round == 5;
+    if (probe) SVDK_PROBE_STORE(g_jprobe, 0, SVDK_CLOCK());
     for (int e = tid; e < 64 * 64; e += Q_THREADS) {
         const int i = e & 63, j = e >> 6;
         M64[i + j * L64] = __ldcg(&A[g(i) + g(j) * lda]);
@@ -1275,12 +1277,14 @@ __global__ void __launch_bounds__(Q_THREADS, 1)
         }
         const int w0 = __syncthreads_or(big && h == 0);
         const int w1 = __syncthreads_or(big && h == 1);
+        if (probe) SVDK_PROBE_STORE(g_jprobe, 1 + 3 * s, SVDK_CLOCK());
         if (!(w0 | w1)) continue;  // uniform: nothing to rotate in this sub-stage
         any = true;
         // each half's rotation Q_h (32 x 32, ld L32) lands in the P region
         quad_sub_solve(Mc, Mn, Qs, P + h * SUB32, *st, cs, sn, R, ltid, 1 + h, h ? w1 != 0 : w0 != 0,
                        skip_tau);
         __syncthreads();
+        if (probe) SVDK_PROBE_STORE(g_jprobe, 2 + 3 * s, SVDK_CLOCK());
         // M <- P^T M P and Qa <- Qa P with P = Q_0 (+) Q_1 on the two index
         // sets, as 16 x 32 warp tiles: T1 forms Y_{h1 h2} = M[h1, h2] Q_h2 for
         // the three blocks h1 <= h2 and Qa[:, h] Q_h; T2 forms Q_h1^T Y_{h1 h2},
@@ -1289,7 +1293,8 @@ __global__ void __launch_bounds__(Q_THREADS, 1)
         double* Y = H;                 // Y_00, Y_01, Y_11 (ld L32)
         double* Qn = H + 4 * SUB32;    // Qa[:, h] Q_h: two 64 x 32 (ld L64)
         const int wi = tid >> 5;
-        if (wi < 6) {
+        const bool last = s == nsub - 1;  // after the last sub-stage only Qa is needed
+        if (wi < 6 && !last) {
             const int blk = wi >> 1, r0 = 16 * (wi & 1);
             const int h1 = blk == 2 ? 1 : 0, h2 = blk == 0 ? 0 : 1;
             warp_tile_16x32(
@@ -1303,7 +1308,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1)
                             [&](int m, int n, double v) { Qn[hq * 32 * L64 + (r0 + m) + n * L64] = v; });
         }
         __syncthreads();
-        if (wi < 6) {
+        if (wi < 6 && !last) {
             const int blk = wi >> 1, r0 = 16 * (wi & 1);
             const int h1 = blk == 2 ? 1 : 0, h2 = blk == 0 ? 0 : 1;
             warp_tile_16x32([&](int m, int k) { return Qh[h1 * SUB32 + k + (r0 + m) * L32]; },
@@ -1315,11 +1320,13 @@ __global__ void __launch_bounds__(Q_THREADS, 1)
                                 M64[j + i * L64] = v;
                             });
         } else {
-            for (int e = tid - 6 * 32; e < 64 * 64; e += Q_THREADS - 6 * 32) {
+            const int t0 = last ? 0 : 6 * 32;
+            for (int e = tid - t0; e < 64 * 64; e += Q_THREADS - t0) {
                 const int row = e & 63, col = (e >> 6) & 31, hq = e >> 11;
                 Qa[row + quad_idx(kind, hq, col) * L64] = Qn[hq * 32 * L64 + row + col * L64];
             }
         }
+        if (probe && s < 2) SVDK_PROBE_STORE(g_jprobe, 3 + 3 * s, SVDK_CLOCK());
     }
     __syncthreads();
     if (any) {
@@ -1327,6 +1334,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1)
         for (int e = tid; e < 64 * 64; e += Q_THREADS) out[e] = Qa[(e & 63) + (e >> 6) * L64];
     }
     if (tid == 0) active[blockIdx.x] = any ? 1 : 0;
+    if (probe) SVDK_PROBE_STORE(g_jprobe, 7, SVDK_CLOCK());
 }
 
 // A[ST_p, ST_q] <- Q_p^T A[ST_p, ST_q] Q_q for one super-pair block (p <= q)
