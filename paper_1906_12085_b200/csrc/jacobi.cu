@@ -929,6 +929,80 @@ double device_sumsq(Ctx* c, const double* A, int64_t n, int mode, DBuf& scratch)
     return out;
 }
 
+// Convergence test of one sweep on the device: off = sqrt(2 sum partial)
+// (fixed order, as device_sumsq), sweep counter, and the WHILE condition of
+// the enclosing graph: keep sweeping while off > thr and sweeps < max_sweeps
+// (kernels.cpp:274-326, the host loop's exact test).
+__global__ void jacobi_decide_kernel(cudaGraphConditionalHandle h, const double* partial, int count, double thr,
+                                     int max_sweeps, double* state) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double s = 0.0;
+    for (int i = 0; i < count; ++i) s += partial[i];
+    const double off = sqrt(2.0 * s);
+    const double sw = state[1] + 1.0;
+    state[0] = off;
+    state[1] = sw;
+    cudaGraphSetConditional(h, (off > thr && sw < static_cast<double>(max_sweeps)) ? 1u : 0u);
+}
+
+// All sweeps of eig_sym as ONE graph launch: a WHILE conditional node whose
+// body is the captured sweep (enqueue_sweep, the same kernels and streams as
+// the per-sweep graph) followed by the off-diagonal sum of squares and
+// jacobi_decide_kernel. The host no longer reads off(A) back between sweeps
+// (one round trip per sweep: ~10 sweeps x ~20-30 us of idle GPU at small n).
+// Returns false (nothing launched) where conditional nodes are unavailable.
+template <class Enqueue>
+bool sweep_loop_graph(Ctx* c, Enqueue&& enqueue_sweep, const double* A, int64_t n_pad, double thr,
+                      int max_sweeps, DBuf& scratch, int launches_per_sweep, int& sweeps, double& off) {
+    if (const char* e = std::getenv("SVDK_JACOBI_DEVLOOP"))
+        if (std::string(e) == "0") return false;
+    cudaStream_t S = c->stream;
+    if (!S) return false;
+    const int blocks = static_cast<int>(
+        std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_pad * n_pad, 256), 2 * c->num_sms)));
+    double* partial = scratch.p();
+    double* state = scratch.p() + blocks + 1;  // {off, sweeps}
+    cudaGraph_t outer = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    if (cudaGraphCreate(&outer, 0) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    cudaGraphConditionalHandle h;
+    cudaGraphNodeParams cp = {};
+    cudaGraphNode_t cnode;
+    if (cudaGraphConditionalHandleCreate(&h, outer, 1, cudaGraphCondAssignDefault) != cudaSuccess ||
+        (cp.type = cudaGraphNodeTypeConditional, cp.conditional.handle = h,
+         cp.conditional.type = cudaGraphCondTypeWhile, cp.conditional.size = 1,
+         cudaGraphAddNode(&cnode, outer, nullptr, 0, &cp) != cudaSuccess)) {
+        cudaGetLastError();
+        cudaGraphDestroy(outer);
+        return false;
+    }
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    SVDK_CUDA(cudaStreamBeginCaptureToGraph(S, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    enqueue_sweep();
+    jacobi_sumsq_kernel<<<blocks, 256, 0, S>>>(A, n_pad, 1, partial);
+    jacobi_decide_kernel<<<1, 32, 0, S>>>(h, partial, blocks, thr, max_sweeps, state);
+    cudaGraph_t captured = nullptr;
+    SVDK_CUDA(cudaStreamEndCapture(S, &captured));
+    const cudaError_t ie = cudaGraphInstantiate(&exec, outer, 0);
+    cudaGraphDestroy(outer);
+    if (ie != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    SVDK_CUDA(cudaMemsetAsync(state, 0, 2 * sizeof(double), S));
+    SVDK_CUDA(cudaGraphLaunch(exec, S));
+    double hs[2] = {0.0, 0.0};
+    d2h(c, hs, state, 2);
+    cudaGraphExecDestroy(exec);
+    off = hs[0];
+    sweeps = static_cast<int>(hs[1]);
+    c->launches += static_cast<int64_t>(sweeps) * (launches_per_sweep + 2);
+    return true;
+}
+
 template <int TB>
 void run_sweeps(Ctx* c, double* A, double* V, int64_t n_pad, int max_sweeps, double thr, double fro,
                 DBuf& scratch, int& sweeps, double& off) {
@@ -1025,6 +1099,9 @@ void run_sweeps(Ctx* c, double* A, double* V, int64_t n_pad, int max_sweeps, dou
     };
     // One sweep = 3 (nb - 1) launches on two streams: capture them once as a
     // CUDA graph (a DAG with the V chain beside the A chain) and replay it.
+    if (off > thr && max_sweeps > 0 && nb > 2 &&
+        sweep_loop_graph(c, enqueue_sweep, A, n_pad, thr, max_sweeps, scratch, 3 * slots, sweeps, off))
+        return;
     cudaGraphExec_t exec = nullptr;
     const bool use_graph = nb > 2 && S != nullptr;
     if (use_graph) {
@@ -1564,6 +1641,9 @@ void run_sweeps_quad(Ctx* c, double* A, double* V, int64_t n_pad, int max_sweeps
         SVDK_CUDA(cudaEventRecord(c->aux_ev[1], S2));
         SVDK_CUDA(cudaStreamWaitEvent(S, c->aux_ev[1], 0));
     };
+    if (off > thr && max_sweeps > 0 &&
+        sweep_loop_graph(c, enqueue_sweep, A, n_pad, thr, max_sweeps, scratch, 3 * rounds, sweeps, off))
+        return;
     cudaGraphExec_t exec = nullptr;
     const bool use_graph = S != nullptr;
     if (use_graph) {
