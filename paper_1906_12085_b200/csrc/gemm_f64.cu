@@ -433,6 +433,119 @@ void launch(Ctx* c, Params& p, const CUtensorMap& ma, const CUtensorMap& mb) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// Compact small-K GEMM / SYRK (K <= 128): the Cholesky / triangular-inverse
+// panel updates (K = 64) are a few tiles each, and a one-tile launch of the
+// big TMA/mbarrier kernel above costs ~40 us, mostly instruction fetch for its
+// fully unrolled body (ncu: `no_instruction` stalls). This kernel is small:
+// 64 x 64 output tiles, 4 warps of 32 x 32 (m8n8k4 DMMA), operands staged in
+// shared memory 16 k at a time with plain coalesced loads. Same epilogue
+// semantics as store_out (flag, column scale, alpha, beta, SYRK mirror).
+// ---------------------------------------------------------------------------
+constexpr int ST = 64, SK = 16, SLD = ST + 4;
+
+__global__ void __launch_bounds__(128)
+    gemm_small_kernel(int kind, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B,
+                      int64_t ldb, double* C, int64_t ldc, double alpha, int beta_one, const double* col_scale,
+                      int* flag, int tiles_n) {
+    __shared__ double As[SK][SLD], Bs[SK][SLD];
+    const int ti = blockIdx.x / tiles_n, tj = blockIdx.x % tiles_n;
+    if (kind == KIND_SYRK && ti > tj) return;  // upper tiles only; mirrored in the epilogue
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, r = lane >> 2, kq = lane & 3;
+    const int wm = w & 1, wn = w >> 1;
+    const int64_t row0 = static_cast<int64_t>(ti) * ST, col0 = static_cast<int64_t>(tj) * ST;
+    const double* Bm = kind == KIND_SYRK ? A : B;
+    const int64_t ldbm = kind == KIND_SYRK ? lda : ldb;
+    double acc[4][4][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    for (int64_t k0 = 0; k0 < K; k0 += SK) {
+        // A chunk -> As[k][m]: NN reads A[m + k lda] (m fastest), TN / SYRK A[k + m lda] (k fastest)
+#pragma unroll
+        for (int it = 0; it < SK * ST / 128; ++it) {
+            const int e = tid + it * 128;
+            int kk, mm;
+            if (kind == KIND_NN) {
+                mm = e % ST;
+                kk = e / ST;
+            } else {
+                kk = e % SK;
+                mm = e / SK;
+            }
+            const int64_t gm = row0 + mm, gk = k0 + kk;
+            double v = 0.0;
+            if (gm < M && gk < K) v = kind == KIND_NN ? A[gm + gk * lda] : A[gk + gm * lda];
+            As[kk][mm] = v;
+            const int64_t gn = col0 + e / SK;
+            const int kb = e % SK;
+            double u = 0.0;
+            if (gn < N && k0 + kb < K) u = Bm[(k0 + kb) + gn * ldbm];
+            Bs[kb][e / SK] = u;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int ks = 0; ks < SK / 4; ++ks) {
+            double af[4], bf[4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) af[a] = As[4 * ks + kq][32 * wm + 8 * a + r];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) bf[b] = Bs[4 * ks + kq][32 * wn + 8 * b + r];
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const int64_t row = row0 + 32 * wm + 8 * a + r, col = col0 + 32 * wn + 8 * b + 2 * kq + i;
+                if (row >= M || col >= N) continue;
+                double v = acc[a][b][i];
+                if (kind == KIND_SYRK) {
+                    if (row > col) continue;  // one value per mirror pair -> exact symmetry
+                    if (alpha != 1.0) v *= alpha;
+                    if (beta_one) v += C[row + col * ldc];
+                    C[row + col * ldc] = v;
+                    C[col + row * ldc] = v;
+                    continue;
+                }
+                if (flag && !isfinite(v)) atomicOr(flag, 1);
+                if (col_scale) v *= col_scale[col];
+                if (alpha != 1.0) v *= alpha;
+                if (beta_one) v += C[row + col * ldc];
+                C[row + col * ldc] = v;
+            }
+}
+
+// Small-K problems go to gemm_small_kernel (measured: see DESIGN 3.3).
+bool small_k(int64_t m, int64_t n, int64_t k) {
+    static const bool on = [] {
+        const char* e = std::getenv("SVDK_SMALL_GEMM");
+        return !(e && e[0] == '0');
+    }();
+    return on && k <= 128 && m * n <= (int64_t{1} << 22);
+}
+
+void launch_small(Ctx* c, int kind, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
+                  const double* B, int64_t ldb, double* C, int64_t ldc, double alpha, bool beta_one,
+                  const double* col_scale, int* flag) {
+    const int tiles_m = static_cast<int>(ceil_div(M, ST)), tiles_n = static_cast<int>(ceil_div(N, ST));
+    const double flops = kind == KIND_SYRK ? static_cast<double>(K) * M * (M + 1) : 2.0 * M * N * K;
+    const double bytes = kind == KIND_SYRK ? 8.0 * (K * M + M * M) : 8.0 * (M * K + K * N + M * N);
+    PhaseTimer timer(c, "dmma_gemm", flops, bytes);
+    gemm_small_kernel<<<tiles_m * tiles_n, 128, 0, c->stream>>>(kind, M, N, K, A, lda, B, ldb, C, ldc, alpha,
+                                                                beta_one ? 1 : 0, col_scale, flag, tiles_n);
+    SVDK_CHECK_LAUNCH();
+    c->launches++;
+}
+
 }  // namespace
 
 CUtensorMap tensor_map_2d(const double* base, int64_t rows, int64_t cols, int64_t ld, uint32_t box0,
@@ -455,6 +568,10 @@ void syrk(Ctx* c, int64_t m, int64_t n, const double* A, int64_t lda, double* G,
     if (m == 0) {
         if (!beta_one)
             for (int64_t j = 0; j < n; ++j) fill(c, G + j * ldg, n, 0.0);
+        return;
+    }
+    if (small_k(n, n, m)) {
+        launch_small(c, KIND_SYRK, n, n, m, A, lda, nullptr, 0, G, ldg, alpha, beta_one, nullptr, nullptr);
         return;
     }
     DBuf padded;
@@ -492,6 +609,11 @@ void gemm(Ctx* c, bool transa, int64_t m, int64_t n, int64_t k, const double* A,
     if (k == 0) {
         if (!beta_one)
             for (int64_t j = 0; j < n; ++j) fill(c, C + j * ldc, m, 0.0);
+        return;
+    }
+    if (!b_upper && small_k(m, n, k)) {
+        launch_small(c, transa ? KIND_TN : KIND_NN, m, n, k, A, lda, B, ldb, C, ldc, alpha, beta_one, col_scale,
+                     nonfinite_check ? c->d_flags : nullptr);
         return;
     }
     DBuf pa, pb;
