@@ -980,11 +980,23 @@ bool sweep_loop_graph(Ctx* c, Enqueue&& enqueue_sweep, const double* A, int64_t 
         return false;
     }
     cudaGraph_t body = cp.conditional.phGraph_out[0];
-    SVDK_CUDA(cudaStreamBeginCaptureToGraph(S, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-    enqueue_sweep();
-    jacobi_sumsq_kernel<<<blocks, 256, 0, S>>>(A, n_pad, 1, partial);
-    jacobi_decide_kernel<<<1, 32, 0, S>>>(h, partial, blocks, thr, max_sweeps, state);
+    if (cudaStreamBeginCaptureToGraph(S, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) !=
+        cudaSuccess) {
+        cudaGetLastError();
+        cudaGraphDestroy(outer);
+        return false;
+    }
     cudaGraph_t captured = nullptr;
+    try {
+        enqueue_sweep();
+        jacobi_sumsq_kernel<<<blocks, 256, 0, S>>>(A, n_pad, 1, partial);
+        jacobi_decide_kernel<<<1, 32, 0, S>>>(h, partial, blocks, thr, max_sweeps, state);
+    } catch (...) {  // leave the stream out of capture mode
+        cudaStreamEndCapture(S, &captured);
+        cudaGetLastError();
+        cudaGraphDestroy(outer);
+        throw;
+    }
     SVDK_CUDA(cudaStreamEndCapture(S, &captured));
     const cudaError_t ie = cudaGraphInstantiate(&exec, outer, 0);
     cudaGraphDestroy(outer);
