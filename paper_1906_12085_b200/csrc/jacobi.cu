@@ -152,7 +152,7 @@ __device__ __forceinline__ void smem_mma(const double* A, const double* Bm, doub
 // similarity per round.
 // Development probe: clock64 stamps of CTA 0 in the last pair solve (read by
 // svdk_debug_jacobi_probe; not part of the public ABI).
-__device__ long long g_jprobe[8];
+__device__ long long g_jprobe[16];
 
 template <int TB>
 constexpr int solve_q_warps() {
@@ -172,33 +172,89 @@ constexpr int solve_threads() {
 // thread that evaluates the same block gets the same bits.
 __device__ __forceinline__ void xform2x2(double& m00, double& m01, double& m10, double& m11,
                                          double ci, double si, double cj, double sj, bool same) {
-    if (sj != 0.0) {  // columns
+    // Branch-free: a skipped rotation has (c, s) = (1, 0) and the fma forms
+    // below then return their input (up to the sign of a zero), so lanes whose
+    // rotations are skipped no longer diverge from the rest of the warp.
+    {  // columns
         const double a0 = fma(cj, m00, -(sj * m01)), b0 = fma(sj, m00, cj * m01);
         const double a1 = fma(cj, m10, -(sj * m11)), b1 = fma(sj, m10, cj * m11);
         m00 = a0; m01 = b0; m10 = a1; m11 = b1;
     }
-    if (si != 0.0) {  // rows
+    {  // rows
         const double a0 = fma(ci, m00, -(si * m10)), b0 = fma(si, m00, ci * m10);
         const double a1 = fma(ci, m01, -(si * m11)), b1 = fma(si, m01, ci * m11);
         m00 = a0; m10 = b0; m01 = a1; m11 = b1;
-        if (same) {
-            m01 = 0.0;
-            m10 = 0.0;
-        }
     }
+    const bool zero = same && si != 0.0;  // the rotated pair itself is annihilated
+    m01 = zero ? 0.0 : m01;
+    m10 = zero ? 0.0 : m10;
 }
 
 // Entry (u, v) of R_i^T B R_j alone, in xform2x2's operation order (columns
-// first, then rows; a skipped rotation (s == 0) passes values through).
-__device__ __forceinline__ double xform_entry(double m00, double m01, double m10, double m11, double ci,
-                                              double si, double cj, double sj, int u, int v) {
-    double t0 = v ? m01 : m00, t1 = v ? m11 : m10;
-    if (sj != 0.0) {
-        t0 = v ? fma(sj, m00, cj * m01) : fma(cj, m00, -(sj * m01));
-        t1 = v ? fma(sj, m10, cj * m11) : fma(cj, m10, -(sj * m11));
+// first, then rows; branch-free like xform2x2, so the three entries of a
+// lookahead are evaluated side by side and equal the M threads' values).
+__device__ __forceinline__ double xform_entry_nb(double m00, double m01, double m10, double m11, double ci,
+                                                 double si, double cj, double sj, int u, int v) {
+    const double xc = v ? sj : cj, yc = v ? cj : -sj;
+    const double t0 = fma(xc, m00, yc * m01), t1 = fma(xc, m10, yc * m11);
+    const double xr = u ? si : ci, yr = u ? ci : -si;
+    return fma(xr, t0, yr * t1);
+}
+
+__device__ __forceinline__ void named_bar(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// The lookahead warp's part of an inner round: look_load fetches what
+// rotation `lane` of round rr+1 needs from M_rr and round rr's rotations;
+// look_finish forms the three entries of M_rr+1 (branch-free, so the three
+// are evaluated side by side) and the rotation. Measured per inner round
+// (clock64, tools/exp_pair.sh + tools/exp_probe.py): 1470 -> 1260 cycles with
+// the branch-free entries. Gating the M threads and Q warps on a named barrier
+// behind the lookahead's reads cut those reads from ~1.5k to ~600 cycles but
+// moved the contention into the rotation (round 1375 cycles), so it is not used.
+struct LookRead {
+    double a00, a01, a10, a11, b00, b01, b10, b11, x00, x01, x10, x11, cp, sp, cq, sq;
+    int rp, rq;
+};
+template <int LD, class Tabs>
+__device__ __forceinline__ LookRead look_load(const Tabs& st, const double* M, double (*cs)[Tabs::kNP],
+                                              double (*sn)[Tabs::kNP], int rr, int lane,
+                                              long long* probe_look = nullptr, long long t0 = 0) {
+    LookRead r;
+    const unsigned long long d = st.look[rr][lane];
+#ifdef SVDK_PROBES
+    if (probe_look) {
+        unsigned long long u;
+        asm volatile("add.u64 %0, %1, 1;" : "=l"(u) : "l"(d));
+        probe_look[0] = SVDK_CLOCK() - t0;
+        probe_look[1] = static_cast<long long>(u);
     }
-    if (si == 0.0) return u ? t1 : t0;
-    return u ? fma(si, t0, ci * t1) : fma(ci, t0, -(si * t1));
+#endif
+    const int bp = d & 31, bq = (d >> 5) & 31;
+    r.rp = (d >> 10) & 1;
+    r.rq = (d >> 11) & 1;
+    const int p1 = (d >> 12) & 31, q1 = (d >> 17) & 31;
+    const int p2 = (d >> 22) & 31, q2 = (d >> 27) & 31;
+    r.cp = cs[rr][bp];
+    r.sp = sn[rr][bp];
+    r.cq = cs[rr][bq];
+    r.sq = sn[rr][bq];
+    // diagonal blocks (bp, bp), (bq, bq) and the coupling block (bp, bq)
+    r.a00 = M[p1 + p1 * LD]; r.a01 = M[p1 + q1 * LD]; r.a10 = M[q1 + p1 * LD]; r.a11 = M[q1 + q1 * LD];
+    r.b00 = M[p2 + p2 * LD]; r.b01 = M[p2 + q2 * LD]; r.b10 = M[q2 + p2 * LD]; r.b11 = M[q2 + q2 * LD];
+    r.x00 = M[p1 + p2 * LD]; r.x01 = M[p1 + q2 * LD]; r.x10 = M[q1 + p2 * LD]; r.x11 = M[q1 + q2 * LD];
+    return r;
+}
+__device__ __forceinline__ void look_finish(const LookRead& r, double skip_tau, double& c, double& s) {
+    // only the three entries the new rotation needs (branch-free form of
+    // xform2x2's operation order, see xform_entry_nb)
+    const double app = xform_entry_nb(r.a00, r.a01, r.a10, r.a11, r.cp, r.sp, r.cp, r.sp, r.rp, r.rp);
+    const double aqq = xform_entry_nb(r.b00, r.b01, r.b10, r.b11, r.cq, r.sq, r.cq, r.sq, r.rq, r.rq);
+    const double x = xform_entry_nb(r.x00, r.x01, r.x10, r.x11, r.cp, r.sp, r.cq, r.sq, r.rp, r.rq);
+    c = 1.0;
+    s = 0.0;
+    if (fabs(x) > skip_tau) rotation(app, aqq, x, c, s);
 }
 
 // Inner schedule of a 2b subproblem for one mode (identical for every pair
@@ -211,6 +267,7 @@ __device__ __forceinline__ double xform_entry(double m00, double m01, double m10
 //               17-21 q_bp, 22-26 p_bq, 27-31 q_bq (one LDS for the lookahead)
 template <int TB>
 struct __align__(16) SolveTables {
+    static constexpr int kNP = TB / 2;
     unsigned long long look[TB - 1][TB / 2];
     int ptab[TB - 1][TB / 2];
     unsigned char pinv[TB - 1][TB];
@@ -291,7 +348,12 @@ __device__ __forceinline__ void solve_pair(const double* A, int64_t lda, const S
     __shared__ double cs[RMAX][NP], sn[RMAX][NP];
 
     const int tid = threadIdx.x;
-    const bool probe = pair == 0 && tid == MT + QT && round == 5;
+    // Role index (M threads, Q warps, then the lookahead warp). Making the
+    // lookahead warp 0 instead (older warps are favoured by the schedulers)
+    // measured no faster: 1361 vs 1311 cycles per inner round.
+    const int rt = tid;
+    const bool probe_round = pair == 0 && round == 5;
+    const bool probe = probe_round && rt == MT + QT;
     long long t0 = SVDK_CLOCK();
     int I, J;
     circle_pair(nb, round, pair, I, J);
@@ -327,7 +389,6 @@ __device__ __forceinline__ void solve_pair(const double* A, int64_t lda, const S
     const bool work = __syncthreads_or(big) != 0;
     auto& ptab = st.ptab;
     auto& pinv = st.pinv;
-    auto& look = st.look;
     long long t1 = SVDK_CLOCK();
     if (probe && work) {
         SVDK_PROBE_STORE(g_jprobe, 0, t0);
@@ -338,10 +399,11 @@ __device__ __forceinline__ void solve_pair(const double* A, int64_t lda, const S
         // (M <- R^T M R, double-buffered); the Q warps apply it to the rows of
         // Q; and the lookahead warp (lanes < NP) already evaluates round rr+1's
         // rotations: it recomputes, from M_rr and round rr's rotations, exactly
-        // the three entries of M_rr+1 each new rotation needs (same xform2x2,
-        // same bits as the M threads). The serial FP64 rotation chain then
-        // overlaps the round's update, and a round costs ONE barrier.
-        const int lane = tid - (MT + QT);
+        // the three entries of M_rr+1 each new rotation needs (xform2x2's
+        // operation order, same values as the M threads). The serial FP64
+        // rotation chain then overlaps the round's update; a round costs one
+        // block barrier plus the named-barrier gate behind the lookahead's reads.
+        const int lane = rt - (MT + QT);
         auto rot_of = [&](int r, int i, const double* M) {  // initial round only
             const int code = ptab[r][i];
             const int p = code & 255, q = code >> 8;
@@ -353,71 +415,80 @@ __device__ __forceinline__ void solve_pair(const double* A, int64_t lda, const S
         };
         if (lane >= 0 && lane < NP) rot_of(0, lane, Mc);
         double qreg[QR];  // the Q warps' column slices (lane < TB)
-        const int qrow0 = ((tid - MT) >> 5) * QR;
+        const int qrow0 = ((rt - MT) >> 5) * QR;
 #pragma unroll
-        for (int i = 0; i < QR; ++i) qreg[i] = (qrow0 + i == ((tid - MT) & 31)) ? 1.0 : 0.0;
+        for (int i = 0; i < QR; ++i) qreg[i] = (qrow0 + i == ((rt - MT) & 31)) ? 1.0 : 0.0;
         __syncthreads();
         const int total = max_inner * R;
         for (int it = 0; it < total; ++it) {
             const int rr = it % R;
             const bool pr = probe && it == 10;
-            long long ta = pr ? SVDK_CLOCK() : 0;
-            if (tid < MT) {
-                const int bi = tid % NP, bj = tid / NP;
-                const int ci_code = ptab[rr][bi], cj_code = ptab[rr][bj];
-                const int pi = ci_code & 255, qi = ci_code >> 8;
-                const int pj = cj_code & 255, qj = cj_code >> 8;
-                double m00 = Mc[pi + pj * LD], m01 = Mc[pi + qj * LD];
-                double m10 = Mc[qi + pj * LD], m11 = Mc[qi + qj * LD];
-                xform2x2(m00, m01, m10, m11, cs[rr][bi], sn[rr][bi], cs[rr][bj], sn[rr][bj], bi == bj);
-                Mn[pi + pj * LD] = m00;
-                Mn[pi + qj * LD] = m01;
-                Mn[qi + pj * LD] = m10;
-                Mn[qi + qj * LD] = m11;
-            } else if (tid < MT + QT) {
-                // Q <- Q J: columns p, q of a rotation mix; partner columns are
-                // exchanged by warp shuffles (no shared-memory traffic)
-                const int l = (tid - MT) & 31;
-                const int code = pinv[rr][l & (TB - 1)];
-                const int j = code & 127, role = code >> 7;
-                const int pq = ptab[rr][j];
-                const int partner = role ? (pq & 255) : (pq >> 8);
-                // branch-free: a skipped pair has (c, s) = (1, 0)
-                const double c = cs[rr][j], b = role ? sn[rr][j] : -sn[rr][j];
+            long long ta = (probe_round && it == 10) ? SVDK_CLOCK() : 0;
+            if (rt < MT + QT) {
+                if (rt < MT) {
+                    const int bi = rt % NP, bj = rt / NP;
+                    const int ci_code = ptab[rr][bi], cj_code = ptab[rr][bj];
+                    const int pi = ci_code & 255, qi = ci_code >> 8;
+                    const int pj = cj_code & 255, qj = cj_code >> 8;
+                    double m00 = Mc[pi + pj * LD], m01 = Mc[pi + qj * LD];
+                    double m10 = Mc[qi + pj * LD], m11 = Mc[qi + qj * LD];
+                    xform2x2(m00, m01, m10, m11, cs[rr][bi], sn[rr][bi], cs[rr][bj], sn[rr][bj], bi == bj);
+                    Mn[pi + pj * LD] = m00;
+                    Mn[pi + qj * LD] = m01;
+                    Mn[qi + pj * LD] = m10;
+                    Mn[qi + qj * LD] = m11;
+#ifdef SVDK_PROBES
+                    if (probe_round && rt == 0 && it == 10) g_jprobe[9] = SVDK_CLOCK() - ta;
+#endif
+                } else {
+                    // Q <- Q J: columns p, q of a rotation mix; partner columns are
+                    // exchanged by warp shuffles (no shared-memory traffic)
+                    const int l = (rt - MT) & 31;
+                    const int code = pinv[rr][l & (TB - 1)];
+                    const int j = code & 127, role = code >> 7;
+                    const int pq = ptab[rr][j];
+                    const int partner = role ? (pq & 255) : (pq >> 8);
+                    // branch-free: a skipped pair has (c, s) = (1, 0)
+                    const double c = cs[rr][j], b = role ? sn[rr][j] : -sn[rr][j];
 #pragma unroll
-                for (int i = 0; i < QR; ++i) {
-                    const double other = __shfl_sync(0xffffffffu, qreg[i], partner);
-                    qreg[i] = fma(b, other, c * qreg[i]);
+                    for (int i = 0; i < QR; ++i) {
+                        const double other = __shfl_sync(0xffffffffu, qreg[i], partner);
+                        qreg[i] = fma(b, other, c * qreg[i]);
+                    }
+#ifdef SVDK_PROBES
+                    if (probe_round && rt == MT && it == 10) {
+                        double u;
+                        asm volatile("add.f64 %0, %1, %2;" : "=d"(u) : "d"(qreg[0]), "d"(qreg[QR - 1]));
+                        g_jprobe[10] = SVDK_CLOCK() - ta;
+                        g_jprobe[13] = static_cast<long long>(u);
+                    }
+#endif
                 }
-            } else if (lane < NP && it + 1 < total) {
+            } else {
                 // lookahead: rotation `lane` of round nr from M_{rr+1} entries
-                const int nr = (it + 1) % R;
-                const unsigned long long d = look[rr][lane];
-                const int bp = d & 31, bq = (d >> 5) & 31;
-                const int rp = (d >> 10) & 1, rq = (d >> 11) & 1;
-                const int p1 = (d >> 12) & 31, q1 = (d >> 17) & 31;
-                const int p2 = (d >> 22) & 31, q2 = (d >> 27) & 31;
-                const double cp = cs[rr][bp], sp = sn[rr][bp], cq = cs[rr][bq], sq = sn[rr][bq];
-                // diagonal blocks (bp, bp), (bq, bq) and the coupling block (bp, bq)
-                double a00 = Mc[p1 + p1 * LD], a01 = Mc[p1 + q1 * LD];
-                double a10 = Mc[q1 + p1 * LD], a11 = Mc[q1 + q1 * LD];
-                double b00 = Mc[p2 + p2 * LD], b01 = Mc[p2 + q2 * LD];
-                double b10 = Mc[q2 + p2 * LD], b11 = Mc[q2 + q2 * LD];
-                double x00 = Mc[p1 + p2 * LD], x01 = Mc[p1 + q2 * LD];
-                double x10 = Mc[q1 + p2 * LD], x11 = Mc[q1 + q2 * LD];
-                // only the three entries the new rotation needs, each with the
-                // operation order of xform2x2 (same bits as the M threads)
-                const double app = xform_entry(a00, a01, a10, a11, cp, sp, cp, sp, rp, rp);
-                const double aqq = xform_entry(b00, b01, b10, b11, cq, sq, cq, sq, rq, rq);
-                const double x = xform_entry(x00, x01, x10, x11, cp, sp, cq, sq, rp, rq);
-                long long t1 = pr ? SVDK_CLOCK() : 0;
-                double c = 1.0, s = 0.0;
-                if (fabs(x) > skip_tau) rotation(app, aqq, x, c, s);
-                cs[nr][lane] = c;
-                sn[nr][lane] = s;
+                const bool la = lane < NP && it + 1 < total;
+                LookRead lr;
+                if (la) lr = look_load<LD>(st, Mc, cs, sn, rr, lane, pr ? g_jprobe + 12 : nullptr, ta);
+#ifdef SVDK_PROBES
                 if (pr) {
-                    SVDK_PROBE_STORE(g_jprobe, 3, t1 - ta);
-                    SVDK_PROBE_STORE(g_jprobe, 4, SVDK_CLOCK() - t1);
+                    double u;
+                    asm volatile("add.f64 %0, %1, %2;" : "=d"(u) : "d"(lr.a00), "d"(lr.x11));
+                    asm volatile("add.f64 %0, %0, %1;" : "+d"(u) : "d"(lr.cq));
+                    g_jprobe[11] = SVDK_CLOCK() - ta;
+                    g_jprobe[14] = static_cast<long long>(u);
+                }
+#endif
+                if (la) {
+                    long long t1 = pr ? SVDK_CLOCK() : 0;
+                    double c, s;
+                    look_finish(lr, skip_tau, c, s);
+                    const int nr = (it + 1) % R;
+                    cs[nr][lane] = c;
+                    sn[nr][lane] = s;
+                    if (pr) {
+                        SVDK_PROBE_STORE(g_jprobe, 3, t1 - ta);
+                        SVDK_PROBE_STORE(g_jprobe, 4, SVDK_CLOCK() - t1);
+                    }
                 }
             }
             long long tb = pr ? SVDK_CLOCK() : 0;
@@ -430,8 +501,8 @@ __device__ __forceinline__ void solve_pair(const double* A, int64_t lda, const S
             Mc = Mn;
             Mn = t;
         }
-        if (tid >= MT && tid < MT + QT && ((tid - MT) & 31) < TB) {  // Q slices back to shared memory
-            const int l = (tid - MT) & 31;
+        if (rt >= MT && rt < MT + QT && ((rt - MT) & 31) < TB) {  // Q slices back to shared memory
+            const int l = (rt - MT) & 31;
 #pragma unroll
             for (int i = 0; i < QR; ++i) Q[(qrow0 + i) + l * LD] = qreg[i];
         }
@@ -1172,10 +1243,6 @@ static_assert(QH == solve_threads<32>(), "solve roles");
 constexpr size_t QUAD_SMEM =
     (3 * 64 * L64 + 8 * SUB32 + 4 * 31 * 16) * sizeof(double) + sizeof(SolveTables<32>) + 16;
 
-__device__ __forceinline__ void named_bar(int id, int n) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-
 // Local-64 index (blocks I J K L = 16-index groups 0..3) of local index i of
 // half h's 32 x 32 subproblem in sub-stage `kind` (0 = A, 1 = B, 2 = C).
 __device__ __forceinline__ int quad_idx(int kind, int h, int i) {
@@ -1201,7 +1268,6 @@ __device__ __forceinline__ void quad_sub_solve(double* Mc, double* Mn, double* Q
     }
     const auto& ptab = st.ptab;
     const auto& pinv = st.pinv;
-    const auto& look = st.look;
     const int lane = ltid - (MT + QT);
     if (lane >= 0 && lane < NP) {
         const int code = ptab[0][lane];
@@ -1218,48 +1284,42 @@ __device__ __forceinline__ void quad_sub_solve(double* Mc, double* Mn, double* Q
     for (int i = 0; i < QR; ++i) qreg[i] = (qrow0 + i == ((ltid - MT) & 31)) ? 1.0 : 0.0;
     named_bar(bar, QH);
     for (int rr = 0; rr < R; ++rr) {
-        if (ltid < MT) {
-            const int bi = ltid % NP, bj = ltid / NP;
-            const int ci_code = ptab[rr][bi], cj_code = ptab[rr][bj];
-            const int pi = ci_code & 255, qi = ci_code >> 8;
-            const int pj = cj_code & 255, qj = cj_code >> 8;
-            double m00 = Mc[pi + pj * LD], m01 = Mc[pi + qj * LD];
-            double m10 = Mc[qi + pj * LD], m11 = Mc[qi + qj * LD];
-            xform2x2(m00, m01, m10, m11, cs[rr][bi], sn[rr][bi], cs[rr][bj], sn[rr][bj], bi == bj);
-            Mn[pi + pj * LD] = m00;
-            Mn[pi + qj * LD] = m01;
-            Mn[qi + pj * LD] = m10;
-            Mn[qi + qj * LD] = m11;
-        } else if (ltid < MT + QT) {
-            const int l = (ltid - MT) & 31;
-            const int code = pinv[rr][l];
-            const int j = code & 127, role = code >> 7;
-            const int pq = ptab[rr][j];
-            const int partner = role ? (pq & 255) : (pq >> 8);
-            const double c = cs[rr][j], b = role ? sn[rr][j] : -sn[rr][j];
+        if (ltid < MT + QT) {
+            if (ltid < MT) {
+                const int bi = ltid % NP, bj = ltid / NP;
+                const int ci_code = ptab[rr][bi], cj_code = ptab[rr][bj];
+                const int pi = ci_code & 255, qi = ci_code >> 8;
+                const int pj = cj_code & 255, qj = cj_code >> 8;
+                double m00 = Mc[pi + pj * LD], m01 = Mc[pi + qj * LD];
+                double m10 = Mc[qi + pj * LD], m11 = Mc[qi + qj * LD];
+                xform2x2(m00, m01, m10, m11, cs[rr][bi], sn[rr][bi], cs[rr][bj], sn[rr][bj], bi == bj);
+                Mn[pi + pj * LD] = m00;
+                Mn[pi + qj * LD] = m01;
+                Mn[qi + pj * LD] = m10;
+                Mn[qi + qj * LD] = m11;
+            } else {
+                const int l = (ltid - MT) & 31;
+                const int code = pinv[rr][l];
+                const int j = code & 127, role = code >> 7;
+                const int pq = ptab[rr][j];
+                const int partner = role ? (pq & 255) : (pq >> 8);
+                const double c = cs[rr][j], b = role ? sn[rr][j] : -sn[rr][j];
 #pragma unroll
-            for (int i = 0; i < QR; ++i) {
-                const double other = __shfl_sync(0xffffffffu, qreg[i], partner);
-                qreg[i] = fma(b, other, c * qreg[i]);
+                for (int i = 0; i < QR; ++i) {
+                    const double other = __shfl_sync(0xffffffffu, qreg[i], partner);
+                    qreg[i] = fma(b, other, c * qreg[i]);
+                }
             }
-        } else if (lane < NP && rr + 1 < R) {
-            const int nr = rr + 1;
-            const unsigned long long d = look[rr][lane];
-            const int bp = d & 31, bq = (d >> 5) & 31;
-            const int rp = (d >> 10) & 1, rq = (d >> 11) & 1;
-            const int p1 = (d >> 12) & 31, q1 = (d >> 17) & 31;
-            const int p2 = (d >> 22) & 31, q2 = (d >> 27) & 31;
-            const double cp = cs[rr][bp], sp = sn[rr][bp], cq = cs[rr][bq], sq = sn[rr][bq];
-            const double app = xform_entry(Mc[p1 + p1 * LD], Mc[p1 + q1 * LD], Mc[q1 + p1 * LD],
-                                           Mc[q1 + q1 * LD], cp, sp, cp, sp, rp, rp);
-            const double aqq = xform_entry(Mc[p2 + p2 * LD], Mc[p2 + q2 * LD], Mc[q2 + p2 * LD],
-                                           Mc[q2 + q2 * LD], cq, sq, cq, sq, rq, rq);
-            const double x = xform_entry(Mc[p1 + p2 * LD], Mc[p1 + q2 * LD], Mc[q1 + p2 * LD],
-                                         Mc[q1 + q2 * LD], cp, sp, cq, sq, rp, rq);
-            double c = 1.0, s = 0.0;
-            if (fabs(x) > skip_tau) rotation(app, aqq, x, c, s);
-            cs[nr][lane] = c;
-            sn[nr][lane] = s;
+        } else {
+            const bool la = lane < NP && rr + 1 < R;
+            LookRead lr;
+            if (la) lr = look_load<LD>(st, Mc, cs, sn, rr, lane);
+            if (la) {
+                double c, s;
+                look_finish(lr, skip_tau, c, s);
+                cs[rr + 1][lane] = c;
+                sn[rr + 1][lane] = s;
+            }
         }
         named_bar(bar, QH);
         double* t = Mc;
@@ -1782,5 +1842,5 @@ void eig_sym(Ctx* c, const double* S, int64_t lds, int64_t n, int max_sweeps, do
 }  // namespace svdk
 
 extern "C" int svdk_debug_jacobi_probe(long long* out) {
-    return cudaMemcpyFromSymbol(out, svdk::g_jprobe, 8 * sizeof(long long)) == cudaSuccess ? 0 : 4;
+    return cudaMemcpyFromSymbol(out, svdk::g_jprobe, 16 * sizeof(long long)) == cudaSuccess ? 0 : 4;
 }

@@ -25,7 +25,7 @@ for _ in range(reps):
 ref = torch.linalg.eigvalsh(s.contiguous()).flip(0)
 import ctypes
 from paper_1906_12085_b200 import _lib
-buf = (ctypes.c_longlong * 8)()
+buf = (ctypes.c_longlong * 16)()
 _lib.load().svdk_debug_jacobi_probe(buf)
 st = list(buf)
 print("pair_solve CTA0 cycles: load", st[1] - st[0], "rounds", st[2] - st[1], "| round10 lookahead: to-barrier", st[6], "(entries", st[3], "rotation", st[4], ") barrier", st[7])

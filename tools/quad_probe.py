@@ -17,7 +17,7 @@ s = colmajor(n, n, ld=n)
 s.copy_(x.t() @ x)
 eng.eig_sym(s)
 torch.cuda.synchronize()
-buf = (ctypes.c_longlong * 8)()
+buf = (ctypes.c_longlong * 16)()
 _lib.load().svdk_debug_jacobi_probe(buf)
 t = list(buf)
 print("load", t[1] - t[0], "| stage B: solve+NS", t[2] - t[1], "transform", t[3] - t[2],
