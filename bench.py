@@ -12,8 +12,10 @@ SVD -> U back-projection -> K) over the device-resident matrix.
 Multi-GPU (torchrun, one process per GPU): each rank holds its own m-row
 shard (weak scaling); every reduction over rows is an NCCL allreduce inside
 the engine. Timing: CUDA events on the engine's stream, barrier +
-synchronize on both sides, max over ranks. A (>= 1.6 GB) is larger than
-L2, so no explicit flush is needed between steps.
+synchronize on both sides, max over ranks. For A larger than L2 (c2-c5) the
+steps run back to back; c1's A (41 MB) fits in the 126 MB L2, so each step is
+timed by its own events and a 512 MB buffer is written between steps
+(outside the events) to flush L2.
 """
 from __future__ import annotations
 
@@ -328,6 +330,9 @@ def ours(args, cfg):
     torch.cuda.synchronize()
 
     # ---------------- timed region (device-resident A) ----------------
+    l2_bytes = 126 << 20
+    flush_buf = (torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+                 if 8 * m * n < 2 * l2_bytes else None)
     eng.ctx.set_timing(True)
     eng.ctx.timing_reset()
     clk_path = tempfile.NamedTemporaryFile(suffix=".csv", delete=False).name
@@ -335,16 +340,25 @@ def ours(args, cfg):
     l0 = eng.launches()
     barrier()
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(eng.stream)
-    for _ in range(args.steps):
-        out = step()
-    e1.record(eng.stream)
+    if flush_buf is None:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(eng.stream)
+        for _ in range(args.steps):
+            out = step()
+        e1.record(eng.stream)
+    else:
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.steps)]
+        for a, b in ev:
+            flush_buf.fill_(1.0)  # evict A (and everything else) from L2, untimed
+            a.record(eng.stream)
+            out = step()
+            b.record(eng.stream)
     torch.cuda.synchronize()
     barrier()
     launches = eng.launches() - l0
     clocks = clocks_sampler_stop(clk, clk_path, local) if rank == 0 else None
-    ms = e0.elapsed_time(e1)
+    ms = e0.elapsed_time(e1) if flush_buf is None else sum(a.elapsed_time(b) for a, b in ev)
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -358,6 +372,9 @@ def ours(args, cfg):
 
     # ---------------- e2e: host buffers through the C-ABI ----------------
     e2e_bytes_in = 8 * m * n
+    # short steps (c1: ~4 ms) are timed over enough calls (>= ~0.25 s) that host
+    # jitter on the box does not dominate the wall-clock mean
+    e2e_steps = max(args.steps, min(100, int(250.0 / max(ms_step, 1e-3))))
     width = {"randomized": cfg["l"]}.get(cfg["method"], n)
     result = {"rank": out.rank, "K": out.k, "total_variance": out.total}
     if world == 1:
@@ -382,10 +399,10 @@ def ours(args, cfg):
         e2e_step()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        for _ in range(args.steps):
+        for _ in range(e2e_steps):
             e2e_step()
         torch.cuda.synchronize()
-        e2e_sec = (time.perf_counter() - t0) / args.steps
+        e2e_sec = (time.perf_counter() - t0) / e2e_steps
         e2e_out = 8 * (n * rank_c.value + rank_c.value + n)
         e2e_k = kk.value
     else:
@@ -407,11 +424,11 @@ def ours(args, cfg):
         torch.cuda.synchronize()
         barrier()
         t0 = time.perf_counter()
-        for _ in range(args.steps):
+        for _ in range(e2e_steps):
             o = e2e_step()
         torch.cuda.synchronize()
         barrier()
-        tt = torch.tensor([(time.perf_counter() - t0) / args.steps], dtype=torch.float64, device="cuda")
+        tt = torch.tensor([(time.perf_counter() - t0) / e2e_steps], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_sec = float(tt.item())
         e2e_out = 8 * (n * o.rank + o.rank)
@@ -497,12 +514,14 @@ def ours(args, cfg):
             "data": "synthetic: seeded low-rank + Gaussian noise generator of SURVEY 8d, column-centred",
             "config": {"workload": cfg["desc"], "m_per_gpu": m, "n": n, "method": cfg["method"], "l": cfg["l"],
                        "q": cfg["q"], "threshold": cfg["t"], "parallelism": f"dp{world} (row shards, NCCL allreduce)",
-                       "l2": "no flush: A is larger than the 126 MB L2"},
+                       "l2": "no flush: A is larger than the 126 MB L2" if flush_buf is None
+                       else "A fits in L2: 512 MB buffer written between steps, each step timed by its own events"},
             "pipeline_tflops": flops / (ms_step / 1e3) / 1e12,
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "rows/s", "h2d_bytes_per_step": e2e_bytes_in,
-                    "d2h_bytes_per_step": e2e_out, "path": "svdk_fit_pca + svdk_select_components (host buffers)"
+                    "d2h_bytes_per_step": e2e_out, "steps": e2e_steps,
+                    "path": "svdk_fit_pca + svdk_select_components (host buffers)"
                     if world == 1 else "H2D shard + svdk_dev_pca + D2H basis/sigma"},
             "gpu_launches": launches,
             "clocks": clocks,
