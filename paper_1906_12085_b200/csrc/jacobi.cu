@@ -742,6 +742,159 @@ __device__ __forceinline__ void upd_a_unit(double* A, int64_t lda, const double*
     }
 }
 
+// The same unit with both contractions re-indexed so that no data crosses
+// lanes and every operand load is a vector load (one warp per unit):
+//   step 1, U = Q_p^T X: k-step s takes contraction index
+//     k1(s, kq) = 16 (s >> 2) + 4 kq + (s & 3)
+//   so lane (r, kq) needs rows 16h + 4kq .. +3 of a column of Q_p and of X for
+//   the four k-steps of half h: one 32-byte load each (8 + 8 instead of
+//   32 + 32 scalar loads);
+//   step 2, X' = U Q_q: k-step s takes k2(s, kq) = 8 (s >> 1) + 2 kq + (s & 1),
+//   which is exactly the column of U that lane (r, kq) already holds in
+//   accumulator acc[m][s >> 1][s & 1] (C layout C[r][2 kq + i]), so the 64
+//   quad shuffles of upd_a_unit disappear; Q_q is read as 16-byte row pairs.
+// The contraction order differs from upd_a_unit (a permutation of k), so the
+// results differ from it by rounding only. The mirror block is written with
+// 16-byte stores (rows 2kq, 2kq+1 of a column).
+__device__ __forceinline__ double2 ld_cg2(const double* p) {
+    double2 v;
+    asm volatile("ld.global.cg.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void st2(double* p, double a, double b) {
+    asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(a), "d"(b) : "memory");
+}
+
+// MS warps share a unit (MS = 1, 2, 4): warp `part` forms the rows
+// [32 part / MS, 32 (part + 1) / MS) of X' (its rows of U stay in its own
+// accumulators) and reads all of X and Q_q; the warps of a CTA meet at a
+// barrier between the last read of X and the first store.
+template <int MS>
+__device__ __forceinline__ void upd_a_unit_vec(double* A, int64_t lda, const double* Qbuf,
+                                               const int* active, int nb, int round, int u, int part) {
+    constexpr int B = 16, MW = 4 / MS;  // m-tiles (8 rows each) per warp
+    const int lane = threadIdx.x & 31, r = lane >> 2, kq = lane & 3;
+    const int k = nb / 2;
+    bool live = u < k * (k + 1) / 2;
+    int p = 0, q = 0;
+    if (live) {
+        q = static_cast<int>((sqrt(8.0 * u + 1.0) - 1.0) * 0.5);
+        while ((q + 1) * (q + 2) / 2 <= u) ++q;
+        while (q * (q + 1) / 2 > u) --q;
+        p = u - q * (q + 1) / 2;
+    }
+    const bool ap = live && __ldcg(&active[p]) != 0, aq = live && __ldcg(&active[q]) != 0;
+    live = live && (ap | aq);  // both rotations the identity: nothing to do
+    int Ip, Jp, Iq, Jq;
+    circle_pair(nb, round, p, Ip, Jp);
+    circle_pair(nb, round, q, Iq, Jq);
+    const double* Qa = Qbuf + static_cast<size_t>(p) * 1024;
+    const double* Qb = Qbuf + static_cast<size_t>(q) * 1024;
+    const int m0 = part * MW;
+    double out[MW][4][2];
+    if (live) {
+        // global row of local index 16h + 4kq (h = 0: block I_p, 1: J_p) and
+        // global column of local index 8t + r
+        const int64_t rowh[2] = {static_cast<int64_t>(Ip) * B + 4 * kq, static_cast<int64_t>(Jp) * B + 4 * kq};
+        int64_t colt[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) colt[t] = gidx(B, Iq, Jq, 8 * t + r);
+        double4 xv[2][4], qa[2][MW];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+#pragma unroll
+            for (int t = 0; t < 4; ++t) xv[h][t] = ld_cg4(A + rowh[h] + colt[t] * lda);
+#pragma unroll
+            for (int m = 0; m < MW; ++m) {
+                // Q_p[16h + 4kq + j][8(m0 + m) + r]; identity when inactive
+                const int k0 = 16 * h + 4 * kq, c = 8 * (m0 + m) + r;
+                qa[h][m] = ap ? ld_cg4(Qa + k0 + c * 32)
+                              : make_double4(k0 == c, k0 + 1 == c, k0 + 2 == c, k0 + 3 == c);
+            }
+        }
+        double2 qb[4][4];  // Q_q[8a + 2kq + {0,1}][8t + r]
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const int k0 = 8 * a + 2 * kq, c = 8 * t + r;
+                qb[a][t] = aq ? ld_cg2(Qb + k0 + c * 32) : make_double2(k0 == c, k0 + 1 == c);
+            }
+        double acc[MW][4][2];
+#pragma unroll
+        for (int m = 0; m < MW; ++m)
+#pragma unroll
+            for (int t = 0; t < 4; ++t) acc[m][t][0] = acc[m][t][1] = 0.0;
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+            const int h = s >> 2, j = s & 3;
+#pragma unroll
+            for (int m = 0; m < MW; ++m) {
+                const double4 av = qa[h][m];
+                const double a = j == 0 ? av.x : (j == 1 ? av.y : (j == 2 ? av.z : av.w));
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const double4 bv = xv[h][t];
+                    const double b = j == 0 ? bv.x : (j == 1 ? bv.y : (j == 2 ? bv.z : bv.w));
+                    dmma(acc[m][t][0], acc[m][t][1], a, b);
+                }
+            }
+        }
+#pragma unroll
+        for (int m = 0; m < MW; ++m)
+#pragma unroll
+            for (int t = 0; t < 4; ++t) out[m][t][0] = out[m][t][1] = 0.0;
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+            const int a2 = s >> 1, i2 = s & 1;
+#pragma unroll
+            for (int m = 0; m < MW; ++m)
+#pragma unroll
+                for (int t = 0; t < 4; ++t)
+                    dmma(out[m][t][0], out[m][t][1], acc[m][a2][i2], i2 ? qb[a2][t].y : qb[a2][t].x);
+        }
+    }
+    if (MS > 1) __syncthreads();  // every warp of the CTA has read its X
+    if (!live) return;
+    if (p == q) {  // diagonal pair block: upper triangle and its mirror, scalar
+#pragma unroll
+        for (int m = 0; m < MW; ++m) {
+            const int li = 8 * (m0 + m) + r;
+            const int64_t gi = gidx(B, Ip, Jp, li);
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const int lj = 8 * t + 2 * kq + i;
+                    if (li > lj) continue;
+                    const int64_t gj = gidx(B, Iq, Jq, lj);
+                    A[gi + gj * lda] = out[m][t][i];
+                    A[gj + gi * lda] = out[m][t][i];
+                }
+        }
+        return;
+    }
+#pragma unroll
+    for (int m = 0; m < MW; ++m) {
+        const int64_t gi = gidx(B, Ip, Jp, 8 * (m0 + m) + r);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int64_t gj = gidx(B, Iq, Jq, 8 * t + 2 * kq);  // and gj + 1 (same 16-index block)
+            A[gi + gj * lda] = out[m][t][0];
+            A[gi + (gj + 1) * lda] = out[m][t][1];
+            st2(A + gj + gi * lda, out[m][t][0], out[m][t][1]);
+        }
+    }
+}
+
+template <int MS>
+__global__ void __launch_bounds__(UPD_WARPS * 32)
+    jacobi_update_a_vec(double* A, int64_t lda, const double* Qbuf, const int* active, int nb,
+                        int round) {
+    const int w = threadIdx.x >> 5;
+    upd_a_unit_vec<MS>(A, lda, Qbuf, active, nb, round, blockIdx.x * (UPD_WARPS / MS) + w / MS, w % MS);
+}
+
 // The same update split over the four warps of a CTA (one unit per CTA):
 // warp w4 produces rows [8 w4, 8 w4 + 8) of Q_p^T X Q_q. Its rows of
 // U = Q_p^T X stay in its own accumulators, so no data crosses warps; each
@@ -1131,11 +1284,21 @@ void run_sweeps(Ctx* c, double* A, double* V, int64_t n_pad, int max_sweeps, dou
     const char* upd_env = std::getenv("SVDK_JACOBI_UPD");
     const bool reg_upd = TB == 32 && !(upd_env && std::string(upd_env) == "smem");
     const int a_warp_ctas = static_cast<int>(ceil_div(static_cast<int64_t>(a_ctas), UPD_WARPS));
-    // latency-bound rounds (small n): each A block unit split over four warps.
-    // Measured (tools/eig_time.py): n = 256 / 512 3.71 -> 3.36 / 7.25 -> 6.80 ms;
-    // n = 1024 / 2048 17.2 -> 17.7 / 61.2 -> 74.2 ms (4x the warps, more L2 reads)
+    // Default: the vector-load, shuffle-free unit (upd_a_unit_vec) with 2 warps
+    // per unit up to n = 1024 and 1 above. Measured eig(n) in ms, same box
+    // (tools/exp_probe.py; SVDK_JACOBI_AVEC = warps per unit, 0 = upd_a_unit,
+    // SVDK_JACOBI_AQ4=1 = jacobi_update_a_q4):
+    //   n        256   512   1024  2048  3000
+    //   vec x1  3.39  6.97  16.70  54.3   161
+    //   vec x2  3.23  6.28  15.52  59.7   182
+    //   vec x4  3.27  6.40  15.79  56.7   175
+    //   q4      3.23  6.57  17.23
+    //   reg          (1024: 16.62, 2048: 58.6, 3000: 167.7 in another run)
     const char* q4_env = std::getenv("SVDK_JACOBI_AQ4");
-    const bool a_q4 = q4_env ? std::atoi(q4_env) != 0 : n_pad <= 768;
+    const bool a_q4 = q4_env && std::atoi(q4_env) != 0;
+    const char* avec_env = std::getenv("SVDK_JACOBI_AVEC");
+    const int a_vec = avec_env ? std::atoi(avec_env) : (n_pad <= 1024 ? 2 : 1);
+    const int a_ctas2 = static_cast<int>(ceil_div(static_cast<int64_t>(a_ctas), 2));
     const int v_warp_ctas =
         static_cast<int>(ceil_div(ceil_div(n_pad, static_cast<int64_t>(VT_ROWS)) * k, UPD_WARPS));
     auto launch_updates = [&](const double* qr, const int* ar, int r) {
@@ -1143,6 +1306,12 @@ void run_sweeps(Ctx* c, double* A, double* V, int64_t n_pad, int max_sweeps, dou
             jacobi_update_v_reg<<<v_warp_ctas, UPD_WARPS * 32, 0, S2>>>(V, n_pad, n_pad, qr, ar, nb, r);
             if (a_q4)
                 jacobi_update_a_q4<<<a_ctas, 128, 0, S>>>(A, n_pad, qr, ar, nb, r);
+            else if (a_vec == 1)
+                jacobi_update_a_vec<1><<<a_warp_ctas, UPD_WARPS * 32, 0, S>>>(A, n_pad, qr, ar, nb, r);
+            else if (a_vec == 2)
+                jacobi_update_a_vec<2><<<a_ctas2, UPD_WARPS * 32, 0, S>>>(A, n_pad, qr, ar, nb, r);
+            else if (a_vec == 4)
+                jacobi_update_a_vec<4><<<a_ctas, UPD_WARPS * 32, 0, S>>>(A, n_pad, qr, ar, nb, r);
             else
                 jacobi_update_a_reg<<<a_warp_ctas, UPD_WARPS * 32, 0, S>>>(A, n_pad, qr, ar, nb, r);
         } else {
@@ -1615,10 +1784,6 @@ __global__ void __launch_bounds__(A64_THREADS)
 // 8 lanes cover a full 128-byte column run). Four CTAs per SM keep loads of
 // one warp in flight under the DMMAs of the others.
 constexpr int V64_ROWS = 256;
-
-__device__ __forceinline__ double2 ld_cg2(const double* p) {
-    return __ldcg(reinterpret_cast<const double2*>(p));
-}
 
 __global__ void __launch_bounds__(128, 4)
     jacobi_update_v64(double* V, int64_t ldv, int64_t n_rows, const double* Qbuf, const int* active,
