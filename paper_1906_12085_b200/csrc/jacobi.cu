@@ -201,6 +201,25 @@ __device__ __forceinline__ double xform_entry_nb(double m00, double m01, double 
     return fma(xr, t0, yr * t1);
 }
 
+// Programmatic dependent launch (PDL) inside a Jacobi round chain
+// (solve -> A update -> next solve on one stream): the successor is launched
+// with the programmatic-serialisation attribute, so its launch overlaps the
+// predecessor's tail and it runs its independent prologue (the solve's
+// schedule tables) before pdl_wait(), which returns once the predecessor grid
+// has completed and its memory is visible (a no-op without the attribute).
+// An explicit early trigger (griddepcontrol.launch_dependents at kernel
+// start, -DSVDK_PDL_TRIGGER) measured mixed: eig(256) 3.20 -> 3.12 ms and
+// eig(2048) 54.1 -> 50.4 ms, but eig(512) 6.2 -> 7.4 ms and eig(1024) 13.8 ->
+// 16.4 ms (the early-resident waiting CTAs crowd the running grid), so the
+// implicit trigger at grid completion is used. Without PDL: 3.28 / 6.31 /
+// 15.6 / 54.0 ms for n = 256 / 512 / 1024 / 2048.
+__device__ __forceinline__ void pdl_trigger() {
+#ifdef SVDK_PDL_TRIGGER
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ void named_bar(int id, int n) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
@@ -366,8 +385,10 @@ __device__ __forceinline__ void solve_pair(const double* A, int64_t lda, const S
         const uint4* src = reinterpret_cast<const uint4*>(tabs) + static_cast<size_t>(mode) *
                                (sizeof(SolveTables<TB>) / 16);
         uint4* dst = reinterpret_cast<uint4*>(&st);
+        pdl_trigger();
         for (int e = tid; e < static_cast<int>(sizeof(SolveTables<TB>) / 16); e += NT) dst[e] = src[e];
     }
+    pdl_wait();  // A (and the Q / active slots) of the previous round's update
     bool big = false;
     {
         double xv[PER];
@@ -667,6 +688,8 @@ __device__ __forceinline__ void upd_a_unit(double* A, int64_t lda, const double*
     constexpr int B = 16;
     const int lane = threadIdx.x & 31, r = lane >> 2, kq = lane & 3;
     const int k = nb / 2;
+    pdl_trigger();
+    pdl_wait();
     if (u >= k * (k + 1) / 2) return;
     int q = static_cast<int>((sqrt(8.0 * u + 1.0) - 1.0) * 0.5);
     while ((q + 1) * (q + 2) / 2 <= u) ++q;
@@ -775,6 +798,8 @@ __device__ __forceinline__ void upd_a_unit_vec(double* A, int64_t lda, const dou
     constexpr int B = 16, MW = 4 / MS;  // m-tiles (8 rows each) per warp
     const int lane = threadIdx.x & 31, r = lane >> 2, kq = lane & 3;
     const int k = nb / 2;
+    pdl_trigger();
+    pdl_wait();  // Q_p, Q_q and the active flags of this round's solve
     bool live = u < k * (k + 1) / 2;
     int p = 0, q = 0;
     if (live) {
@@ -909,6 +934,8 @@ __global__ void __launch_bounds__(128)
     constexpr int B = 16;
     const int lane = threadIdx.x & 31, r = lane >> 2, kq = lane & 3, w4 = threadIdx.x >> 5;
     const int u = blockIdx.x;
+    pdl_trigger();
+    pdl_wait();
     int q = static_cast<int>((sqrt(8.0 * u + 1.0) - 1.0) * 0.5);
     while ((q + 1) * (q + 2) / 2 <= u) ++q;
     while (q * (q + 1) / 2 > u) --q;
@@ -1301,19 +1328,37 @@ void run_sweeps(Ctx* c, double* A, double* V, int64_t n_pad, int max_sweeps, dou
     const int a_ctas2 = static_cast<int>(ceil_div(static_cast<int64_t>(a_ctas), 2));
     const int v_warp_ctas =
         static_cast<int>(ceil_div(ceil_div(n_pad, static_cast<int64_t>(VT_ROWS)) * k, UPD_WARPS));
+    // Programmatic dependent launches on the solve -> A update -> solve chain
+    // (SVDK_JACOBI_PDL=0: plain launches; see pdl_wait for the measurements).
+    const char* pdl_env = std::getenv("SVDK_JACOBI_PDL");
+    const bool pdl = !(pdl_env && std::atoi(pdl_env) == 0);
+    auto launch = [&](auto kern, int grid, int block, size_t smem, bool prog, auto... args) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(static_cast<unsigned>(grid));
+        cfg.blockDim = dim3(static_cast<unsigned>(block));
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = S;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = (prog && pdl) ? 1 : 0;
+        SVDK_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
+    };
     auto launch_updates = [&](const double* qr, const int* ar, int r) {
         if (reg_upd) {
             jacobi_update_v_reg<<<v_warp_ctas, UPD_WARPS * 32, 0, S2>>>(V, n_pad, n_pad, qr, ar, nb, r);
+            int64_t ld = n_pad;
             if (a_q4)
-                jacobi_update_a_q4<<<a_ctas, 128, 0, S>>>(A, n_pad, qr, ar, nb, r);
+                launch(jacobi_update_a_q4, a_ctas, 128, 0, true, A, ld, qr, ar, nb, r);
             else if (a_vec == 1)
-                jacobi_update_a_vec<1><<<a_warp_ctas, UPD_WARPS * 32, 0, S>>>(A, n_pad, qr, ar, nb, r);
+                launch(jacobi_update_a_vec<1>, a_warp_ctas, UPD_WARPS * 32, 0, true, A, ld, qr, ar, nb, r);
             else if (a_vec == 2)
-                jacobi_update_a_vec<2><<<a_ctas2, UPD_WARPS * 32, 0, S>>>(A, n_pad, qr, ar, nb, r);
+                launch(jacobi_update_a_vec<2>, a_ctas2, UPD_WARPS * 32, 0, true, A, ld, qr, ar, nb, r);
             else if (a_vec == 4)
-                jacobi_update_a_vec<4><<<a_ctas, UPD_WARPS * 32, 0, S>>>(A, n_pad, qr, ar, nb, r);
+                launch(jacobi_update_a_vec<4>, a_ctas, UPD_WARPS * 32, 0, true, A, ld, qr, ar, nb, r);
             else
-                jacobi_update_a_reg<<<a_warp_ctas, UPD_WARPS * 32, 0, S>>>(A, n_pad, qr, ar, nb, r);
+                launch(jacobi_update_a_reg, a_warp_ctas, UPD_WARPS * 32, 0, true, A, ld, qr, ar, nb, r);
         } else {
             jacobi_update_v<TB><<<v_ctas, 256, smem_v, S2>>>(V, n_pad, qr, ar, nb, r);
             jacobi_update_a<TB><<<a_ctas, 256, smem_a, S>>>(A, n_pad, qr, ar, nb, r);
@@ -1325,8 +1370,10 @@ void run_sweeps(Ctx* c, double* A, double* V, int64_t n_pad, int max_sweeps, dou
     SVDK_CHECK_LAUNCH();
     c->launches++;
     auto launch_solve = [&](double* qr, int* ar, int r, int mode) {
-        jacobi_pair_solve<TB><<<k, nthreads_solve, smem_solve, S>>>(A, n_pad, tabs, qr, ar, nb, r,
-                                                                    skip_tau, max_inner, mode);
+        const double* a = A;
+        int64_t ld = n_pad;
+        launch(jacobi_pair_solve<TB>, k, nthreads_solve, smem_solve, true, a, ld, tabs, qr, ar, nb, r,
+               skip_tau, max_inner, mode);
     };
     auto enqueue_sweep = [&] {
         if (split) {  // in-block stage on the round-0 block pairing
