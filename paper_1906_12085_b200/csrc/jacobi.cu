@@ -1616,6 +1616,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1)
     };
     const bool probe = blockIdx.x == 0 && tid == 0 && round == 5;
     if (probe) SVDK_PROBE_STORE(g_jprobe, 0, SVDK_CLOCK());
+    pdl_wait();  // A of the previous round's a64 update (see pdl_trigger)
     for (int e = tid; e < 64 * 64; e += Q_THREADS) {
         const int i = e & 63, j = e >> 6;
         M64[i + j * L64] = __ldcg(&A[g(i) + g(j) * lda]);
@@ -1722,6 +1723,7 @@ __global__ void __launch_bounds__(A64_THREADS)
     double* Qs = sm + 64 * L64;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, r = lane >> 2, kq = lane & 3;
     const int u = blockIdx.x;
+    pdl_wait();  // Q and the active flags of this round's quad solve
     int q = static_cast<int>((sqrt(8.0 * u + 1.0) - 1.0) * 0.5);
     while ((q + 1) * (q + 2) / 2 <= u) ++q;
     while (q * (q + 1) / 2 > u) --q;
@@ -1911,16 +1913,36 @@ void run_sweeps_quad(Ctx* c, double* A, double* V, int64_t n_pad, int max_sweeps
     c->launches++;
     const int a_ctas = ks * (ks + 1) / 2;
     const int v_ctas = static_cast<int>(ceil_div(n_pad, static_cast<int64_t>(V64_ROWS))) * ks;
+    // solve -> a64 -> solve as programmatic dependent launches (see pdl_trigger)
+    const char* pdl_env = std::getenv("SVDK_JACOBI_PDL");
+    const bool pdl = !(pdl_env && std::atoi(pdl_env) == 0);
+    const double* a_in = A;
+    int64_t ld = n_pad;
+    auto launch = [&](auto kern, int grid, int block, size_t smem, auto... args) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(static_cast<unsigned>(grid));
+        cfg.blockDim = dim3(static_cast<unsigned>(block));
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = S;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = pdl ? 1 : 0;
+        SVDK_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
+    };
     auto enqueue_sweep = [&] {
         for (int r = 0; r < rounds; ++r) {
             double* qr = qbuf.p() + static_cast<size_t>(r) * ks * 4096;
             int* ar = active + static_cast<size_t>(r) * ks;
-            jacobi_quad_solve<<<ks, Q_THREADS, QUAD_SMEM, S>>>(A, n_pad, tabs, qr, ar, ns, r, skip_tau,
-                                                              r == 0 ? 1 : 0);
+            launch(jacobi_quad_solve, ks, Q_THREADS, QUAD_SMEM, a_in, ld, tabs, qr, ar, ns, r, skip_tau,
+                   r == 0 ? 1 : 0);
             SVDK_CUDA(cudaEventRecord(c->aux_ev[0], S));
             SVDK_CUDA(cudaStreamWaitEvent(S2, c->aux_ev[0], 0));
             jacobi_update_v64<<<v_ctas, 128, 0, S2>>>(V, n_pad, n_pad, qr, ar, ns, r);
-            jacobi_update_a64<<<a_ctas, A64_THREADS, A64_SMEM, S>>>(A, n_pad, qr, ar, ns, r);
+            const double* qc = qr;
+            const int* ac = ar;
+            launch(jacobi_update_a64, a_ctas, A64_THREADS, A64_SMEM, A, ld, qc, ac, ns, r);
         }
         SVDK_CUDA(cudaEventRecord(c->aux_ev[1], S2));
         SVDK_CUDA(cudaStreamWaitEvent(S, c->aux_ev[1], 0));
