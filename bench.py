@@ -1,21 +1,26 @@
 #!/usr/bin/env python
 """bench.py — PCA throughput of the B200 FP64 engine on BASELINE.json's configs.
 
-Default workload (N=1): config c2 — randomized PCA of a 200000 x 1024 FP64
-matrix (l = min(k + p, n) = 1024, q = 2 power iterations, CholeskyQR2,
-t = 0.99), i.e. BASELINE.json configs[1]. A "step" is one full fit_pca +
-select_components pass (center -> total variance -> range finder -> small
-SVD -> U back-projection -> K) over the device-resident matrix.
+Default workload (N=1): config c4 — BASELINE.json configs[3], the largest
+config and the one north_star's scaling target is quoted on: truncated SVD /
+PCA of an 8388608 x 1024 FP64 matrix (64 GB, fits one 180 GB B200), t = 0.95.
+A "step" is one full fit_pca + select_components pass (centre -> total
+variance -> Gram -> Jacobi eigensolve -> U back-projection -> K) over the
+device-resident matrix. `--config c1|c2|c3|c5` selects the other configs.
 
   python bench.py [--gpus N --steps K --warmup W] [--config c1..c5] [--impl reference]
 
-Multi-GPU (torchrun, one process per GPU): each rank holds its own m-row
-shard (weak scaling); every reduction over rows is an NCCL allreduce inside
-the engine. Timing: CUDA events on the engine's stream, barrier +
-synchronize on both sides, max over ranks. For A larger than L2 (c2-c5) the
-steps run back to back; c1's A (41 MB) fits in the 126 MB L2, so each step is
-timed by its own events and a 512 MB buffer is written between steps
-(outside the events) to flush L2.
+Inputs: the shared seeded generator (paper_1906_12085_b200/synth.py) — the
+same bytes the golden fixtures fed the compiled reference, so the line carries
+a `parity` block against tests/golden/<config>.npz. Multi-GPU (torchrun, one
+process per GPU): c4 is strong-scaled (rank r holds rows [r m/N, (r+1) m/N) of
+the SAME matrix, so K and parity are checked at every N); the other configs
+are weak-scaled (m rows per GPU of an (N m)-row matrix). Every reduction over
+rows is an NCCL allreduce inside the engine. Timing: CUDA events on the
+engine's stream, barrier + synchronize on both sides, max over ranks. For A
+larger than L2 (c2-c5) the steps run back to back; c1's A (41 MB) fits in the
+126 MB L2, so each step is timed by its own events and a 512 MB buffer is
+written between steps (outside the events) to flush L2.
 """
 from __future__ import annotations
 
@@ -32,57 +37,72 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-# measured on this pool's B200s (profiles/fp64_peaks.json): cuBLAS DGEMM
-# 8192^3 sustained 35.4 TF/s (the FP64 roofline denominator, same method as
-# MEASURED_PEAKS.json's bf16 figure) and the raw DMMA pipe 37.0 TF/s.
+from paper_1906_12085_b200 import synth  # noqa: E402
+
+# Fallback FP64 roofline denominator: cuBLAS DGEMM 8192^3 sustained, measured on
+# this pool's B200s in round 1 (profiles/fp64_peaks.json; MEASURED_PEAKS.json has
+# no FP64 entry). Every run re-measures it live (dgemm_peak) and uses that.
 FP64_PEAK_TFLOPS = 35.43
-FP64_PIPE_TFLOPS = 37.0
+FP64_PIPE_TFLOPS = 37.0  # raw DMMA.8x8x4 pipe, tools/probes/fp64_peak.cu
 
 
 def _hbm_peak():
     try:
-        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
     except Exception:
-        return 6650.0  # profiling guide fallback
+        return 6650.0, "fallback 6.65 TB/s of B200_PROFILING.md"
 
 
-HBM_PEAK_GBS = _hbm_peak()
-
-CONFIGS = {
-    "c1": dict(m=20000, n=256, method="truncated", l=0, q=0, t=0.95, spec="c1", noise=1e-3,
-               desc="c1: truncated SVD via Gram, 20000x256, t=0.95"),
-    "c2": dict(m=200000, n=1024, method="randomized", l=1024, q=2, t=0.99, spec="c2", noise=1e-3,
-               desc="c2: randomized PCA 200000x1024, l=min(1024+10,1024), q=2, CholeskyQR2, t=0.99"),
-    "c3": dict(m=500000, n=2048, method="lanczos", l=0, q=0, t=0.95, spec="c3", noise=1e-4,
-               desc="c3: Lanczos on A^T A, 500000x2048, n steps, full reorth, t=0.95"),
-    "c4": dict(m=8388608, n=1024, method="truncated", l=0, q=0, t=0.95, spec="c4", noise=1e-3,
-               desc="c4: row-sharded truncated SVD 8388608x1024 (64 GB), t=0.95"),
-    "c5": dict(m=65536, n=4096, method="truncated", l=0, q=0, t=0.90, spec="c5", noise=1e-2,
-               desc="c5: full-spectrum truncated SVD 65536x4096, t=0.90"),
-}
+HBM_PEAK_GBS, HBM_PEAK_SRC = _hbm_peak()
 METHOD_ID = {"truncated": 0, "randomized": 1, "krylov": 2, "lanczos": 3}
-SPECTRA = {
-    "c1": lambda i: math.exp(-i / 20.0),
-    "c2": lambda i: i ** -1.5,
-    "c3": lambda i: math.exp(-i / 200.0),
-    "c4": lambda i: 1.0 / i,
-    "c5": lambda i: 1.0 / (1.0 + 0.01 * i),
-}
+STRONG = {"c4"}  # north_star: c4 is row-sharded over 1/2/4/8 GPUs (same matrix)
+
+
+def config(name):
+    c = synth.CONFIGS[name]
+    return dict(name=name, m=c.m, n=c.n, method=c.method, l=c.l, q=c.q, t=c.t, sigma=c.sigma, desc=c.desc,
+                strong=name in STRONG)
 
 
 # --------------------------------------------------------------------------- helpers
 def method_flops(cfg, m):
-    """Algorithmic FP64 flops of one pipeline pass (SURVEY 8d counts)."""
+    """Algorithmic FP64 flops of one pipeline pass (SURVEY 8d counts). The
+    sketch route's second CholeskyQR pass is implicit (R2^-1 folded into T and
+    U, DESIGN 3.3), so its Q2 = Q1 R2^-1 TRSM is not counted."""
     n, l, q = cfg["n"], cfg["l"], cfg["q"]
     if cfg["method"] == "truncated":
         return m * n * (n + 1) + 2.0 * m * n * n  # Gram + U = A V
     if cfg["method"] == "randomized":
         gemms = 2.0 * m * n * l * (1 + 2 * q + 1)  # A Omega, q x (A^T Y, A Z), T = A^T Q
-        qr = 2 * (m * l * (l + 1) + m * l * l)    # CholeskyQR2: 2 x (SYRK + TRSM)
-        return gemms + qr + 2.0 * m * l * l       # + U = Q W
+        qr = 2 * m * l * (l + 1) + m * l * l       # CholeskyQR2: 2 SYRK + one TRSM
+        return gemms + qr + 2.0 * m * l * l        # + U = Q W
     if cfg["method"] == "lanczos":
         return 4.0 * m * n * n + 2.0 * m * n * n  # n GEMV pairs + U
     return float("nan")
+
+
+def dgemm_peak(device) -> float:
+    """The FP64 roofline denominator, measured live: cuBLAS DGEMM 8192^3
+    (torch.matmul fp64), best of 5 after a warm-up — the MEASURED_PEAKS.json
+    method, in FP64 (outside every timed region)."""
+    import torch
+    try:
+        a = torch.randn(8192, 8192, dtype=torch.float64, device=device)
+        b = torch.randn(8192, 8192, dtype=torch.float64, device=device)
+        torch.matmul(a, b)
+        best = float("inf")
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch.matmul(a, b)
+            e1.record()
+            e1.synchronize()
+            best = min(best, e0.elapsed_time(e1) / 1e3)
+        del a, b
+        torch.cuda.empty_cache()
+        return 2.0 * 8192 ** 3 / best / 1e12
+    except Exception:
+        return float("nan")
 
 
 def clocks_sampler_start(path):
@@ -124,105 +144,142 @@ def clocks_sampler_stop(proc, path, device):
 
 
 # --------------------------------------------------------------------------- data
-def generate(cfg, m, device, rank, seed=42):
-    """A = U0 diag(s) V0^T + noise N, column-centred: U0 = X R^-1
-    with X Gaussian and R the Cholesky factor of X^T X (CholeskyQR; the Q of
-    X's thin QR), generated in row chunks so only A itself stays resident."""
+def generate(eng, cfg, world, rank):
+    """This rank's rows of the config's A (synth.device_matrix: the generator
+    the golden fixtures were made with). Strong (c4): rows [r m/N, (r+1) m/N)
+    of the m-row matrix. Weak: rows [r m, (r+1) m) of an N m-row matrix. The
+    partial X^T X are allreduced (exact), so every rank builds the same M."""
     import torch
-
-    from paper_1906_12085_b200.engine import colmajor
-    n = cfg["n"]
-    f64 = torch.float64
-    gen = torch.Generator(device=device)
-    chunk = 1 << 17
-
-    def xchunk(c0, rows):
-        gen.manual_seed((seed * 1000003 + rank * 7919 + c0 // chunk) % (2 ** 63))
-        return torch.randn(rows, n, dtype=f64, device=device, generator=gen)
-
-    G = torch.zeros(n, n, dtype=f64, device=device)
-    for c0 in range(0, m, chunk):
-        x = xchunk(c0, min(chunk, m - c0))
-        G += x.T @ x
-    L = torch.linalg.cholesky(G)  # G = L L^T, R = L^T
-    gen.manual_seed(seed + 17)
-    v0, _ = torch.linalg.qr(torch.randn(n, n, dtype=f64, device=device, generator=gen))
-    s = torch.tensor([SPECTRA[cfg["spec"]](i) for i in range(1, n + 1)], dtype=f64, device=device)
-    Mx = torch.linalg.solve_triangular(L.T, s[:, None] * v0.T, upper=True)  # R^-1 S V0^T
-    A = colmajor(m, n, device)
-    noise_gen = torch.Generator(device=device)
-    for c0 in range(0, m, chunk):
-        rows = min(chunk, m - c0)
-        x = xchunk(c0, rows)
-        noise_gen.manual_seed((seed * 31 + rank * 131071 + c0 // chunk + 99991) % (2 ** 63))
-        A[c0:c0 + rows] = x @ Mx + cfg["noise"] * torch.randn(rows, n, dtype=f64, device=device, generator=noise_gen)
-        del x
-    mean = A.sum(0) / m
-    A -= mean
+    import torch.distributed as dist
+    if cfg["strong"]:
+        m_total = cfg["m"]
+        row0, rows = m_total * rank // world, m_total * (rank + 1) // world - m_total * rank // world
+    else:
+        m_total = cfg["m"] * world
+        row0, rows = cfg["m"] * rank, cfg["m"]
+    red = (lambda g: dist.all_reduce(g)) if world > 1 else None
+    c = synth.CONFIGS[cfg["name"]]
+    a = synth.device_matrix(eng, m_total, cfg["n"], c.spectrum(), c.sigma, synth.MATRIX_SEED, row0, rows, red)
     torch.cuda.synchronize()
-    return A
+    return a, m_total
+
+
+def parity_block(cfg, m_total, lam, basis, k, total):
+    """Compare the run's result with the committed golden fixture of the same
+    input bytes (tests/golden/<config>.npz, from the compiled reference)."""
+    import numpy as np
+
+    from tests.parity import fixture_parity, parity_ok
+    path = os.path.join(ROOT, "tests", "golden", f"{cfg['name']}.npz")
+    if not os.path.exists(path):
+        return {"unavailable": f"tests/golden/{cfg['name']}.npz not generated"}
+    gz = np.load(path)
+    if int(gz["m"]) != m_total or "a_rows" not in gz:
+        return {"unavailable": f"fixture is for m={int(gz['m'])}, this run's matrix has m={m_total}"}
+    p = fixture_parity(gz, "truncated", lam, basis, k)
+    p["total_rel_err"] = abs(total - float(gz["total"])) / float(gz["total"])
+    p["oracle"] = str(gz["oracle"])
+    p["ok"] = bool(parity_ok(p) and p["total_rel_err"] <= 1e-12)
+    p["bars"] = "eig_rel_err<=1e-10, K==K_ref, topK_sine<=1e-8, per-vector (gap>=1e-6) sines<=1e-8"
+    return p
 
 
 # --------------------------------------------------------------------------- reference arm
+def _llc_bytes():
+    try:
+        best = 0
+        base = "/sys/devices/system/cpu/cpu0/cache"
+        for d in os.listdir(base):
+            if d.startswith("index"):
+                lvl = open(os.path.join(base, d, "level")).read().strip()
+                if lvl == "3":
+                    sz = open(os.path.join(base, d, "size")).read().strip().upper()
+                    mult = {"K": 1 << 10, "M": 1 << 20}.get(sz[-1], 1)
+                    best = max(best, int(sz.rstrip("KM")) * mult)
+        return best or (32 << 20)
+    except Exception:
+        return 32 << 20
+
+
 def reference_arm(args, cfg):
     """The reference's own CPU implementation (oracle/_ref: the unmodified
-    reference sources compiled in place) on a bounded row sample of the same
+    reference sources compiled in place) on a bounded sample of the same
     workload, on all the host threads it can use. Each reference call is
     single-threaded by design, but callers may run independent calls in
-    parallel, so the work that scales with m (centering, the
-    tall GEMMs, Householder QR, U = Q W) runs as `threads` concurrent
-    reference pipelines on independent m_s-row samples: the step time for m
-    rows is the concurrent wall time x m / (threads x m_s), which includes
-    the cores' shared memory-bandwidth contention. The m-independent small
-    problem (Gram of T + eig_sym(l) + T W, or eig_sym(n) for the Gram route)
-    is one sequential reference call, timed once per process at full size n
-    and added to every step."""
+    parallel, so the work that scales with m runs as `threads`
+    concurrent reference pipelines on independent ms-row samples of the
+    config's own matrix (ms >= 4096 rows and the samples together >= 4x the
+    LLC, so they stream from DRAM like the full matrix): the step time for m
+    rows is the concurrent wall time x m / (threads x ms). The m-independent
+    small problem (eig_sym(n) of the Gram route; Gram of T + eig_sym(l) + T W
+    of the sketch) is one sequential reference call timed once per process.
+    The Gram-route pipeline per sample is the reference's fit_pca: center,
+    total_variance, gram, U = A V with a DENSE V (matmul skips zero entries of
+    its right operand, kernels.cpp:25-27, so an identity would skip the work).
+    c3 (Lanczos) has no reference counterpart: its reference arm is the
+    reference's truncated_svd pipeline on the same matrix (its oracle)."""
     import numpy as np
 
     from oracle.pyoracle import Oracle, available
     if not available("ref"):
         raise SystemExit(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
     ref = Oracle("ref")
-    m, n, l, q = cfg["m"] * args.gpus, cfg["n"], cfg["l"], cfg["q"]
-    full = cfg["m"] * cfg["n"] <= 20000 * 256  # c1 runs whole
-    ms = m if full else max(n, 1024)
+    m, n, l, q = cfg["m"] * (1 if cfg["strong"] else args.gpus), cfg["n"], cfg["l"], cfg["q"]
     threads = max(1, int(getattr(args, "ref_threads", 0) or len(os.sched_getaffinity(0))))
     threads = min(threads, 128)
-    scale = np.array([SPECTRA[cfg["spec"]](i) for i in range(1, n + 1)])
-    samples = [np.asfortranarray(np.random.default_rng(7 + i).standard_normal((ms, n)) * scale)
-               for i in range(threads if not full else 1)]
-    a = samples[0]
+    full = cfg["m"] * cfg["n"] <= 20000 * 256  # c1 runs whole
+    llc = _llc_bytes()
+    if full:
+        ms, threads = m, 1
+    else:
+        ms = max(4096, -(-4 * llc // (threads * 8 * n)))
+        ms = min(ms, m)
+    c = synth.CONFIGS[cfg["name"]]
+    rng = np.random.default_rng(11)
+    # samples from the same generator (spectrum, noise, quantised X): one ms-row
+    # block per thread of a (threads x ms)-row matrix — statistically the
+    # config's rows (the reference's run time does not depend on the values)
+    if full:
+        samples = [synth.config_host_matrix(c)]
+    else:
+        mt = ms * threads
+        mix, _ = synth.mixing(synth.host_gram_x(mt, n, synth.MATRIX_SEED), c.spectrum(), synth.MATRIX_SEED)
+        samples = [synth.host_matrix(mt, n, c.spectrum(), c.sigma, synth.MATRIX_SEED, row0=i * ms, rows=ms,
+                                     mix=mix) for i in range(threads)]
+    dense_v = np.linalg.qr(rng.standard_normal((n, n)))[0]
+    dense_v = np.asfortranarray(dense_v)
+    dense_w = np.asfortranarray(np.linalg.qr(rng.standard_normal((l, l)))[0]) if l else None
 
-    def rows_part(a=a):
+    def rows_part(a):
         t0 = time.perf_counter()
-        c, _ = ref.center(a, 1)
-        ref.frobenius_norm_sq(c)
+        cc, _ = ref.center(a, 1)
+        ref.frobenius_norm_sq(cc)
         if cfg["method"] == "randomized":
-            om = ref.gaussian_matrix(n, l, 4242)
-            h = ref.matmul(c, om)
+            om = ref.gaussian_matrix(n, l, synth.METHOD_SEED)
+            h = ref.matmul(cc, om)
             for _ in range(q):
-                h = ref.matmul(c, ref.matmul_tl(c, h))
+                h = ref.matmul(cc, ref.matmul_tl(cc, h))
             qq, _, _ = ref.qr_thin(h)
-            t = ref.matmul_tl(c, qq)
-            ref.matmul(qq, np.asfortranarray(np.eye(l)))  # U = Q W  (m x l x l)
+            t = ref.matmul_tl(cc, qq)
+            ref.matmul(qq, dense_w)  # U = Q W (m x l x l)
             return time.perf_counter() - t0, t
-        g = ref.gram(c)
-        ref.matmul(c, np.asfortranarray(np.eye(n)))  # U = A V (m x n x n)
+        g = ref.gram(cc)
+        ref.matmul(cc, dense_v)  # U = A V (m x n x n)
         return time.perf_counter() - t0, g
 
     fixed = 0.0
-    sample = ""
     if full:
+        a = samples[0]
+
         def step():
             t0 = time.perf_counter()
-            c, _ = ref.center(a, 1)
-            ref.frobenius_norm_sq(c)
-            ref.truncated_svd(c)
+            cc, _ = ref.center(a, 1)
+            ref.frobenius_norm_sq(cc)
+            ref.truncated_svd(cc)
             return time.perf_counter() - t0
-        threads = 1  # one whole-matrix reference call: nothing independent to run beside it
-        sample = f"full reference fit_pca (center, total, truncated_svd) on {m}x{n}"
+        sample = f"full reference fit_pca (center, total_variance, truncated_svd) on the whole {m}x{n} matrix"
     else:
-        _, small = rows_part()
+        _, small = rows_part(samples[0])
         extrap = ""
         t0 = time.perf_counter()
         if cfg["method"] == "randomized":
@@ -232,9 +289,10 @@ def reference_arm(args, cfg):
         elif n <= 1024:
             ref.eig_sym(small)
         else:
-            # eig_sym(n) takes 17 min at n = 2048 and ~3.4 h at 4096 on one core:
-            # time it at 512 and scale by the measured 12x per doubling of n
-            # (0.54 / 6.75 / 82.0 / 1002.7 s for n = 256..2048)
+            # eig_sym(n) takes ~17 min at n = 2048 and hours at 4096 on one core:
+            # time it at 512 and scale by 12x per doubling of n (SURVEY 6:
+            # 0.54 / 6.75 / 82.0 / 1002.7 s for n = 256..2048; the fixture runs'
+            # measured eig_sym times are in profiles/r2_reference_fixture_times.json)
             ref.eig_sym(np.asfortranarray(small[:512, :512]))
             extrap = f", eig_sym({n}) extrapolated from n=512 by 12^log2(n/512)"
         fixed = time.perf_counter() - t0
@@ -253,9 +311,14 @@ def reference_arm(args, cfg):
                 list(pool.map(rows_part, samples))
             t = time.perf_counter() - t0
             return t * (m / (ms * threads)) + fixed
-        sample = (f"{threads} concurrent reference pipelines, each on its own {ms}-row sample (x{m / (ms * threads):.1f}"
-                  f" to {m} rows, m-proportional phases) + m-independent small problem (one sequential reference "
-                  f"call) timed once ({fixed:.1f} s{extrap})")
+        sample = (f"{threads} concurrent reference pipelines (center, total_variance, "
+                  + ("A Omega, q x A(A^T H), qr_thin, A^T Q, U = Q W" if cfg["method"] == "randomized"
+                     else "gram, U = A V") +
+                  f"), each on its own {ms}-row block of the config's generator ({threads * ms * n * 8 / 2**20:.0f} MiB "
+                  f"together vs {llc / 2**20:.0f} MiB LLC), scaled x{m / (ms * threads):.1f} to {m} rows; + the "
+                  f"m-independent small problem (one sequential reference call) timed once ({fixed:.1f} s{extrap}). "
+                  "Extrapolated: the m-proportional phases (linear in m at fixed n); full-height single-core "
+                  "reference runs are in profiles/r2_reference_fixture_times.json")
     for _ in range(args.warmup):
         step()
     ts = [step() for _ in range(args.steps)]
@@ -263,7 +326,8 @@ def reference_arm(args, cfg):
     value = m / sec
     return {"metric": "pca_rows_per_sec", "value": value, "unit": "rows/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded Gaussian sample)",
+            "scaling": "strong" if cfg["strong"] else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: row blocks of the shared seeded generator (paper_1906_12085_b200/synth.py)",
             "impl": "reference",
             "config": {"workload": cfg["desc"], "m": m, "n": n, "method": cfg["method"], "l": l, "q": q},
             "cpu_baseline": {"value": value, "unit": "rows/s", "cores": threads, "kind": "reference", "sample": sample},
@@ -274,6 +338,7 @@ def reference_arm(args, cfg):
 def ours(args, cfg):
     import ctypes as C
 
+    import numpy as np
     import torch
     import torch.distributed as dist
 
@@ -292,11 +357,14 @@ def ours(args, cfg):
         dist.broadcast_object_list(obj, src=0)
         eng.ctx.attach_nccl(obj[0], rank, world)
 
-    m, n = cfg["m"], cfg["n"]
-    if cfg.get("strong"):
-        m = m // world
+    peak = dgemm_peak(torch.device("cuda", local))
+    peak_src = "measured in this run: cuBLAS DGEMM 8192^3 fp64 (torch.matmul), best of 5"
+    if not (peak == peak) or peak <= 0:
+        peak, peak_src = FP64_PEAK_TFLOPS, "round-1 measurement on this pool (profiles/fp64_peaks.json)"
+    n = cfg["n"]
     mid = METHOD_ID[cfg["method"]]
-    A = generate(cfg, m, torch.device("cuda", local), rank)
+    A, m_total = generate(eng, cfg, world, rank)
+    m = A.shape[0]
 
     cpu_proc = None
     cpu_out = tempfile.NamedTemporaryFile(suffix=".json", delete=False).name
@@ -305,7 +373,7 @@ def ours(args, cfg):
         env = dict(os.environ, CUDA_VISIBLE_DEVICES="")
         # the in-run baseline stays on ONE pinned core so it cannot disturb the
         # GPU run's host thread; `--impl reference` alone uses every core
-        cmd = [sys.executable, os.path.abspath(__file__), "--impl", "reference", "--config", args.config,
+        cmd = [sys.executable, os.path.abspath(__file__), "--impl", "reference", "--config", cfg["name"],
                "--steps", "1", "--warmup", "0", "--ref-threads", "1"]
         if ncpu > 2:
             cmd = ["taskset", "-c", str(ncpu - 1)] + cmd
@@ -317,8 +385,8 @@ def ours(args, cfg):
     def step():
         # center=2: fit_pca's centring runs every step, in place on the scratch A
         # (no second m x n buffer; the 64 GB c4 matrix then fits one GPU)
-        return eng.pca(A, method=mid, l=cfg["l"], q=cfg["q"], seed=4242, center=2, threshold=cfg["t"],
-                       out=out)
+        return eng.pca(A, method=mid, l=cfg["l"], q=cfg["q"], seed=synth.METHOD_SEED, center=2,
+                       threshold=cfg["t"], out=out)
 
     def barrier():
         if world > 1:
@@ -367,16 +435,26 @@ def ours(args, cfg):
     phases = {nm: eng.ctx.timing(nm) for nm in names}
     eng.ctx.set_timing(False)
     ms_step = ms / args.steps
-    rows_total = m * world
+    rows_total = m * world if not cfg["strong"] else m_total
     value = rows_total * args.steps / (ms / 1e3)
+
+    # ---------------- parity of the last timed step vs the golden fixture ----------------
+    width = {"randomized": cfg["l"]}.get(cfg["method"], n)
+    result = {"rank": out.rank, "K": out.k, "total_variance": out.total}
+    parity = None
+    if rank == 0:
+        sig = out.sigma[:out.rank].cpu().numpy()
+        try:
+            parity = parity_block(cfg, m_total, sig * sig, out.v[:, :out.rank].cpu().numpy(), out.k, out.total)
+        except Exception as e:  # pragma: no cover - report, never hide
+            parity = {"error": f"{type(e).__name__}: {e}"}
 
     # ---------------- e2e: host buffers through the C-ABI ----------------
     e2e_bytes_in = 8 * m * n
     # short steps (c1: ~4 ms) are timed over enough calls (>= ~0.25 s) that host
     # jitter on the box does not dominate the wall-clock mean
     e2e_steps = max(args.steps, min(100, int(250.0 / max(ms_step, 1e-3))))
-    width = {"randomized": cfg["l"]}.get(cfg["method"], n)
-    result = {"rank": out.rank, "K": out.k, "total_variance": out.total}
+    e2e_parity = None
     if world == 1:
         lib = _lib.load()
         host = torch.empty(n, m, dtype=torch.float64, pin_memory=True).t()
@@ -392,8 +470,9 @@ def ours(args, cfg):
 
         def e2e_step():
             _lib.check(lib.svdk_fit_pca(eng.ctx.handle, C.c_void_p(host.data_ptr()), m, n, 1, mid, cfg["l"],
-                                        cfg["q"], 4242, 1, C.c_void_p(basis.data_ptr()), C.c_void_p(eig.data_ptr()),
-                                        C.byref(total), C.c_void_p(mean.data_ptr()), C.byref(rank_c)))
+                                        cfg["q"], synth.METHOD_SEED, 1, C.c_void_p(basis.data_ptr()),
+                                        C.c_void_p(eig.data_ptr()), C.byref(total), C.c_void_p(mean.data_ptr()),
+                                        C.byref(rank_c)))
             _lib.check(lib.svdk_select_components(eng.ctx.handle, C.c_void_p(eig.data_ptr()), rank_c.value,
                                                   total.value, cfg["t"], C.byref(kk)))
         e2e_step()
@@ -405,6 +484,14 @@ def ours(args, cfg):
         e2e_sec = (time.perf_counter() - t0) / e2e_steps
         e2e_out = 8 * (n * rank_c.value + rank_c.value + n)
         e2e_k = kk.value
+        r = rank_c.value
+        bas = basis.numpy()[:r].T  # basis is written column-major n x r
+        try:
+            ep = parity_block(cfg, m_total, eig.numpy()[:r].copy(), np.asfortranarray(bas), e2e_k, total.value)
+            e2e_parity = {k: ep.get(k) for k in ("ok", "eig_rel_err", "topK_sine", "K", "K_ref", "unavailable")
+                          if k in ep}
+        except Exception as e:  # pragma: no cover
+            e2e_parity = {"error": f"{type(e).__name__}: {e}"}
     else:
         host = torch.empty(n, m, dtype=torch.float64, pin_memory=True).t()
         host.copy_(A)
@@ -415,7 +502,8 @@ def ours(args, cfg):
 
         def e2e_step():
             dev.copy_(host, non_blocking=True)
-            o = eng.pca(dev, method=mid, l=cfg["l"], q=cfg["q"], seed=4242, center=2, threshold=cfg["t"])
+            o = eng.pca(dev, method=mid, l=cfg["l"], q=cfg["q"], seed=synth.METHOD_SEED, center=2,
+                        threshold=cfg["t"])
             r = o.rank
             res[:n * r].copy_(o.v[:, :r].t().reshape(-1), non_blocking=True)
             res[n * r:n * r + r].copy_(o.sigma[:r], non_blocking=True)
@@ -439,6 +527,16 @@ def ours(args, cfg):
     # DMMA GEMM/SYRK (FP64 tensor pipe) or the Lanczos GEMV pair (HBM), by share of the step
     zero = {"count": 0, "ms": 0.0, "flops": 0.0, "bytes": 0.0}
     g, gv, ej = phases.get("dmma_gemm", zero), phases.get("gemv_pair", zero), phases.get("eig_sym", zero)
+
+    def traffic_of(kernel_key):
+        tpath = os.path.join(ROOT, "profiles", f"dram_traffic_{cfg['name']}.json")
+        if os.path.exists(tpath):
+            try:
+                return json.load(open(tpath)).get(kernel_key, json.load(open(tpath)).get("bytes_per_launch"))
+            except Exception:
+                return None
+        return None
+
     if ej["ms"] > max(g["ms"], gv["ms"]):
         # the n x n Jacobi eigensolve dominates (c1, c5): its algorithmic work is
         # 8 n^3 flops per sweep on the DMMA pipe (two-sided update of the upper
@@ -447,53 +545,30 @@ def ours(args, cfg):
         n_eig = cfg["l"] if cfg["method"] == "randomized" else n
         eflops = ej["count"] * sweeps * 8.0 * n_eig ** 3
         achieved = eflops / (ej["ms"] / 1e3) / 1e12 if ej["ms"] > 0 else 0.0
-        roofline = {"bound": "tensor",
-                    "kernel": ("Jacobi sweep (quad scheme: jacobi_quad_solve + jacobi_update_a64/_v64 DMMA, one "
-                               "CUDA graph per sweep)" if n_eig >= 3072 else
-                               "Jacobi sweep (jacobi_pair_solve + jacobi_update_a_reg/_v_reg DMMA, one CUDA graph "
-                               "per sweep)"),
-                    "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                    "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None, "launches": ej["count"],
-                    "share_of_step": ej["ms"] / ms if ms else None,
-                    "algorithmic_flops_per_launch": eflops / max(ej["count"], 1),
-                    "peak_source": "measured cuBLAS DGEMM 8192^3 sustained on B200 (profiles/fp64_peaks.json)",
-                    "note": f"{sweeps} sweeps x 8 n^3 (n = {n_eig}); at small n the sweep is latency-bound "
-                            "(~n dependent inner rotation rounds per sweep); at n = 4096 the 64-wide A/V updates "
-                            "are DMMA-bound (pipe 64% / 77% active, profiles/r1_jacobi_quad_ncu.txt) behind the "
-                            "latency-bound 64x64 solves"}
+        roofline = {"bound": "tensor", "kernel": "Jacobi sweep graph (pair/quad solves + DMMA A/V block updates)",
+                    "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                    "launches": ej["count"], "share_of_step": ej["ms"] / ms if ms else None,
+                    "algorithmic_flops_per_launch": eflops / max(ej["count"], 1), "peak_source": peak_src,
+                    "note": f"{sweeps} sweeps x 8 n^3 (n = {n_eig})"}
     elif gv["ms"] > g["ms"]:
         achieved = gv["bytes"] / (gv["ms"] / 1e3) / 1e9 if gv["ms"] > 0 else 0.0
-        peak = HBM_PEAK_GBS
-        traffic = None
-        tpath = os.path.join(ROOT, "profiles", f"dram_traffic_{args.config}.json")
-        if os.path.exists(tpath):
-            try:
-                traffic = json.load(open(tpath)).get("bytes_per_launch")
-            except Exception:
-                traffic = None
         roofline = {"bound": "hbm",
-                    "kernel": "gemv_pair_cluster_kernel (Lanczos w = A^T (A q): one HBM read of A by TMA, 4-CTA clusters, "
-                              "second pass from L2, y exchanged over DSMEM)",
-                    "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                    "kernel": "gemv_pair_cluster_kernel (Lanczos w = A^T (A q): one HBM read of A by TMA, "
+                              "CTA clusters, second pass from L2, y exchanged over DSMEM)",
+                    "achieved": achieved, "peak": HBM_PEAK_GBS, "unit": "GB/s", "frac": achieved / HBM_PEAK_GBS,
                     "algorithmic_bytes_per_launch": gv["bytes"] / max(gv["count"], 1),
-                    "traffic": traffic, "launches": gv["count"], "share_of_step": gv["ms"] / ms if ms else None,
-                    "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, best of 10)",
+                    "traffic": traffic_of("gemv_pair"), "launches": gv["count"],
+                    "share_of_step": gv["ms"] / ms if ms else None, "peak_source": HBM_PEAK_SRC,
                     "note": "algorithmic bytes = one read of A (8mn) per launch"}
     else:
         achieved = g["flops"] / (g["ms"] / 1e3) / 1e12 if g["ms"] > 0 else 0.0
-        traffic = None
-        tpath = os.path.join(ROOT, "profiles", f"dram_traffic_{args.config}.json")
-        if os.path.exists(tpath):
-            try:
-                traffic = json.load(open(tpath)).get("bytes_per_launch")
-            except Exception:
-                traffic = None
-        roofline = {"bound": "tensor", "kernel": "gemm_kernel (FP64 DMMA.8x8x4 + TMA)", "achieved": achieved,
-                    "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
-                    "traffic": traffic, "launches": g["count"], "share_of_step": g["ms"] / ms if ms else None,
-                    "peak_source": "measured cuBLAS DGEMM 8192^3 sustained on B200 (profiles/fp64_peaks.json); "
-                                   f"DMMA pipe peak {FP64_PIPE_TFLOPS} TF/s -> frac_pipe "
-                                   f"{achieved / FP64_PIPE_TFLOPS:.3f}"}
+        roofline = {"bound": "tensor", "kernel": "gemm_kernel (FP64 DMMA.8x8x4 + TMA mbarrier ring)",
+                    "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                    "traffic": traffic_of("dmma_gemm"), "launches": g["count"],
+                    "algorithmic_flops_per_launch": g["flops"] / max(g["count"], 1),
+                    "share_of_step": g["ms"] / ms if ms else None, "peak_source": peak_src,
+                    "frac_of_dmma_pipe": achieved / FP64_PIPE_TFLOPS,
+                    "peak_committed_round1": FP64_PEAK_TFLOPS}
 
     cpu = None
     if cpu_proc is not None:
@@ -506,14 +581,16 @@ def ours(args, cfg):
             cpu = {"unavailable": f"cpu baseline failed: {e}"}
 
     if rank == 0:
-        flops = method_flops(cfg, m) * world
+        flops = method_flops(cfg, rows_total)
         line = {
             "metric": "pca_rows_per_sec", "value": value, "unit": "rows/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "strong" if cfg.get("strong") else "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic: seeded low-rank + Gaussian noise generator of SURVEY 8d, column-centred",
-            "config": {"workload": cfg["desc"], "m_per_gpu": m, "n": n, "method": cfg["method"], "l": cfg["l"],
-                       "q": cfg["q"], "threshold": cfg["t"], "parallelism": f"dp{world} (row shards, NCCL allreduce)",
+            "scaling": "strong" if cfg["strong"] else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: the shared seeded generator (synth.py; A = X M + sigma N, SURVEY 8d spectrum), "
+                    "centred by fit_pca inside every step",
+            "config": {"workload": cfg["desc"], "m_total": m_total, "m_per_gpu": m, "n": n, "method": cfg["method"],
+                       "l": cfg["l"], "q": cfg["q"], "threshold": cfg["t"],
+                       "parallelism": f"dp{world} (row shards, NCCL allreduce)",
                        "l2": "no flush: A is larger than the 126 MB L2" if flush_buf is None
                        else "A fits in L2: 512 MB buffer written between steps, each step timed by its own events"},
             "pipeline_tflops": flops / (ms_step / 1e3) / 1e12,
@@ -521,10 +598,11 @@ def ours(args, cfg):
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "rows/s", "h2d_bytes_per_step": e2e_bytes_in,
                     "d2h_bytes_per_step": e2e_out, "steps": e2e_steps,
-                    "path": "svdk_fit_pca + svdk_select_components (host buffers)"
-                    if world == 1 else "H2D shard + svdk_dev_pca + D2H basis/sigma"},
+                    "path": "svdk_fit_pca + svdk_select_components (pinned host buffers)"
+                    if world == 1 else "H2D shard + svdk_dev_pca + D2H basis/sigma", "parity": e2e_parity},
             "gpu_launches": launches,
             "clocks": clocks,
+            "parity": parity,
             "phases_ms_per_step": {k: round(v["ms"] / args.steps, 3) for k, v in phases.items()},
             "result": dict(result, e2e_K=e2e_k),
         }
@@ -538,22 +616,17 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c4", choices=sorted(synth.CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-threads", type=int, default=0,
                     help="--impl reference: concurrent reference pipelines (default: every usable core)")
     args = ap.parse_args()
-    cfg = dict(CONFIGS[args.config])
-    if args.config == "c4":
-        cfg["strong"] = True
+    cfg = config(args.config)
     if args.impl == "reference":
         if int(os.environ.get("RANK", 0)) != 0:
             return
-        cfg_ref = dict(cfg)
-        if cfg.get("strong"):
-            args.gpus = 1  # the reference works on the whole matrix
-        print(json.dumps(reference_arm(args, cfg_ref)), flush=True)
+        print(json.dumps(reference_arm(args, cfg)), flush=True)
         return
     ours(args, cfg)
 

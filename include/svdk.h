@@ -205,6 +205,29 @@ int svdk_dev_pca(svdk_ctx* ctx, const double* a, int64_t m_local, int64_t n, int
 int svdk_dev_idx_to_matrix(svdk_ctx* ctx, const uint8_t* pixels, int64_t count,
                            int64_t pixels_per_image, double* out, int64_t ldo);
 
+/* ---- seeded synthetic inputs (bench / tests / fixtures; no reference
+ * counterpart — SURVEY §8d's generator, not on the PCA path) ----
+ * A = X M + sigma N: X quantised Gaussians (stream 1), M = R_X^-1 diag(s) V0^T
+ * on a fixed-point grid (V0 from stream 2), N Gaussians (stream 3). Element e
+ * of a stream = global_row + column * m_total; Philox4x32-10 + Box-Muller with
+ * explicitly rounded polynomial log/sin/cos, so host and device produce the
+ * same bits and X^T X, X M are exact in any summation order (synth.h).
+ * svdk_synth_fill / svdk_dev_synth_fill: rows [row0, row0+rows) x cols of a
+ * stream into out (ld); quantise != 0 applies the X grid.
+ * svdk_synth_add_noise / _dev_: a += sigma * N on the same block.
+ * svdk_synth_mixing: M (n x n, ldm) from the exact gram gx = X^T X (ldg), the
+ * spectrum s (n) and the seed; *grid = M's fixed-point quantum. Host-only. */
+int svdk_synth_fill(uint64_t seed, int stream, int quantise, int64_t m_total, int64_t row0, int64_t rows,
+                    int64_t cols, double* out, int64_t ld);
+int svdk_synth_add_noise(uint64_t seed, int64_t m_total, int64_t row0, int64_t rows, int64_t cols,
+                         double sigma, double* a, int64_t lda);
+int svdk_synth_mixing(int64_t n, const double* gx, int64_t ldg, const double* s, uint64_t seed, double* mix,
+                      int64_t ldm, double* grid);
+int svdk_dev_synth_fill(svdk_ctx* ctx, uint64_t seed, int stream, int quantise, int64_t m_total,
+                        int64_t row0, int64_t rows, int64_t cols, double* out, int64_t ld);
+int svdk_dev_synth_add_noise(svdk_ctx* ctx, uint64_t seed, int64_t m_total, int64_t row0, int64_t rows,
+                             int64_t cols, double sigma, double* a, int64_t lda);
+
 #ifdef __cplusplus
 }
 #endif

@@ -69,6 +69,11 @@ SIGNATURES = {
     "svdk_cost_model": (C.c_int, [C.c_int, _u64, _u64, _u64, _u64, _dp, _dp, _dp]),
     "svdk_idx_parse": (C.c_int, [_vp, _u64, C.POINTER(_u64), C.POINTER(_u64)]),
     "svdk_idx_to_matrix": (C.c_int, [_ctxp, _vp, _i64, _i64, _vp]),
+    "svdk_synth_fill": (C.c_int, [_u64, C.c_int, C.c_int, _i64, _i64, _i64, _i64, _vp, _i64]),
+    "svdk_synth_add_noise": (C.c_int, [_u64, _i64, _i64, _i64, _i64, C.c_double, _vp, _i64]),
+    "svdk_synth_mixing": (C.c_int, [_i64, _vp, _i64, _vp, _u64, _vp, _i64, _dp]),
+    "svdk_dev_synth_fill": (C.c_int, [_ctxp, _u64, C.c_int, C.c_int, _i64, _i64, _i64, _i64, _vp, _i64]),
+    "svdk_dev_synth_add_noise": (C.c_int, [_ctxp, _u64, _i64, _i64, _i64, _i64, C.c_double, _vp, _i64]),
 }
 
 _lib = None

@@ -31,6 +31,10 @@ CostOut cost_model(int model, uint64_t m, uint64_t n, uint64_t l, uint64_t i);
 void idx_parse(const uint8_t* bytes, uint64_t len, uint64_t dims[3], uint64_t* err_offset);
 void idx_to_matrix_dev(Ctx* c, const uint8_t* px, int64_t count, int64_t P, double* out,
                        int64_t ldo);
+void synth_fill_dev(Ctx* c, uint64_t seed, int stream, int quantise, int64_t m_total, int64_t row0,
+                    int64_t rows, int64_t cols, double* out, int64_t ld);
+void synth_add_noise_dev(Ctx* c, uint64_t seed, int64_t m_total, int64_t row0, int64_t rows, int64_t cols,
+                         double sigma, double* a, int64_t lda);
 }  // namespace svdk
 
 using namespace svdk;
@@ -706,6 +710,22 @@ int svdk_dev_idx_to_matrix(svdk_ctx* c, const uint8_t* pixels, int64_t count,
     return guarded([&] {
         need_ctx(c);
         idx_to_matrix_dev(c, pixels, count, pixels_per_image, out, ldo);
+    });
+}
+
+int svdk_dev_synth_fill(svdk_ctx* c, uint64_t seed, int stream, int quantise, int64_t m_total,
+                        int64_t row0, int64_t rows, int64_t cols, double* out, int64_t ld) {
+    return guarded([&] {
+        need_ctx(c);
+        synth_fill_dev(c, seed, stream, quantise, m_total, row0, rows, cols, out, ld);
+    });
+}
+
+int svdk_dev_synth_add_noise(svdk_ctx* c, uint64_t seed, int64_t m_total, int64_t row0, int64_t rows,
+                             int64_t cols, double sigma, double* a, int64_t lda) {
+    return guarded([&] {
+        need_ctx(c);
+        synth_add_noise_dev(c, seed, m_total, row0, rows, cols, sigma, a, lda);
     });
 }
 

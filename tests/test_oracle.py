@@ -171,10 +171,35 @@ def test_golden_small_port():
 
 
 def test_golden_c1_inputs_regenerate():
-    """The c1 input regenerates byte-identically (checksum) from the seed."""
+    """The c1 input regenerates byte-identically on the CPU from the seed: the
+    host-built mixing matrix (checksum) and the fixture's probe rows."""
     import hashlib
 
-    from tests.datagen import make_matrix
+    from paper_1906_12085_b200 import synth
+    from tests.datagen import config_matrix
     gz = _golden("c1.npz")
-    a = make_matrix(20000, 256, "c1", seed=int(gz["seed"]))
-    assert hashlib.sha256(a.tobytes(order="F")).hexdigest() == str(gz["sha256"])
+    m, n, seed = int(gz["m"]), int(gz["n"]), int(gz["seed"])
+    mix, _ = synth.mixing(synth.host_gram_x(m, n, seed), synth.CONFIGS["c1"].spectrum(), seed)
+    assert hashlib.sha256(np.ascontiguousarray(mix).tobytes()).hexdigest() == str(gz["mix_sha256"])
+    a = config_matrix("c1", seed=seed)
+    assert np.array_equal(a[np.asarray(gz["a_rows_idx"])], gz["a_rows"])
+
+
+@pytest.mark.parametrize("name", ["c2mid", "c2", "c3", "c4", "c5"])
+def test_golden_config_mixing_regenerates(name):
+    """Every full-size fixture's mixing matrix M rebuilds bit-identically on
+    this host (deterministic host arithmetic; X^T X exact) — the GPU test
+    test_gpu_synth.py checks the same checksum on the box. c4's X^T X over
+    8.4M rows is skipped here (minutes of CPU); c2/c3/c5 run the whole Gram."""
+    import hashlib
+
+    from paper_1906_12085_b200 import synth
+    gz = _golden(f"{name}.npz")
+    if "mix_sha256" not in gz:
+        pytest.skip("fixture predates the shared generator")
+    m, n, seed = int(gz["m"]), int(gz["n"]), int(gz["seed"])
+    if m * n > 6e8:
+        pytest.skip("X^T X over the full height is checked on the GPU (test_gpu_synth.py)")
+    cfg = synth.CONFIGS[str(gz["cfg"])]
+    mix, _ = synth.mixing(synth.host_gram_x(m, n, seed, chunk=1 << 17), cfg.spectrum(n), seed)
+    assert hashlib.sha256(np.ascontiguousarray(mix).tobytes()).hexdigest() == str(gz["mix_sha256"])
