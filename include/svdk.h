@@ -81,6 +81,22 @@ int svdk_ctx_timing_names(svdk_ctx* ctx, char* buf, int64_t len);
 /* 128-byte NCCL unique id, produced on rank 0 and shared out of band. */
 int svdk_nccl_unique_id(char out[128]);
 int svdk_ctx_attach_nccl(svdk_ctx* ctx, const char id[128], int rank, int world);
+/* In-process host-staged collectives: `world` contexts (any GPUs, including
+ * several on one GPU), each driven by its own host thread, attach to one group
+ * with ranks 0..world-1; every row reduction is staged through host memory and
+ * summed in rank order (no kernel waits on another rank). For running and
+ * testing the sharded paths without a multi-GPU node; NCCL is the production
+ * backend. A failing rank aborts the group: its peers' calls return
+ * SVDK_E_STATE instead of waiting. destroy drops the creator's reference (the
+ * group lives until the last attached context detaches). */
+typedef struct svdk_host_group svdk_host_group;
+int svdk_host_group_create(int world, svdk_host_group** out);
+int svdk_host_group_destroy(svdk_host_group* group);
+int svdk_ctx_attach_host_group(svdk_ctx* ctx, svdk_host_group* group, int rank);
+/* Detach (NCCL: destroy the communicator) and return to single-GPU mode. */
+int svdk_ctx_detach_comm(svdk_ctx* ctx);
+/* rank / world of the attached communicator (0 / 1 when none). */
+int svdk_ctx_comm_info(svdk_ctx* ctx, int* rank, int* world);
 
 /* ---- L1 kernels (reference kernels.hpp / kernels.cpp) ---- */
 /* kernels.cpp:14-45  C (m x l) = A (m x n) * B (n x l); non-finite C -> NUMERICAL */

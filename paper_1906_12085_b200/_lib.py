@@ -40,6 +40,11 @@ SIGNATURES = {
     "svdk_ctx_timing_names": (C.c_int, [_ctxp, C.c_char_p, _i64]),
     "svdk_nccl_unique_id": (C.c_int, [C.c_char_p]),
     "svdk_ctx_attach_nccl": (C.c_int, [_ctxp, C.c_char_p, C.c_int, C.c_int]),
+    "svdk_host_group_create": (C.c_int, [C.c_int, C.POINTER(_vp)]),
+    "svdk_host_group_destroy": (C.c_int, [_vp]),
+    "svdk_ctx_attach_host_group": (C.c_int, [_ctxp, _vp, C.c_int]),
+    "svdk_ctx_detach_comm": (C.c_int, [_ctxp]),
+    "svdk_ctx_comm_info": (C.c_int, [_ctxp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "svdk_matmul": (C.c_int, [_ctxp, _vp, _i64, _i64, _vp, _i64, _vp]),
     "svdk_matmul_transposed_left": (C.c_int, [_ctxp, _vp, _i64, _i64, _vp, _i64, _vp]),
     "svdk_transpose": (C.c_int, [_ctxp, _vp, _i64, _i64, _vp]),
@@ -153,10 +158,43 @@ class Context:
     def attach_nccl(self, unique_id: bytes, rank: int, world: int) -> None:
         check(load().svdk_ctx_attach_nccl(self._h, unique_id, int(rank), int(world)))
 
+    def attach_host_group(self, group: "HostGroup", rank: int) -> None:
+        check(load().svdk_ctx_attach_host_group(self._h, group.handle, int(rank)))
+
+    def detach_comm(self) -> None:
+        check(load().svdk_ctx_detach_comm(self._h))
+
+    def comm_info(self) -> tuple:
+        r, w = C.c_int(0), C.c_int(0)
+        check(load().svdk_ctx_comm_info(self._h, C.byref(r), C.byref(w)))
+        return r.value, w.value
+
     def close(self) -> None:
         if getattr(self, "_h", None):
             load().svdk_ctx_destroy(self._h)
             self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class HostGroup:
+    """In-process host-staged collective group (svdk_host_group_*): `world`
+    contexts driven by host threads act as the ranks of a row-sharded call."""
+
+    def __init__(self, world: int):
+        h = _vp()
+        check(load().svdk_host_group_create(int(world), C.byref(h)))
+        self.handle = h
+        self.world = world
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            load().svdk_host_group_destroy(self.handle)
+            self.handle = None
 
     def __del__(self):
         try:

@@ -40,6 +40,7 @@ void synth_add_noise_dev(Ctx* c, uint64_t seed, int64_t m_total, int64_t row0, i
 using namespace svdk;
 
 struct svdk_ctx : Ctx {};
+struct svdk_host_group {};  // opaque handle of a svdk::HostGroup
 
 namespace {
 
@@ -668,6 +669,39 @@ int svdk_ctx_attach_nccl(svdk_ctx* c, const char id[128], int rank, int world) {
     return guarded([&] {
         need_ctx(c);
         attach_nccl(c, id, rank, world);
+    });
+}
+
+int svdk_host_group_create(int world, svdk_host_group** out) {
+    return guarded([&] {
+        if (!out) fail(SVDK_E_PARAM, "host_group_create: null out");
+        *out = reinterpret_cast<svdk_host_group*>(host_group_create(world));
+    });
+}
+
+int svdk_host_group_destroy(svdk_host_group* g) {
+    return guarded([&] { host_group_release(reinterpret_cast<HostGroup*>(g)); });
+}
+
+int svdk_ctx_attach_host_group(svdk_ctx* c, svdk_host_group* g, int rank) {
+    return guarded([&] {
+        need_ctx(c);
+        attach_host_group(c, reinterpret_cast<HostGroup*>(g), rank);
+    });
+}
+
+int svdk_ctx_detach_comm(svdk_ctx* c) {
+    return guarded([&] {
+        need_ctx(c);
+        destroy_comm(c);
+    });
+}
+
+int svdk_ctx_comm_info(svdk_ctx* c, int* rank, int* world) {
+    return guarded([&] {
+        need_ctx(c);
+        if (rank) *rank = has_comm(c) ? c->rank : 0;
+        if (world) *world = has_comm(c) ? c->world : 1;
     });
 }
 

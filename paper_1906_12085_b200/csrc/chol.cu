@@ -27,14 +27,16 @@ void gaussian_fill(int64_t rows, int64_t cols, uint64_t seed, double* out);
 
 namespace {
 
-constexpr int NB = 64;  // Cholesky panel width (diagonal block factored by one CTA)
+constexpr int NB = 64;             // Cholesky panel width (diagonal block factored by one CTA)
+constexpr int CHOL_THREADS = 256;  // threads of chol_diag_kernel
+static_assert(NB * NB % CHOL_THREADS == 0, "chol_diag_kernel's load phase tiles NB x NB exactly");
 
 __device__ long long g_cprobe[4];  // development probe (svdk_debug_chol_probe)
 
 // Factor the bs x bs diagonal block G[k0.., k0..] (upper part holds the
 // trailing-updated values) as R^T R, write R (upper) and R^-1 (upper).
 // flag |= 1 on a pivot d <= rel_tol * diag0[k] (or d <= 0).
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(CHOL_THREADS)
     chol_diag_kernel(const double* G, int64_t ldg, int64_t k0, int bs, double* R, int64_t ldr,
                      double* Rinv, int ldri, const double* diag0, double rel_tol, int* flag) {
     constexpr int LD = NB + 1;
@@ -47,16 +49,16 @@ __global__ void __launch_bounds__(256)
     // all of a thread's loads are issued before its first store (the earlier
     // load -> store loop was 16 dependent L2 round trips: 9.7k cycles)
     {
-        constexpr int PER = NB * NB / 256;  // launched with 256 threads
+        constexpr int PER = NB * NB / CHOL_THREADS;
         double v[PER];
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
-            const int e = tid + 256 * k, i = e % bs, j = e / bs;
+            const int e = tid + CHOL_THREADS * k, i = e % bs, j = e / bs;
             v[k] = (e < bs * bs && i <= j) ? G[(k0 + i) + (k0 + j) * ldg] : 0.0;
         }
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
-            const int e = tid + 256 * k, i = e % bs, j = e / bs;
+            const int e = tid + CHOL_THREADS * k, i = e % bs, j = e / bs;
             if (e < bs * bs && i <= j) {
                 S[i + j * LD] = v[k];
                 S[j + i * LD] = v[k];
@@ -219,7 +221,7 @@ int read_flag(Ctx* c, int idx) {
 }  // namespace
 
 // Blocked right-looking Cholesky of G (p x p, overwritten) -> R (upper,
-// ldr) and the inverses of its 128 x 128 diagonal blocks (Rinv_blocks,
+// ldr) and the inverses of its NB x NB (64 x 64) diagonal blocks (Rinv_blocks,
 // nblk x NB x NB). Returns false on a pivot breakdown.
 bool potrf_upper(Ctx* c, double* G, int64_t ldg, int64_t p, double* R, int64_t ldr,
                  double* Rinv_blocks, double rel_tol) {
@@ -243,7 +245,7 @@ bool potrf_upper(Ctx* c, double* G, int64_t ldg, int64_t p, double* R, int64_t l
         const int64_t k0 = kb * NB;
         const int bs = static_cast<int>(std::min<int64_t>(NB, p - k0));
         double* rinv = Rinv_blocks + kb * NB * NB;
-        chol_diag_kernel<<<1, 256, smem, c->stream>>>(G, ldg, k0, bs, R, ldr, rinv, NB, diag.p(),
+        chol_diag_kernel<<<1, CHOL_THREADS, smem, c->stream>>>(G, ldg, k0, bs, R, ldr, rinv, NB, diag.p(),
                                                       rel_tol, c->d_flags + 3);
         SVDK_CHECK_LAUNCH();
         c->launches++;
@@ -260,7 +262,7 @@ bool potrf_upper(Ctx* c, double* G, int64_t ldg, int64_t p, double* R, int64_t l
 
 // R^-1 (p x p, upper) from R and the inverses of its diagonal blocks, by a
 // blocked back substitution: X_IJ = -R_II^-1 (R_I,>I X_>I,J), bottom-up, two
-// small triangular-aware GEMMs per 128-row block.
+// small triangular-aware GEMMs per NB-row (64-row) block.
 void trtri_upper(Ctx* c, const double* R, int64_t ldr, int64_t p, const double* Rinv_blocks,
                  double* X, int64_t ldx) {
     const int64_t nblk = ceil_div(p, NB);

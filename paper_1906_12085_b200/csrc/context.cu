@@ -10,6 +10,10 @@ namespace svdk {
     throw Failure{code, msg, residual};
 }
 
+[[noreturn]] void fail_agreed(int code, const std::string& msg, double residual) {
+    throw Failure{code, msg, residual, true};
+}
+
 // ---------------------------------------------------------------------------
 // Pool: grow-only set of cudaMalloc blocks, best-fit reuse. All users order
 // their work on the context's single stream, so a block returned to the pool

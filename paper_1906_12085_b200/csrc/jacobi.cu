@@ -1369,11 +1369,17 @@ void run_sweeps(Ctx* c, double* A, double* V, int64_t n_pad, int max_sweeps, dou
     jacobi_tables_kernel<TB><<<3, 256, 0, S>>>(reinterpret_cast<SolveTables<TB>*>(tab_buf.p()));
     SVDK_CHECK_LAUNCH();
     c->launches++;
+    // The first solve after jacobi_tables_kernel is a plain launch: the solve
+    // copies its schedule tables BEFORE griddepcontrol.wait, which is only
+    // legal when the tables' producer has completed (every later solve follows
+    // kernels that themselves waited on a grid launched after the tables).
+    bool after_tables = true;
     auto launch_solve = [&](double* qr, int* ar, int r, int mode) {
         const double* a = A;
         int64_t ld = n_pad;
-        launch(jacobi_pair_solve<TB>, k, nthreads_solve, smem_solve, true, a, ld, tabs, qr, ar, nb, r,
+        launch(jacobi_pair_solve<TB>, k, nthreads_solve, smem_solve, !after_tables, a, ld, tabs, qr, ar, nb, r,
                skip_tau, max_inner, mode);
+        after_tables = false;
     };
     auto enqueue_sweep = [&] {
         if (split) {  // in-block stage on the round-0 block pairing
@@ -1918,6 +1924,9 @@ void run_sweeps_quad(Ctx* c, double* A, double* V, int64_t n_pad, int max_sweeps
     const bool pdl = !(pdl_env && std::atoi(pdl_env) == 0);
     const double* a_in = A;
     int64_t ld = n_pad;
+    // the first launch after jacobi_tables_kernel is plain (the quad solve
+    // copies its tables before griddepcontrol.wait; see run_sweeps)
+    bool after_tables = true;
     auto launch = [&](auto kern, int grid, int block, size_t smem, auto... args) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(static_cast<unsigned>(grid));
@@ -1928,7 +1937,8 @@ void run_sweeps_quad(Ctx* c, double* A, double* V, int64_t n_pad, int max_sweeps
         at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         at[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = at;
-        cfg.numAttrs = pdl ? 1 : 0;
+        cfg.numAttrs = (pdl && !after_tables) ? 1 : 0;
+        after_tables = false;
         SVDK_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
     };
     auto enqueue_sweep = [&] {

@@ -767,7 +767,7 @@ GemvPair::GemvPair(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n)
     const char* gv_env = std::getenv("SVDK_GEMV");
     int smem_optin = 0;
     SVDK_CUDA(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
-    const bool shape_ok = (lda % 2 == 0) && m < (int64_t(1) << 31) && n < (int64_t(1) << 31) &&
+    const bool shape_ok = m > 0 && (lda % 2 == 0) && m < (int64_t(1) << 31) && n < (int64_t(1) << 31) &&
                           (reinterpret_cast<uintptr_t>(A) % 16 == 0);
     cluster_ = shape_ok && !(gv_env && std::string(gv_env) == "twopass");
     const char* cs_env = std::getenv("SVDK_GEMV_CS");

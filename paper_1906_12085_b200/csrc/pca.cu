@@ -108,13 +108,61 @@ int64_t select_components(Ctx* c, const double* d_w, int64_t count, double total
     return select_components_dev(c, d_w, count, dt.p(), t, nullptr);
 }
 
+namespace {
+void dev_pca_body(Ctx* c, const RowComm* comm, const double* A, int64_t m, int64_t n, int64_t lda, int method,
+                  int64_t l, int64_t q, uint64_t seed, int center_mode, double threshold, double* U,
+                  int64_t ldu, double* sigma, double* V, int64_t ldv, double* mean, int64_t* rank, int64_t* k,
+                  double* total);
+}  // namespace
+
 void dev_pca(Ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, int method, int64_t l,
              int64_t q, uint64_t seed, int center_mode, double threshold, double* U, int64_t ldu,
              double* sigma, double* V, int64_t ldv, double* mean, int64_t* rank, int64_t* k,
              double* total) {
-    const bool center = center_mode != 0, center_in_place = center_mode == 2;
     RowComm rc{c};
-    const RowComm* comm = c->nccl_comm ? &rc : nullptr;
+    const RowComm* comm = has_comm(c) ? &rc : nullptr;
+    // Every rank's arguments are checked locally, then the ranks agree (one
+    // small allreduce) so an invalid shard fails on EVERY rank before any
+    // data collective instead of leaving its peers waiting.
+    int code = 0;
+    std::string msg;
+    if (m < 0 || n < 0) code = SVDK_E_DIM, msg = "fit_pca: negative dimension";
+    else if (lda < std::max<int64_t>(m, 1)) code = SVDK_E_DIM, msg = "fit_pca: lda < rows";
+    else if (m > 0 && n > 0 && !A) code = SVDK_E_PARAM, msg = "fit_pca: null A";
+    if (comm) {
+        // also agree on the replicated arguments (n, method, l, q, centring)
+        const double mine[5] = {static_cast<double>(n), static_cast<double>(method), static_cast<double>(l),
+                                static_cast<double>(q), static_cast<double>(center_mode)};
+        DBuf d(c, 5), s(c, 5);
+        h2d(c, d.p(), mine, 5);
+        copy_mat(c, d.p(), 5, s.p(), 5, 5, 1);
+        comm->broadcast(s.p(), 5, 0);
+        double root[5];
+        d2h(c, root, s.p(), 5);
+        if (!code && std::memcmp(root, mine, sizeof(mine)) != 0)
+            code = SVDK_E_PARAM, msg = "fit_pca: n / method / l / q / center differ from rank 0's";
+        agree_status(c, comm, code, msg);
+    } else if (code) {
+        fail(code, msg);
+    }
+    try {
+        dev_pca_body(c, comm, A, m, n, lda, method, l, q, seed, center_mode, threshold, U, ldu, sigma, V, ldv,
+                     mean, rank, k, total);
+    } catch (const Failure& f) {
+        // Validation that depends only on replicated values (n, l, q, global
+        // rows) fails identically on every rank; anything else (a CUDA error,
+        // a kernel's non-finite flag on one shard) must not strand the peers.
+        if (comm && !f.agreed && f.code != SVDK_E_PARAM && f.code != SVDK_E_DIM) abort_comm(c, f.msg);
+        throw;
+    }
+}
+
+namespace {
+void dev_pca_body(Ctx* c, const RowComm* comm, const double* A, int64_t m, int64_t n, int64_t lda, int method,
+                  int64_t l, int64_t q, uint64_t seed, int center_mode, double threshold, double* U,
+                  int64_t ldu, double* sigma, double* V, int64_t ldv, double* mean, int64_t* rank, int64_t* k,
+                  double* total) {
+    const bool center = center_mode != 0, center_in_place = center_mode == 2;
     const int world = comm ? comm->world() : 1;
     // The reference sampler's Omega (or Lanczos v0) is generated on a host
     // thread while the device centres A and forms the total variance.
@@ -199,5 +247,6 @@ void dev_pca(Ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, int met
     raise_if_nonfinite(c);
     *k = select_components_dev(c, w.p(), r, d_total.p(), threshold, total);
 }
+}  // namespace
 
 }  // namespace svdk

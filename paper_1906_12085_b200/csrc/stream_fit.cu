@@ -262,7 +262,7 @@ bool fit_pca_streamed(Ctx* c, const double* host, int64_t m, int64_t n, int meth
     if (const char* e = std::getenv("SVDK_STREAM"))
         if (std::string(e) == "0") return false;
     if (method != SVDK_TRUNCATED && method != SVDK_RANDOMIZED) return false;
-    if (m < n || n == 0 || (c->nccl_comm && c->world > 1)) return false;
+    if (m < n || n == 0 || has_comm(c)) return false;
     if (!c->copy_stream) {
         SVDK_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
         SVDK_CUDA(cudaEventCreateWithFlags(&c->copy_ev, cudaEventDisableTiming));

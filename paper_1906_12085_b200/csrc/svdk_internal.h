@@ -27,9 +27,12 @@ struct Failure {
     int code;
     std::string msg;
     double residual = 0.0;
+    bool agreed = false;  // raised identically on every rank (in-band status exchange)
 };
 
 [[noreturn]] void fail(int code, const std::string& msg, double residual = 0.0);
+// the same, for a status every rank of a sharded call has agreed on
+[[noreturn]] void fail_agreed(int code, const std::string& msg, double residual = 0.0);
 
 #define SVDK_CUDA(call)                                                                   \
     do {                                                                                  \
@@ -72,6 +75,7 @@ private:
 };
 
 struct Ctx;
+struct HostGroup;  // in-process collective group (comm.cu)
 
 // RAII device buffer of doubles from the context pool.
 class DBuf {
@@ -124,7 +128,8 @@ struct Ctx {
     int* d_flags = nullptr;  // [0] non-finite flag, [1] jacobi status, ...
     double* d_scalars = nullptr;
     // multi-GPU (row-sharded) state
-    void* nccl_comm = nullptr;
+    void* nccl_comm = nullptr;       // NCCL backend (one process per GPU)
+    HostGroup* host_group = nullptr;  // host-staged backend (ranks = host threads)
     int rank = 0, world = 1;
     // pinned host staging for the reference Gaussian sampler (Omega, v0),
     // filled by an asynchronous host job that overlaps device work

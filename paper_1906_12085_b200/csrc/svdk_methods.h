@@ -8,10 +8,11 @@
 
 namespace svdk {
 
-// Row-sharded execution: A is split by rows over `world` GPUs (one process
-// each). Every reduction over the row index (Gram, A^T Y, column sums,
-// norms) is followed by an NCCL allreduce over NVLink; the n x n eigensolve
-// runs on rank 0 and its result is broadcast. nullptr = single GPU.
+// Row-sharded execution: A is split by rows over `world` ranks (NCCL: one
+// process per GPU; host group: host threads of one process). Every reduction
+// over the row index (Gram, A^T Y, column sums, norms) is followed by an
+// allreduce; the n x n eigensolve runs on rank 0 and its result is
+// broadcast. nullptr = single GPU. Backends in comm.cu.
 struct RowComm {
     Ctx* c;
     void allreduce(double* buf, size_t count) const;
@@ -33,7 +34,16 @@ void eig_sym_rows(Ctx* c, const double* S, int64_t lds, int64_t n, double* w, do
 
 void nccl_unique_id(char out[128]);
 void attach_nccl(Ctx* c, const char id[128], int rank, int world);
+HostGroup* host_group_create(int world);
+void host_group_release(HostGroup* g);
+void attach_host_group(Ctx* c, HostGroup* g, int rank);
 void destroy_comm(Ctx* c);
+// true when a communicator (NCCL or host group) with world > 1 is attached
+bool has_comm(const Ctx* c);
+// make the peers fail instead of waiting forever (a rank's call failed)
+void abort_comm(Ctx* c, const std::string& why);
+// raise `code` on every rank if any rank's code is non-zero (before data collectives)
+void agree_status(Ctx* c, const struct RowComm* comm, int code, const std::string& msg);
 
 // Total of squares over all row shards into a device scalar (no host sync).
 void frob_sq_rows_dev(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n, double* d_out,

@@ -111,14 +111,18 @@ class Engine:
     def pca(self, a, method: int = 0, l: int = 0, q: int = 0, seed: int = 0, center=True,
             threshold: float = 0.95, out: PcaOutput | None = None) -> PcaOutput:
         """Full RowsAreExamples PCA on a device-resident (row shard of) A.
-        center: True/1 centre a copy, 2 centre A in place (overwrites A), False/0 none."""
+        center: True/1 centre a copy, 2 centre A in place (overwrites A), False/0 none.
+        The call returns after the engine's stream has produced K (the outputs
+        are complete); the other entry points are asynchronous on ``self.stream``."""
         m, n = a.shape
         width = {1: l, 2: min((q + 1) * l, n), 3: (n if l <= 0 or l > n else l)}.get(int(method), n)
         width = max(width, 1)
         if out is None:
-            out = PcaOutput(colmajor(m, width, a.device), torch.empty(max(width, n), dtype=torch.float64, device=a.device),
-                            colmajor(n, width, a.device, ld=n), torch.empty(n, dtype=torch.float64, device=a.device),
-                            0, None, 0.0)
+            with torch.cuda.stream(self.stream):  # outputs belong to the engine's stream
+                out = PcaOutput(colmajor(m, width, a.device),
+                                torch.empty(max(width, n), dtype=torch.float64, device=a.device),
+                                colmajor(n, width, a.device, ld=n), torch.empty(n, dtype=torch.float64, device=a.device),
+                                0, None, 0.0)
         rank, k, total = C.c_int64(0), C.c_int64(0), C.c_double(0.0)
         _lib.check(self.lib.svdk_dev_pca(self.ctx.handle, _p(a), m, n, _ld(a), int(method), int(l), int(q),
                                          int(seed) & (2**64 - 1), int(center), float(threshold),

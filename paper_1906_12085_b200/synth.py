@@ -142,7 +142,8 @@ def config_host_matrix(cfg: Config | str, seed: int = MATRIX_SEED, row0: int = 0
 def device_gram_x(eng, m_total: int, n: int, seed: int = MATRIX_SEED, row0: int = 0,
                   rows: int | None = None, chunk: int = 1 << 20):
     """X^T X over rows [row0, row0+rows) of the quantised stream, in HBM
-    (svdk_dev_synth_fill + the engine's DMMA SYRK; exact)."""
+    (svdk_dev_synth_fill + the engine's DMMA SYRK; exact). Everything runs on
+    the engine's stream; the result is complete when this returns."""
     import torch
 
     from .engine import colmajor
@@ -150,21 +151,25 @@ def device_gram_x(eng, m_total: int, n: int, seed: int = MATRIX_SEED, row0: int 
     rows = m_total - row0 if rows is None else rows
     dev = torch.device("cuda", eng.device)
     chunk = max(2, min(chunk, max(rows, 2)) & ~1)
-    x = colmajor(chunk, n, dev)
-    g = torch.zeros(n, n, dtype=torch.float64, device=dev)
-    gpart = torch.empty(n, n, dtype=torch.float64, device=dev)
-    for r0 in range(0, rows, chunk):
-        r = min(chunk, rows - r0)
-        _check(lib.svdk_dev_synth_fill(eng.ctx.handle, seed, STREAM_X, 1, m_total, row0 + r0, r, n,
-                                       _vp(x), x.stride(1)))
-        eng.gram(x[:r], gpart.t())
-        g += gpart
+    with torch.cuda.stream(eng.stream):
+        x = colmajor(chunk, n, dev)
+        g = torch.zeros(n, n, dtype=torch.float64, device=dev)
+        gpart = torch.empty(n, n, dtype=torch.float64, device=dev)
+        for r0 in range(0, rows, chunk):
+            r = min(chunk, rows - r0)
+            _check(lib.svdk_dev_synth_fill(eng.ctx.handle, seed, STREAM_X, 1, m_total, row0 + r0, r, n,
+                                           _vp(x), x.stride(1)))
+            eng.gram(x[:r], gpart.t())
+            g += gpart
+        del x, gpart
+    eng.stream.synchronize()
     return g
 
 
 def device_rows(eng, mix: np.ndarray, m_total: int, n: int, sigma: float, seed: int = MATRIX_SEED,
                 row0: int = 0, rows: int | None = None, out=None, chunk: int = 1 << 20):
-    """Rows [row0, row0+rows) of A = X M + sigma N in HBM, given the mixing matrix."""
+    """Rows [row0, row0+rows) of A = X M + sigma N in HBM, given the mixing
+    matrix (engine stream; complete when this returns)."""
     import torch
 
     from .engine import colmajor
@@ -172,17 +177,20 @@ def device_rows(eng, mix: np.ndarray, m_total: int, n: int, sigma: float, seed: 
     rows = m_total - row0 if rows is None else rows
     dev = torch.device("cuda", eng.device)
     chunk = max(2, min(chunk, max(rows, 2)) & ~1)
-    x = colmajor(chunk, n, dev)
-    mdev = torch.from_numpy(np.ascontiguousarray(np.asfortranarray(mix).T)).to(dev).t()  # column-major
-    a = colmajor(rows, n, dev) if out is None else out
-    for r0 in range(0, rows, chunk):
-        r = min(chunk, rows - r0)
-        _check(lib.svdk_dev_synth_fill(eng.ctx.handle, seed, STREAM_X, 1, m_total, row0 + r0, r, n,
-                                       _vp(x), x.stride(1)))
-        eng.gemm(x[:r], mdev, c=a[r0:r0 + r])
-    if sigma and rows:
-        _check(lib.svdk_dev_synth_add_noise(eng.ctx.handle, seed, m_total, row0, rows, n, float(sigma),
-                                            _vp(a), a.stride(1)))
+    with torch.cuda.stream(eng.stream):
+        x = colmajor(chunk, n, dev)
+        mdev = torch.from_numpy(np.ascontiguousarray(np.asfortranarray(mix).T)).to(dev).t()  # column-major
+        a = colmajor(rows, n, dev) if out is None else out
+        for r0 in range(0, rows, chunk):
+            r = min(chunk, rows - r0)
+            _check(lib.svdk_dev_synth_fill(eng.ctx.handle, seed, STREAM_X, 1, m_total, row0 + r0, r, n,
+                                           _vp(x), x.stride(1)))
+            eng.gemm(x[:r], mdev, c=a[r0:r0 + r])
+        if sigma and rows:
+            _check(lib.svdk_dev_synth_add_noise(eng.ctx.handle, seed, m_total, row0, rows, n, float(sigma),
+                                                _vp(a), a.stride(1)))
+        del x, mdev
+    eng.stream.synchronize()
     return a
 
 
@@ -194,9 +202,11 @@ def device_matrix(eng, m_total: int, n: int, s: np.ndarray, sigma: float, seed: 
     = X M by its DMMA GEMM — all exact — then the noise). Multi-rank: pass
     the rank's row range and ``allreduce(tensor)`` summing the n x n partial
     Gram over ranks (exact on the grid). Returns a column-major tensor."""
+    import torch
     g = device_gram_x(eng, m_total, n, seed, row0, rows, chunk)
     if allreduce is not None:
         allreduce(g)
+        torch.cuda.synchronize(g.device)
     mix, _ = mixing(g.cpu().numpy(), s, seed)
     del g
     return device_rows(eng, mix, m_total, n, sigma, seed, row0, rows, out, chunk)

@@ -11,7 +11,7 @@ import numpy as np
 import pytest
 
 from paper_1906_12085_b200 import errors
-from tests.datagen import make_matrix
+from tests.datagen import config_matrix
 from tests.parity import eig_rel_err, orthogonality, per_vector_sines, subspace_sine
 
 pytestmark = pytest.mark.gpu
@@ -76,7 +76,7 @@ def test_small_golden_all_methods(sk):
 def test_c1_fit_pca_vs_reference(sk, method):
     """BASELINE config 1 (20000 x 256, t = 0.95) through fit_pca + select_components."""
     gz = golden("c1.npz")
-    a = make_matrix(20000, 256, "c1", seed=int(gz["seed"]))
+    a = config_matrix("c1", seed=int(gz["seed"]))
     key = "truncated" if method == "lanczos" else method
     l, q, rs = (int(x) for x in gz[f"{key}_params"])
     enum = {"truncated": sk.SvdMethod.Truncated, "randomized": sk.SvdMethod.Randomized,
@@ -102,7 +102,7 @@ def test_fit_pca_streamed_upload(sk, monkeypatch, method):
     correction to the global mean); same golden bars as the plain path; then a matrix with large
     column means (|mu| ~ 1e3 x the spread) against the plain path."""
     gz = golden("c1.npz")
-    a = make_matrix(20000, 256, "c1", seed=int(gz["seed"]))
+    a = config_matrix("c1", seed=int(gz["seed"]))
     l, q, rs = (int(x) for x in gz[f"{method}_params"])
     enum = sk.SvdMethod.Truncated if method == "truncated" else sk.SvdMethod.Randomized
     params = sk.MethodParams(l, q, sk.RngSeed(rs))
@@ -130,24 +130,6 @@ def test_fit_pca_streamed_upload(sk, monkeypatch, method):
     assert eig_rel_err(streamed.eigenvalues, plain.eigenvalues) <= 1e-10
     kk = sk.select_components(plain.eigenvalues, plain.total_variance, 0.95)
     assert subspace_sine(streamed.basis[:, :kk], plain.basis[:, :kk]) <= 1e-8
-
-
-def test_c2mid_golden(sk):
-    """c2's spectrum/method (l = n = 1024, q = 2, t = 0.99) at 20000 rows vs the reference."""
-    gz = golden("c2mid.npz")
-    a = make_matrix(int(gz["m"]), int(gz["n"]), "c2", seed=int(gz["seed"]))
-    for key, enum in (("truncated", sk.SvdMethod.Truncated), ("randomized", sk.SvdMethod.Randomized),
-                      ("lanczos", sk.SvdMethod.Lanczos)):
-        src = "truncated" if key == "lanczos" else key
-        l, q, rs = (int(x) for x in gz[f"{src}_params"])
-        model = sk.fit_pca(a, sk.Orientation.RowsAreExamples, enum,
-                           sk.MethodParams(0 if key == "lanczos" else l, q, sk.RngSeed(rs)), True)
-        lam_ref, v_ref = gz[f"{src}_lambda"], gz[f"{src}_v"]
-        assert eig_rel_err(model.eigenvalues, lam_ref) <= 1e-10, key
-        k = sk.select_components(model.eigenvalues, model.total_variance, float(gz["threshold"]))
-        assert k == int(gz[f"{src}_k"]), key
-        kk = v_ref.shape[1]
-        assert subspace_sine(model.basis[:, :kk], v_ref) <= 1e-8, key
 
 
 def test_live_oracle_random_shapes(sk, ref):
