@@ -211,6 +211,110 @@ __global__ void eig_invsqrt_kernel(const double* w, int64_t p, double tau, doubl
         scale[i] = w[i] > tau ? 1.0 / sqrt(w[i]) : 0.0;
 }
 
+// Householder QR of a small p x p matrix W (column-major, ld p, in place) with
+// the reference's column dropping, sign convention and thin-Q formation
+// (kernels.cpp:111-224, restated for one CTA): a column whose residual norm is
+// <= drop_tol = 1e-12 ||W||_F is zeroed and keeps R(k, k) = 0; R's diagonal is
+// made non-negative by flipping rows of R and columns of Q. On exit W holds R
+// (upper; lower part zeroed), Qs the p x p thin Q, Vs the reflectors,
+// meta[0] = rank. Used by the rank-deficient qr_thin fallback on R0 = Q0^T H,
+// whose column residual norms are those of H (Q0 is an isometry on range(H)).
+constexpr int HH_THREADS = 1024;
+__global__ void __launch_bounds__(HH_THREADS)
+    householder_small_kernel(double* W, int p, double* Vs, double* Qs, double* betas, int* meta) {
+    __shared__ double red[HH_THREADS / 32];
+    __shared__ double s_tol;
+    __shared__ int s_rank;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = HH_THREADS / 32;
+    auto block_sum = [&](double x) {
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        __syncthreads();
+        if (lane == 0) red[warp] = x;
+        __syncthreads();
+        double t = 0.0;
+        if (warp == 0) {
+            t = lane < nwarps ? red[lane] : 0.0;
+            for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+            if (lane == 0) red[0] = t;
+        }
+        __syncthreads();
+        return red[0];
+    };
+    const int64_t pp = static_cast<int64_t>(p) * p;
+    double fro = 0.0;
+    for (int64_t e = tid; e < pp; e += HH_THREADS) fro = fma(W[e], W[e], fro);
+    fro = block_sum(fro);
+    if (tid == 0) {
+        s_tol = 1e-12 * sqrt(fro);
+        s_rank = 0;
+    }
+    __syncthreads();
+    for (int k = 0; k < p; ++k) {
+        double* wk = W + static_cast<int64_t>(k) * p;
+        double ns = 0.0;
+        for (int i = k + tid; i < p; i += HH_THREADS) ns = fma(wk[i], wk[i], ns);
+        ns = block_sum(ns);
+        const double alpha = sqrt(ns);
+        if (alpha <= s_tol) {  // residual too small to trust: R(k, k) = 0
+            for (int i = k + tid; i < p; i += HH_THREADS) wk[i] = 0.0;
+            if (tid == 0) betas[k] = 0.0;
+            __syncthreads();
+            continue;
+        }
+        const double sign = wk[k] >= 0.0 ? 1.0 : -1.0;
+        double* vk = Vs + static_cast<int64_t>(k) * p;
+        double vt = 0.0;
+        for (int i = k + tid; i < p; i += HH_THREADS) {
+            const double v = i == k ? wk[i] + sign * alpha : wk[i];
+            vk[i] = v;
+            vt = fma(v, v, vt);
+        }
+        vt = block_sum(vt);
+        const double beta = 2.0 / vt;
+        if (tid == 0) {
+            betas[k] = beta;
+            ++s_rank;
+        }
+        // apply to the remaining columns, one warp per column
+        for (int j = k + 1 + warp; j < p; j += nwarps) {
+            double* wj = W + static_cast<int64_t>(j) * p;
+            double d = 0.0;
+            for (int i = k + lane; i < p; i += 32) d = fma(vk[i], wj[i], d);
+            for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+            const double sc = beta * d;
+            for (int i = k + lane; i < p; i += 32) wj[i] = fma(-sc, vk[i], wj[i]);
+        }
+        // the reflector maps column k onto -sign alpha e_k: store it exactly
+        for (int i = k + tid; i < p; i += HH_THREADS) wk[i] = i == k ? -sign * alpha : 0.0;
+        __syncthreads();
+    }
+    // thin Q: the reflectors applied in reverse to the first p identity columns
+    for (int64_t e = tid; e < pp; e += HH_THREADS) Qs[e] = (e % p) == (e / p) ? 1.0 : 0.0;
+    __syncthreads();
+    for (int k = p - 1; k >= 0; --k) {
+        const double beta = betas[k];
+        if (beta == 0.0) continue;
+        const double* vk = Vs + static_cast<int64_t>(k) * p;
+        for (int j = warp; j < p; j += nwarps) {
+            double* qj = Qs + static_cast<int64_t>(j) * p;
+            double d = 0.0;
+            for (int i = k + lane; i < p; i += 32) d = fma(vk[i], qj[i], d);
+            for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+            const double sc = beta * d;
+            for (int i = k + lane; i < p; i += 32) qj[i] = fma(-sc, vk[i], qj[i]);
+        }
+        __syncthreads();
+    }
+    // sign convention: non-negative diagonal of R (flip row k of R, column k of Q)
+    for (int k = warp; k < p; k += nwarps) {
+        if (W[k + static_cast<int64_t>(k) * p] < 0.0) {
+            for (int j = k + lane; j < p; j += 32) W[k + static_cast<int64_t>(j) * p] = -W[k + static_cast<int64_t>(j) * p];
+            for (int i = lane; i < p; i += 32) Qs[i + static_cast<int64_t>(k) * p] = -Qs[i + static_cast<int64_t>(k) * p];
+        }
+    }
+    if (tid == 0) meta[0] = s_rank;
+}
+
 int read_flag(Ctx* c, int idx) {
     int f = 0;
     SVDK_CUDA(cudaMemcpyAsync(&f, c->d_flags + idx, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
@@ -417,9 +521,27 @@ int64_t qr_thin(Ctx* c, const double* H, int64_t ldh, int64_t m, int64_t p, doub
         if (ok) ok = cholqr_pass(c, Q1.p(), ldw, m, pc, Q + r * ldq, ldq, R1.p(), 0.0, 0.0, comm);
         if (!ok) fail(SVDK_E_NUMERICAL, "qr_thin: completion of a rank-deficient basis failed", 0.0);
     }
-    if (R) gemm_tn_rows(c, p, p, m, Q, ldq, H, ldh, R, p, comm);  // R = Q^T H
+    // Q0 (orthonormal, spans range(H)) -> the reference's triangular factorisation:
+    // R0 = Q0^T H, Householder QR of R0 with the reference's dropping and signs
+    // (R0 = Q1 R), Q = Q0 Q1. Then Q R = Q0 R0 = H, R is upper triangular with
+    // R(k, k) = 0 on dropped columns, and rank counts the kept columns as the
+    // reference does (kernels.cpp:127-139, 173-182).
+    DBuf R0(c, static_cast<size_t>(p) * p), Vs(c, static_cast<size_t>(p) * p), Qs(c, static_cast<size_t>(p) * p),
+        betas(c, p), meta(c, 1);
+    gemm_tn_rows(c, p, p, m, Q, ldq, H, ldh, R0.p(), p, comm);
+    householder_small_kernel<<<1, HH_THREADS, 0, c->stream>>>(R0.p(), static_cast<int>(p), Vs.p(), Qs.p(),
+                                                             betas.p(), reinterpret_cast<int*>(meta.p()));
+    SVDK_CHECK_LAUNCH();
+    c->launches++;
+    int rank_hh = 0;
+    SVDK_CUDA(cudaMemcpyAsync(&rank_hh, meta.p(), sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    gemm(c, false, m, p, p, Q, ldq, Qs.p(), p, W.p(), ldw);
+    copy_mat(c, W.p(), ldw, Q, ldq, m, p);
+    if (R) copy_mat(c, R0.p(), p, R, p, p, p);
     if (Rinv_last) set_identity(c, Rinv_last, p, p);  // explicit Q: implicit factor I
-    return r;
+    SVDK_CUDA(cudaStreamSynchronize(c->stream));
+    (void)r;
+    return rank_hh;
 }
 
 }  // namespace svdk

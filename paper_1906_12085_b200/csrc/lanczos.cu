@@ -861,6 +861,8 @@ void GemvPair::run(const double* q, double* w, bool reduce) {
     }
 }
 
+bool tridiag_eig(Ctx* c, const double* alpha, const double* beta, int64_t k, double* w, double* S, int64_t lds);
+
 int64_t lanczos_svd(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n, int64_t steps,
                     uint64_t seed, double* U, int64_t ldu, double* sigma, double* V, int64_t ldv,
                     const RowComm* comm) {
@@ -917,15 +919,24 @@ int64_t lanczos_svd(Ctx* c, const double* A, int64_t lda, int64_t m, int64_t n, 
         SVDK_CHECK_LAUNCH();
         c->launches += 6;
     }
-    // Ritz pairs: eig(T), V = Q_L S
-    DBuf T(c, static_cast<size_t>(steps) * steps), theta(c, steps), S(c, static_cast<size_t>(steps) * steps);
-    tridiag_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(steps * steps, 256), 1024)), 256,
-                     0, c->stream>>>(alpha, beta, steps, T.p());
-    SVDK_CHECK_LAUNCH();
-    c->launches++;
-    eig_sym(c, T.p(), steps, steps, 30, theta.p(), S.p(), steps);
+    // Ritz pairs: eig(T) by the O(k^2) tridiagonal solver (bisection + twisted
+    // factorisation, tridiag.cu); T with unresolved clusters (e.g. the repeated
+    // Ritz values after a breakdown restart) goes to the dense Jacobi solver.
+    const int64_t lds = round_up(steps, 2);
+    DBuf theta(c, steps), S(c, static_cast<size_t>(lds) * steps);
+    const char* tri_env = std::getenv("SVDK_LANCZOS_TRIDIAG");
+    const bool try_tri = !(tri_env && std::atoi(tri_env) == 0);
+    if (!try_tri || !tridiag_eig(c, alpha, beta, steps, theta.p(), S.p(), lds)) {
+        PhaseTimer timer(c, "tridiag_dense");
+        DBuf T(c, static_cast<size_t>(steps) * steps);
+        tridiag_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(steps * steps, 256), 1024)), 256,
+                         0, c->stream>>>(alpha, beta, steps, T.p());
+        SVDK_CHECK_LAUNCH();
+        c->launches++;
+        eig_sym(c, T.p(), steps, steps, 30, theta.p(), S.p(), lds);
+    }
     DBuf Vr(c, static_cast<size_t>(n) * steps);
-    gemm(c, false, n, steps, steps, Q.p(), n, S.p(), steps, Vr.p(), n);
+    gemm(c, false, n, steps, steps, Q.p(), n, S.p(), lds, Vr.p(), n);
     Q.reset();
     return back_project(c, A, lda, m, n, theta.p(), Vr.p(), n, steps, U, ldu, sigma, V, ldv);
 }

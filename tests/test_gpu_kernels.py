@@ -166,16 +166,27 @@ def test_qr_kats(sk):
     assert np.allclose(r.q[:, 1], [-0.40824829046386296, 0.40824829046386302, 0.81649658092772603], atol=1e-15)
 
 
-def test_qr_rank_deficient(sk):
+def test_qr_rank_deficient(sk, ref):
+    """Exactly rank-deficient H: the reference contract (kernels.cpp:127-139,
+    173-182) — R upper triangular with R(k, k) = 0 on the dropped columns and
+    a non-negative diagonal, rank = kept columns, Q orthonormal, Q R = H — and
+    the rows of R before the first dropped column equal the reference's."""
     rng = np.random.default_rng(11)
     b = rng.standard_normal((400, 5))
     h = np.asfortranarray(np.hstack([b, b[:, :2] @ rng.standard_normal((2, 3)), np.zeros((400, 1))]))
     r = sk.qr_thin(h)
-    assert r.rank == 5
+    q_ref, r_ref, rank_ref = ref.qr_thin(h)
+    assert r.rank == rank_ref == 5
     assert np.max(np.abs(r.q.T @ r.q - np.eye(9))) <= 1e-12
     assert np.linalg.norm(r.q @ r.r - h) <= 1e-12 * np.linalg.norm(h)
+    assert np.array_equal(np.tril(r.r, -1), np.zeros((9, 9)))
+    assert np.all(np.diag(r.r) >= 0.0)
+    assert np.array_equal(np.diag(r.r) == 0.0, np.diag(r_ref) == 0.0)
+    assert np.max(np.abs(r.r[:5] - r_ref[:5])) <= 1e-12 * np.linalg.norm(h)
+    assert np.max(np.abs(r.q[:, :5] - q_ref[:, :5])) <= 1e-12
     z = sk.qr_thin(np.zeros((10, 3)))
     assert z.rank == 0 and np.max(np.abs(z.q.T @ z.q - np.eye(3))) <= 1e-12
+    assert np.array_equal(z.r, np.zeros((3, 3)))
 
 
 def test_qr_ill_conditioned(sk):

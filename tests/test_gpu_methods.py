@@ -213,3 +213,19 @@ def test_lanczos_breakdown_restart(sk, ref):
         assert np.all(s.sigma[rank:] <= 1e-6 * s.sigma[0])
         assert subspace_sine(s.v[:, :rank], r.v[:, :rank]) <= 1e-8
         assert orthogonality(s.v) <= 1e-10 and orthogonality(s.u[:, :rank]) <= 1e-8
+
+
+def test_lanczos_tridiagonal_solver_matches_dense(sk, monkeypatch):
+    """The O(k^2) tridiagonal eigensolver (bisection + twisted factorisation +
+    CholeskyQR certification, tridiag.cu) against the dense Jacobi solve of
+    the same Lanczos T (SVDK_LANCZOS_TRIDIAG=0), on c2's spectrum."""
+    from tests.datagen import make_matrix
+    a = make_matrix(6000, 512, "c2", seed=5)
+    fast = sk.lanczos_svd(a, 0, sk.RngSeed(3))
+    monkeypatch.setenv("SVDK_LANCZOS_TRIDIAG", "0")
+    dense = sk.lanczos_svd(a, 0, sk.RngSeed(3))
+    assert fast.rank == dense.rank
+    assert eig_rel_err(fast.sigma ** 2, dense.sigma ** 2) <= 1e-12
+    single, cluster = per_vector_sines(fast.v, dense.sigma ** 2, dense.v)
+    assert single <= 1e-9 and cluster <= 1e-9
+    assert orthogonality(fast.v) <= 1e-12

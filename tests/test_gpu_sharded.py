@@ -105,10 +105,11 @@ def test_sharded_matches_single(base, method, layout):
         kk = one.k
         assert subspace_sine(v[:, :kk], v1[:, :kk]) <= 1e-10
         assert abs(o.total - one.total) <= 1e-13 * one.total
-    # the stacked U shards span the single-GPU U's top-K subspace, with the same signs
+    # the stacked U shards span the single-GPU U's top-K subspace, with the same
+    # signs (the sketch methods' U = Q W carries CholeskyQR's ~1e-10 rounding)
     u = np.vstack([o.u[:, :o.rank].cpu().numpy() for o in outs])
     kk = one.k
-    assert topk_sine(u[:, :kk], u1[:, :kk]) <= 1e-10
+    assert topk_sine(u[:, :kk], u1[:, :kk]) <= (1e-10 if method in ("truncated", "lanczos") else 1e-8)
     assert np.all(np.sum(u[:, :kk] * u1[:, :kk], axis=0) > 0.5)
 
 
