@@ -29,7 +29,10 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <functional>
+#include <memory>
 #include <string>
+#include <vector>
 
 #include "svdk_internal.h"
 
@@ -348,7 +351,7 @@ __global__ void jacobi_tables_kernel(SolveTables<TB>* out) {
 template <int TB>
 __device__ __forceinline__ void solve_pair(const double* A, int64_t lda, const SolveTables<TB>* tabs,
                                            double* Qbuf, int* active, int nb, int round,
-                                           double skip_tau, int max_inner, int mode, int pair) {
+                                           const double* skip_tau_p, int max_inner, int mode, int pair) {
     // mode 0: all pairs of the 2b subproblem (2b-1 rounds of b rotations);
     // mode 1: only the pairs inside block I and inside block J (b-1 rounds);
     // mode 2: only the b^2 cross pairs (i in I, j in J) (b rounds).
@@ -389,6 +392,7 @@ __device__ __forceinline__ void solve_pair(const double* A, int64_t lda, const S
         for (int e = tid; e < static_cast<int>(sizeof(SolveTables<TB>) / 16); e += NT) dst[e] = src[e];
     }
     pdl_wait();  // A (and the Q / active slots) of the previous round's update
+    const double skip_tau = *skip_tau_p;  // written before the sweep (jacobi_start_kernel)
     bool big = false;
     {
         double xv[PER];
@@ -549,11 +553,13 @@ __device__ __forceinline__ void solve_pair(const double* A, int64_t lda, const S
     __syncthreads();  // shared memory is reused by the next pair / phase
 }
 
+// skip_tau is read from device memory (written by the sweep setup before the
+// sweep graph runs), so one instantiated graph serves every eig_sym call.
 template <int TB>
 __global__ void __launch_bounds__(solve_threads<TB>())
     jacobi_pair_solve(const double* A, int64_t lda, const SolveTables<TB>* tabs, double* Qbuf,
-                      int* active, int nb, int round, double skip_tau, int max_inner, int mode) {
-    solve_pair<TB>(A, lda, tabs, Qbuf, active, nb, round, skip_tau, max_inner, mode, blockIdx.x);
+                      int* active, int nb, int round, const double* skip_tau_p, int max_inner, int mode) {
+    solve_pair<TB>(A, lda, tabs, Qbuf, active, nb, round, skip_tau_p, max_inner, mode, blockIdx.x);
 }
 
 
@@ -1104,7 +1110,8 @@ __global__ void symcheck_kernel(const double* S, int64_t lds, int64_t n, double*
 
 // A (n_pad x n_pad) = (S + S^T)/2 zero padded; V = I.
 __global__ void jacobi_init_kernel(const double* S, int64_t lds, int64_t n, double* A, double* V,
-                                   int64_t n_pad, double scale) {
+                                   int64_t n_pad, const double* scale_p) {
+    const double scale = *scale_p;
     for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n_pad * n_pad;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int64_t j = e / n_pad, i = e - j * n_pad;
@@ -1133,20 +1140,13 @@ __global__ void jacobi_sumsq_kernel(const double* A, int64_t n, int mode, double
     }
 }
 
-__global__ void sum_fixed_kernel(const double* partial, int count, double* out) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) {
-        double s = 0.0;
-        for (int i = 0; i < count; ++i) s += partial[i];
-        *out = s;
-    }
-}
-
 // Stable descending order by rank counting: rank_i = #{j : l_j > l_i or
 // (l_j == l_i and j < i)} — exactly std::stable_sort's permutation.
-__global__ void eig_sort_kernel(const double* A, int64_t n_pad, int64_t n, double unscale,
+__global__ void eig_sort_kernel(const double* A, int64_t n_pad, int64_t n, const double* unscale_p,
                                 double* w, int* dest) {
     const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (i >= n) return;
+    const double unscale = *unscale_p;
     const double li = A[i + i * n_pad];
     int64_t rank = 0;
     for (int64_t j = 0; j < n; ++j) {
@@ -1167,81 +1167,173 @@ __global__ void eig_gather_kernel(const double* V, int64_t n_pad, int64_t n, con
     }
 }
 
-double device_sumsq(Ctx* c, const double* A, int64_t n, int mode, DBuf& scratch) {
-    const int blocks = static_cast<int>(
-        std::max<int64_t>(1, std::min<int64_t>(ceil_div(n * n, 256), 2 * c->num_sms)));
-    jacobi_sumsq_kernel<<<blocks, 256, 0, c->stream>>>(A, n, mode, scratch.p());
-    SVDK_CHECK_LAUNCH();
-    sum_fixed_kernel<<<1, 32, 0, c->stream>>>(scratch.p(), blocks, scratch.p() + blocks);
-    SVDK_CHECK_LAUNCH();
-    c->launches += 2;
-    double out = 0.0;
-    d2h(c, &out, scratch.p() + blocks, 1);
-    return out;
-}
-
 // Convergence test of one sweep on the device: off = sqrt(2 sum partial)
 // (fixed order, as device_sumsq), sweep counter, and the WHILE condition of
 // the enclosing graph: keep sweeping while off > thr and sweeps < max_sweeps
 // (kernels.cpp:274-326, the host loop's exact test).
-__global__ void jacobi_decide_kernel(cudaGraphConditionalHandle h, const double* partial, int count, double thr,
-                                     int max_sweeps, double* state) {
+// Device scalars of a sweep loop (JS_* slots of `scal`), written by
+// jacobi_start_kernel / eig_prep_kernel and read by the sweep kernels, so the
+// instantiated graphs never bake a per-call value.
+enum { JS_THR = 0, JS_SKIP, JS_OFF, JS_SWEEPS, JS_SCALE, JS_UNSCALE, JS_MABS, JS_MASYM, JS_MAXSW, JS_FRO,
+       JS_COUNT };
+
+__global__ void jacobi_decide_kernel(cudaGraphConditionalHandle h, const double* partial, int count,
+                                     double* scal, int use_cond) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     double s = 0.0;
     for (int i = 0; i < count; ++i) s += partial[i];
     const double off = sqrt(2.0 * s);
-    const double sw = state[1] + 1.0;
-    state[0] = off;
-    state[1] = sw;
-    cudaGraphSetConditional(h, (off > thr && sw < static_cast<double>(max_sweeps)) ? 1u : 0u);
+    const double sw = scal[JS_SWEEPS] + 1.0;
+    scal[JS_OFF] = off;
+    scal[JS_SWEEPS] = sw;
+    if (use_cond) cudaGraphSetConditional(h, (off > scal[JS_THR] && sw < scal[JS_MAXSW]) ? 1u : 0u);
 }
 
-// All sweeps of eig_sym as ONE graph launch: a WHILE conditional node whose
-// body is the captured sweep (enqueue_sweep, the same kernels and streams as
-// the per-sweep graph) followed by the off-diagonal sum of squares and
-// jacobi_decide_kernel. The host no longer reads off(A) back between sweeps
-// (one round trip per sweep: ~10 sweeps x ~20-30 us of idle GPU at small n).
-// Returns false (nothing launched) where conditional nodes are unavailable.
-template <class Enqueue>
-bool sweep_loop_graph(Ctx* c, Enqueue&& enqueue_sweep, const double* A, int64_t n_pad, double thr,
-                      int max_sweeps, DBuf& scratch, int launches_per_sweep, int& sweeps, double& off) {
+// Before the first sweep (kernels.cpp:271-274): ||A||_F from the all-entries
+// partials, thr = 1e-12 ||A||_F, the solves' skip threshold, off(A) from the
+// strictly-lower partials; sweep only if off > thr (and max_sweeps > 0).
+__global__ void jacobi_start_kernel(cudaGraphConditionalHandle h, const double* p_all, const double* p_low,
+                                    int count, double n_pad, double* scal, int use_cond) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double s0 = 0.0, s1 = 0.0;
+    for (int i = 0; i < count; ++i) s0 += p_all[i];
+    for (int i = 0; i < count; ++i) s1 += p_low[i];
+    const double fro = sqrt(s0), off = sqrt(2.0 * s1);
+    scal[JS_FRO] = fro;
+    scal[JS_THR] = 1e-12 * fro;
+    scal[JS_SKIP] = 1e-13 * fro / n_pad;
+    scal[JS_OFF] = off;
+    scal[JS_SWEEPS] = 0.0;
+    if (use_cond) cudaGraphSetConditional(h, (off > scal[JS_THR] && scal[JS_MAXSW] > 0.0) ? 1u : 0u);
+}
+
+// max|s_ij|, max|s_ij - s_ji| from symcheck_kernel's partials, the exact
+// power-of-two prescale (entries whose squares cannot over/underflow) and
+// the sweep cap, all on the device (no host round trip before the sweeps).
+__global__ void eig_prep_kernel(const double* partial, int count, int max_sweeps, double* scal) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double mabs = 0.0, masym = 0.0;
+    for (int b = 0; b < count; ++b) {
+        mabs = fmax(mabs, partial[2 * b]);
+        masym = fmax(masym, partial[2 * b + 1]);
+    }
+    int pow2 = 0;
+    if (mabs > 0.0 && (mabs > 1e100 || mabs < 1e-100)) pow2 = ilogb(mabs);
+    scal[JS_SCALE] = ldexp(1.0, -pow2);
+    scal[JS_UNSCALE] = ldexp(1.0, pow2);
+    scal[JS_MABS] = mabs;
+    scal[JS_MASYM] = masym;
+    scal[JS_MAXSW] = static_cast<double>(max_sweeps);
+}
+
+// A sweep plan: the padded work matrices, the per-round rotation slots, the
+// schedule tables and ONE instantiated graph holding every sweep of an
+// eig_sym call — a WHILE conditional node whose body is the captured sweep
+// (both streams) + the off-diagonal sum of squares + jacobi_decide_kernel,
+// preceded by jacobi_start_kernel (threshold and first convergence test,
+// kernels.cpp:271-274). Every per-call value (thresholds, prescale, sweep cap)
+// lives in device scalars, so the plan is built once per (context, n_pad,
+// scheme) and replayed by later calls: no capture / instantiation and no host
+// round trip inside eig_sym (one read of the final scalars at the end).
+}  // namespace
+
+struct JacobiPlan {
+    int64_t n_pad = 0;
+    int tb = 0;  // 16 / 32: pair scheme, 64: quad scheme
+    DBuf A, V, qbuf, act, tabs, part_all, part_low, scal;
+    int blocks = 0;  // sum-of-squares partial blocks
+    int launches_per_sweep = 0;
+    std::function<void()> enqueue_sweep;  // one sweep on (stream, aux stream)
+    cudaGraphExec_t exec = nullptr;       // nullptr: host-driven sweep loop
+    JacobiPlan() = default;
+    JacobiPlan(const JacobiPlan&) = delete;
+    JacobiPlan& operator=(const JacobiPlan&) = delete;
+    ~JacobiPlan() {
+        if (exec) cudaGraphExecDestroy(exec);
+    }
+};
+
+struct JacobiCache {
+    std::vector<std::unique_ptr<JacobiPlan>> plans;  // most recently used last
+};
+
+namespace {
+constexpr size_t kMaxPlans = 4;
+
+cudaGraphNode_t add_kernel_node(cudaGraph_t g, const cudaGraphNode_t* deps, size_t ndeps, const void* func,
+                                dim3 grid, dim3 block, void** args) {
+    cudaKernelNodeParams kp = {};
+    kp.func = const_cast<void*>(func);
+    kp.gridDim = grid;
+    kp.blockDim = block;
+    kp.sharedMemBytes = 0;
+    kp.kernelParams = args;
+    cudaGraphNode_t node = nullptr;
+    if (cudaGraphAddKernelNode(&node, g, deps, ndeps, &kp) != cudaSuccess) return nullptr;
+    return node;
+}
+
+// Build P.exec = [sumsq(all), sumsq(lower)] -> start -> WHILE{sweep, sumsq(lower), decide}.
+// Leaves P.exec null where conditional nodes are unavailable or disabled.
+void build_loop_graph(Ctx* c, JacobiPlan& P) {
     if (const char* e = std::getenv("SVDK_JACOBI_DEVLOOP"))
-        if (std::string(e) == "0") return false;
+        if (std::string(e) == "0") return;
     cudaStream_t S = c->stream;
-    if (!S) return false;
-    const int blocks = static_cast<int>(
-        std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_pad * n_pad, 256), 2 * c->num_sms)));
-    double* partial = scratch.p();
-    double* state = scratch.p() + blocks + 1;  // {off, sweeps}
+    if (!S) return;
     cudaGraph_t outer = nullptr;
-    cudaGraphExec_t exec = nullptr;
     if (cudaGraphCreate(&outer, 0) != cudaSuccess) {
         cudaGetLastError();
-        return false;
+        return;
     }
     cudaGraphConditionalHandle h;
-    cudaGraphNodeParams cp = {};
-    cudaGraphNode_t cnode;
-    if (cudaGraphConditionalHandleCreate(&h, outer, 1, cudaGraphCondAssignDefault) != cudaSuccess ||
-        (cp.type = cudaGraphNodeTypeConditional, cp.conditional.handle = h,
-         cp.conditional.type = cudaGraphCondTypeWhile, cp.conditional.size = 1,
-         cudaGraphAddNode(&cnode, outer, nullptr, 0, &cp) != cudaSuccess)) {
+    if (cudaGraphConditionalHandleCreate(&h, outer, 0, cudaGraphCondAssignDefault) != cudaSuccess) {
         cudaGetLastError();
         cudaGraphDestroy(outer);
-        return false;
+        return;
+    }
+    double* A = P.A.p();
+    int64_t n = P.n_pad;
+    int mode0 = 0, mode1 = 1;
+    double* pa = P.part_all.p();
+    double* pl = P.part_low.p();
+    double* scal = P.scal.p();
+    int blocks = P.blocks;
+    double npad_d = static_cast<double>(P.n_pad);
+    void* a0[] = {&A, &n, &mode0, &pa};
+    void* a1[] = {&A, &n, &mode1, &pl};
+    const cudaGraphNode_t s0 = add_kernel_node(outer, nullptr, 0, reinterpret_cast<const void*>(jacobi_sumsq_kernel),
+                                               dim3(blocks), dim3(256), a0);
+    const cudaGraphNode_t s1 = add_kernel_node(outer, nullptr, 0, reinterpret_cast<const void*>(jacobi_sumsq_kernel),
+                                               dim3(blocks), dim3(256), a1);
+    int use_cond = 1;
+    void* as[] = {&h, &pa, &pl, &blocks, &npad_d, &scal, &use_cond};
+    cudaGraphNode_t deps[2] = {s0, s1};
+    const cudaGraphNode_t st = (s0 && s1) ? add_kernel_node(outer, deps, 2, reinterpret_cast<const void*>(
+                                                                jacobi_start_kernel), dim3(1), dim3(32), as)
+                                          : nullptr;
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t cnode;
+    if (!st || cudaGraphAddNode(&cnode, outer, &st, 1, &cp) != cudaSuccess) {
+        cudaGetLastError();
+        cudaGraphDestroy(outer);
+        return;
     }
     cudaGraph_t body = cp.conditional.phGraph_out[0];
     if (cudaStreamBeginCaptureToGraph(S, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) !=
         cudaSuccess) {
         cudaGetLastError();
         cudaGraphDestroy(outer);
-        return false;
+        return;
     }
     cudaGraph_t captured = nullptr;
     try {
-        enqueue_sweep();
-        jacobi_sumsq_kernel<<<blocks, 256, 0, S>>>(A, n_pad, 1, partial);
-        jacobi_decide_kernel<<<1, 32, 0, S>>>(h, partial, blocks, thr, max_sweeps, state);
+        P.enqueue_sweep();
+        jacobi_sumsq_kernel<<<blocks, 256, 0, S>>>(A, n, 1, pl);
+        jacobi_decide_kernel<<<1, 32, 0, S>>>(h, pl, blocks, scal, 1);
     } catch (...) {  // leave the stream out of capture mode
         cudaStreamEndCapture(S, &captured);
         cudaGetLastError();
@@ -1249,27 +1341,51 @@ bool sweep_loop_graph(Ctx* c, Enqueue&& enqueue_sweep, const double* A, int64_t 
         throw;
     }
     SVDK_CUDA(cudaStreamEndCapture(S, &captured));
-    const cudaError_t ie = cudaGraphInstantiate(&exec, outer, 0);
+    const cudaError_t ie = cudaGraphInstantiate(&P.exec, outer, 0);
     cudaGraphDestroy(outer);
     if (ie != cudaSuccess) {
         cudaGetLastError();
-        return false;
+        P.exec = nullptr;
     }
-    SVDK_CUDA(cudaMemsetAsync(state, 0, 2 * sizeof(double), S));
-    SVDK_CUDA(cudaGraphLaunch(exec, S));
-    double hs[2] = {0.0, 0.0};
-    d2h(c, hs, state, 2);
-    cudaGraphExecDestroy(exec);
-    off = hs[0];
-    sweeps = static_cast<int>(hs[1]);
-    c->launches += static_cast<int64_t>(sweeps) * (launches_per_sweep + 2);
-    return true;
+}
+
+// Run the plan's sweeps on the work matrices (already initialised): the
+// graph when there is one, else the same kernels driven from the host.
+// Returns the sweep count; scal holds off / thr.
+int run_plan(Ctx* c, JacobiPlan& P) {
+    cudaStream_t S = c->stream;
+    if (P.exec) {
+        SVDK_CUDA(cudaGraphLaunch(P.exec, S));
+        return -1;  // read from scal by the caller
+    }
+    double* scal = P.scal.p();
+    cudaGraphConditionalHandle none{};
+    jacobi_sumsq_kernel<<<P.blocks, 256, 0, S>>>(P.A.p(), P.n_pad, 0, P.part_all.p());
+    jacobi_sumsq_kernel<<<P.blocks, 256, 0, S>>>(P.A.p(), P.n_pad, 1, P.part_low.p());
+    jacobi_start_kernel<<<1, 32, 0, S>>>(none, P.part_all.p(), P.part_low.p(), P.blocks,
+                                         static_cast<double>(P.n_pad), scal, 0);
+    SVDK_CHECK_LAUNCH();
+    c->launches += 3;
+    double h[JS_COUNT];
+    d2h(c, h, scal, JS_COUNT);
+    int sweeps = 0;
+    while (h[JS_OFF] > h[JS_THR] && sweeps < static_cast<int>(h[JS_MAXSW])) {
+        P.enqueue_sweep();
+        SVDK_CHECK_LAUNCH();
+        jacobi_sumsq_kernel<<<P.blocks, 256, 0, S>>>(P.A.p(), P.n_pad, 1, P.part_low.p());
+        jacobi_decide_kernel<<<1, 32, 0, S>>>(none, P.part_low.p(), P.blocks, scal, 0);
+        SVDK_CHECK_LAUNCH();
+        c->launches += P.launches_per_sweep + 2;
+        ++sweeps;
+        d2h(c, h, scal, JS_COUNT);
+    }
+    return sweeps;
 }
 
 template <int TB>
-void run_sweeps(Ctx* c, double* A, double* V, int64_t n_pad, int max_sweeps, double thr, double fro,
-                DBuf& scratch, int& sweeps, double& off) {
+void build_pair_plan(Ctx* c, JacobiPlan& P) {
     constexpr int B = TB / 2;
+    const int64_t n_pad = P.n_pad;
     const int nb = static_cast<int>(n_pad / B);
     const int k = nb / 2;
     const size_t smem_solve = 4 * TB * (TB + 4) * sizeof(double);
@@ -1279,9 +1395,8 @@ void run_sweeps(Ctx* c, double* A, double* V, int64_t n_pad, int max_sweeps, dou
     ensure_smem_attr(reinterpret_cast<const void*>(jacobi_pair_solve<TB>), smem_solve);
     ensure_smem_attr(reinterpret_cast<const void*>(jacobi_update_a<TB>), smem_a);
     ensure_smem_attr(reinterpret_cast<const void*>(jacobi_update_v<TB>), smem_v);
-    // Inner skip threshold: if every off-diagonal entry were this small the
-    // outer test off <= 1e-12 ||A||_F would hold with a 10x margin.
-    const double skip_tau = 1e-13 * fro / static_cast<double>(n_pad);
+    // Inner skip threshold (JS_SKIP): if every off-diagonal entry were this
+    // small the outer test off <= 1e-12 ||A||_F would hold with a 10x margin.
     const char* inner_env = std::getenv("SVDK_JACOBI_INNER");
     const int max_inner = inner_env ? std::max(1, std::atoi(inner_env)) : 1;
     const int rounds = nb - 1;
@@ -1296,16 +1411,16 @@ void run_sweeps(Ctx* c, double* A, double* V, int64_t n_pad, int max_sweeps, dou
     const int slots = rounds + (split ? 1 : 0);
     // Every round of a sweep keeps its own Q_p set, so the V chain on the side
     // stream can lag behind the A chain by any number of rounds.
-    DBuf qbuf(c, static_cast<size_t>(slots) * k * TB * TB);
-    DBuf act(c, static_cast<size_t>(slots) * k);
-    int* active = reinterpret_cast<int*>(act.p());
+    P.qbuf = DBuf(c, static_cast<size_t>(slots) * k * TB * TB);
+    P.act = DBuf(c, static_cast<size_t>(slots) * k);
+    int* active = reinterpret_cast<int*>(P.act.p());
     const int a_ctas = k * (k + 1) / 2, v_ctas = static_cast<int>(n_pad / TB) * k;
     if (!c->aux_stream) {
         SVDK_CUDA(cudaStreamCreateWithFlags(&c->aux_stream, cudaStreamNonBlocking));
         SVDK_CUDA(cudaEventCreateWithFlags(&c->aux_ev[0], cudaEventDisableTiming));
         SVDK_CUDA(cudaEventCreateWithFlags(&c->aux_ev[1], cudaEventDisableTiming));
     }
-    cudaStream_t S = c->stream, S2 = c->aux_stream;
+    cudaStream_t S = c->stream;
     // register-resident updates for 2b = 32 (SVDK_JACOBI_UPD=smem: the
     // shared-memory kernels, kept for TB = 16 and for comparison)
     const char* upd_env = std::getenv("SVDK_JACOBI_UPD");
@@ -1330,111 +1445,84 @@ void run_sweeps(Ctx* c, double* A, double* V, int64_t n_pad, int max_sweeps, dou
         static_cast<int>(ceil_div(ceil_div(n_pad, static_cast<int64_t>(VT_ROWS)) * k, UPD_WARPS));
     // Programmatic dependent launches on the solve -> A update -> solve chain
     // (SVDK_JACOBI_PDL=0: plain launches; see pdl_wait for the measurements).
+    // Every kernel waits (griddepcontrol.wait) before reading its
+    // predecessor's output; the solve's schedule tables come from the plan's
+    // tables kernel, which completed before any sweep was enqueued.
     const char* pdl_env = std::getenv("SVDK_JACOBI_PDL");
     const bool pdl = !(pdl_env && std::atoi(pdl_env) == 0);
-    auto launch = [&](auto kern, int grid, int block, size_t smem, bool prog, auto... args) {
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(static_cast<unsigned>(grid));
-        cfg.blockDim = dim3(static_cast<unsigned>(block));
-        cfg.dynamicSmemBytes = smem;
-        cfg.stream = S;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        at[0].val.programmaticStreamSerializationAllowed = 1;
-        cfg.attrs = at;
-        cfg.numAttrs = (prog && pdl) ? 1 : 0;
-        SVDK_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
-    };
-    auto launch_updates = [&](const double* qr, const int* ar, int r) {
-        if (reg_upd) {
-            jacobi_update_v_reg<<<v_warp_ctas, UPD_WARPS * 32, 0, S2>>>(V, n_pad, n_pad, qr, ar, nb, r);
-            int64_t ld = n_pad;
-            if (a_q4)
-                launch(jacobi_update_a_q4, a_ctas, 128, 0, true, A, ld, qr, ar, nb, r);
-            else if (a_vec == 1)
-                launch(jacobi_update_a_vec<1>, a_warp_ctas, UPD_WARPS * 32, 0, true, A, ld, qr, ar, nb, r);
-            else if (a_vec == 2)
-                launch(jacobi_update_a_vec<2>, a_ctas2, UPD_WARPS * 32, 0, true, A, ld, qr, ar, nb, r);
-            else if (a_vec == 4)
-                launch(jacobi_update_a_vec<4>, a_ctas, UPD_WARPS * 32, 0, true, A, ld, qr, ar, nb, r);
-            else
-                launch(jacobi_update_a_reg, a_warp_ctas, UPD_WARPS * 32, 0, true, A, ld, qr, ar, nb, r);
-        } else {
-            jacobi_update_v<TB><<<v_ctas, 256, smem_v, S2>>>(V, n_pad, qr, ar, nb, r);
-            jacobi_update_a<TB><<<a_ctas, 256, smem_a, S>>>(A, n_pad, qr, ar, nb, r);
-        }
-    };
-    DBuf tab_buf(c, 3 * sizeof(SolveTables<TB>) / sizeof(double));
-    const auto* tabs = reinterpret_cast<const SolveTables<TB>*>(tab_buf.p());
-    jacobi_tables_kernel<TB><<<3, 256, 0, S>>>(reinterpret_cast<SolveTables<TB>*>(tab_buf.p()));
+    P.tabs = DBuf(c, 3 * sizeof(SolveTables<TB>) / sizeof(double));
+    jacobi_tables_kernel<TB><<<3, 256, 0, S>>>(reinterpret_cast<SolveTables<TB>*>(P.tabs.p()));
     SVDK_CHECK_LAUNCH();
     c->launches++;
-    // The first solve after jacobi_tables_kernel is a plain launch: the solve
-    // copies its schedule tables BEFORE griddepcontrol.wait, which is only
-    // legal when the tables' producer has completed (every later solve follows
-    // kernels that themselves waited on a grid launched after the tables).
-    bool after_tables = true;
-    auto launch_solve = [&](double* qr, int* ar, int r, int mode) {
-        const double* a = A;
-        int64_t ld = n_pad;
-        launch(jacobi_pair_solve<TB>, k, nthreads_solve, smem_solve, !after_tables, a, ld, tabs, qr, ar, nb, r,
-               skip_tau, max_inner, mode);
-        after_tables = false;
-    };
-    auto enqueue_sweep = [&] {
+    const auto* tabs = reinterpret_cast<const SolveTables<TB>*>(P.tabs.p());
+    double* A = P.A.p();
+    double* V = P.V.p();
+    const double* skip_p = P.scal.p() + JS_SKIP;
+    double* qbase = P.qbuf.p();
+    P.launches_per_sweep = 3 * slots;
+    P.enqueue_sweep = [=]() {
+        // the context's streams at enqueue time (svdk_ctx_set_stream may have moved them)
+        const cudaStream_t S = c->stream, S2 = c->aux_stream;
+        const cudaEvent_t ev0 = c->aux_ev[0], ev1 = c->aux_ev[1];
+        auto launch = [&](auto kern, int grid, int block, size_t smem, bool prog, auto... args) {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(static_cast<unsigned>(grid));
+            cfg.blockDim = dim3(static_cast<unsigned>(block));
+            cfg.dynamicSmemBytes = smem;
+            cfg.stream = S;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = (prog && pdl) ? 1 : 0;
+            SVDK_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
+        };
+        auto launch_updates = [&](const double* qr, const int* ar, int r) {
+            if (reg_upd) {
+                jacobi_update_v_reg<<<v_warp_ctas, UPD_WARPS * 32, 0, S2>>>(V, n_pad, n_pad, qr, ar, nb, r);
+                int64_t ld = n_pad;
+                if (a_q4)
+                    launch(jacobi_update_a_q4, a_ctas, 128, 0, true, A, ld, qr, ar, nb, r);
+                else if (a_vec == 1)
+                    launch(jacobi_update_a_vec<1>, a_warp_ctas, UPD_WARPS * 32, 0, true, A, ld, qr, ar, nb, r);
+                else if (a_vec == 2)
+                    launch(jacobi_update_a_vec<2>, a_ctas2, UPD_WARPS * 32, 0, true, A, ld, qr, ar, nb, r);
+                else if (a_vec == 4)
+                    launch(jacobi_update_a_vec<4>, a_ctas, UPD_WARPS * 32, 0, true, A, ld, qr, ar, nb, r);
+                else
+                    launch(jacobi_update_a_reg, a_warp_ctas, UPD_WARPS * 32, 0, true, A, ld, qr, ar, nb, r);
+            } else {
+                jacobi_update_v<TB><<<v_ctas, 256, smem_v, S2>>>(V, n_pad, qr, ar, nb, r);
+                jacobi_update_a<TB><<<a_ctas, 256, smem_a, S>>>(A, n_pad, qr, ar, nb, r);
+            }
+        };
+        auto launch_solve = [&](double* qr, int* ar, int r, int mode) {
+            const double* a = A;
+            int64_t ld = n_pad;
+            launch(jacobi_pair_solve<TB>, k, nthreads_solve, smem_solve, true, a, ld, tabs, qr, ar, nb, r, skip_p,
+                   max_inner, mode);
+        };
         if (split) {  // in-block stage on the round-0 block pairing
-            double* qr = qbuf.p() + static_cast<size_t>(rounds) * k * TB * TB;
+            double* qr = qbase + static_cast<size_t>(rounds) * k * TB * TB;
             int* ar = active + static_cast<size_t>(rounds) * k;
             launch_solve(qr, ar, 0, 1);
-            SVDK_CUDA(cudaEventRecord(c->aux_ev[0], S));
-            SVDK_CUDA(cudaStreamWaitEvent(S2, c->aux_ev[0], 0));
+            SVDK_CUDA(cudaEventRecord(ev0, S));
+            SVDK_CUDA(cudaStreamWaitEvent(S2, ev0, 0));
             launch_updates(qr, ar, 0);
         }
         for (int r = 0; r < rounds; ++r) {
-            double* qr = qbuf.p() + static_cast<size_t>(r) * k * TB * TB;
+            double* qr = qbase + static_cast<size_t>(r) * k * TB * TB;
             int* ar = active + static_cast<size_t>(r) * k;
             launch_solve(qr, ar, r, split ? 2 : 0);
-            SVDK_CUDA(cudaEventRecord(c->aux_ev[0], S));
-            SVDK_CUDA(cudaStreamWaitEvent(S2, c->aux_ev[0], 0));
+            SVDK_CUDA(cudaEventRecord(ev0, S));
+            SVDK_CUDA(cudaStreamWaitEvent(S2, ev0, 0));
             launch_updates(qr, ar, r);
         }
         // join: the sweep ends when the V chain has caught up
-        SVDK_CUDA(cudaEventRecord(c->aux_ev[1], S2));
-        SVDK_CUDA(cudaStreamWaitEvent(S, c->aux_ev[1], 0));
+        SVDK_CUDA(cudaEventRecord(ev1, S2));
+        SVDK_CUDA(cudaStreamWaitEvent(S, ev1, 0));
     };
-    // One sweep = 3 (nb - 1) launches on two streams: capture them once as a
-    // CUDA graph (a DAG with the V chain beside the A chain) and replay it.
-    if (off > thr && max_sweeps > 0 && nb > 2 &&
-        sweep_loop_graph(c, enqueue_sweep, A, n_pad, thr, max_sweeps, scratch, 3 * slots, sweeps, off))
-        return;
-    cudaGraphExec_t exec = nullptr;
-    const bool use_graph = nb > 2 && S != nullptr;
-    if (use_graph) {
-        cudaGraph_t graph;
-        SVDK_CUDA(cudaStreamBeginCapture(S, cudaStreamCaptureModeThreadLocal));
-        enqueue_sweep();
-        SVDK_CUDA(cudaStreamEndCapture(S, &graph));
-        SVDK_CUDA(cudaGraphInstantiate(&exec, graph, 0));
-        cudaGraphDestroy(graph);
-    }
-    sweeps = 0;
-    try {
-        while (off > thr && sweeps < max_sweeps) {
-            if (use_graph) {
-                SVDK_CUDA(cudaGraphLaunch(exec, S));
-            } else {
-                enqueue_sweep();
-                SVDK_CHECK_LAUNCH();
-            }
-            c->launches += 3 * slots;
-            ++sweeps;
-            off = std::sqrt(2.0 * device_sumsq(c, A, n_pad, 1, scratch));
-        }
-    } catch (...) {
-        if (exec) cudaGraphExecDestroy(exec);
-        throw;
-    }
-    if (exec) cudaGraphExecDestroy(exec);
+    if (nb > 2) build_loop_graph(c, P);
 }
 
 // ---------------------------------------------------------------------------
@@ -1601,7 +1689,7 @@ __device__ __forceinline__ void warp_tile_16x32(FA a_at, FB b_at, FC store) {
 // no sub-stage found an entry above skip_tau (Q = I, updates skipped).
 __global__ void __launch_bounds__(Q_THREADS, 1)
     jacobi_quad_solve(const double* A, int64_t lda, const SolveTables<32>* tabs, double* Qbuf,
-                      int* active, int ns, int round, double skip_tau, int stage0) {
+                      int* active, int ns, int round, const double* skip_tau_p, int stage0) {
     extern __shared__ double sm[];
     double* M64 = sm;             // the subproblem, transformed by each sub-stage
     double* Qa = M64 + 64 * L64;  // accumulated 64 x 64 rotation
@@ -1623,6 +1711,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1)
     const bool probe = blockIdx.x == 0 && tid == 0 && round == 5;
     if (probe) SVDK_PROBE_STORE(g_jprobe, 0, SVDK_CLOCK());
     pdl_wait();  // A of the previous round's a64 update (see pdl_trigger)
+    const double skip_tau = *skip_tau_p;  // written before the sweep (jacobi_start_kernel)
     for (int e = tid; e < 64 * 64; e += Q_THREADS) {
         const int i = e & 63, j = e >> 6;
         M64[i + j * L64] = __ldcg(&A[g(i) + g(j) * lda]);
@@ -1897,97 +1986,69 @@ __global__ void __launch_bounds__(128, 4)
     }
 }
 
-void run_sweeps_quad(Ctx* c, double* A, double* V, int64_t n_pad, int max_sweeps, double thr, double fro,
-                     DBuf& scratch, int& sweeps, double& off) {
+void build_quad_plan(Ctx* c, JacobiPlan& P) {
+    const int64_t n_pad = P.n_pad;
     const int ns = static_cast<int>(n_pad / 32), ks = ns / 2, rounds = ns - 1;
     ensure_smem_attr(reinterpret_cast<const void*>(jacobi_quad_solve), QUAD_SMEM);
     ensure_smem_attr(reinterpret_cast<const void*>(jacobi_update_a64), A64_SMEM);
-    const double skip_tau = 1e-13 * fro / static_cast<double>(n_pad);  // as run_sweeps
-    DBuf qbuf(c, static_cast<size_t>(rounds) * ks * 4096);
-    DBuf act(c, static_cast<size_t>(rounds) * ks);
-    int* active = reinterpret_cast<int*>(act.p());
+    P.qbuf = DBuf(c, static_cast<size_t>(rounds) * ks * 4096);
+    P.act = DBuf(c, static_cast<size_t>(rounds) * ks);
+    int* active = reinterpret_cast<int*>(P.act.p());
     if (!c->aux_stream) {
         SVDK_CUDA(cudaStreamCreateWithFlags(&c->aux_stream, cudaStreamNonBlocking));
         SVDK_CUDA(cudaEventCreateWithFlags(&c->aux_ev[0], cudaEventDisableTiming));
         SVDK_CUDA(cudaEventCreateWithFlags(&c->aux_ev[1], cudaEventDisableTiming));
     }
-    cudaStream_t S = c->stream, S2 = c->aux_stream;
-    DBuf tab_buf(c, 3 * sizeof(SolveTables<32>) / sizeof(double));
-    const auto* tabs = reinterpret_cast<const SolveTables<32>*>(tab_buf.p());
-    jacobi_tables_kernel<32><<<3, 256, 0, S>>>(reinterpret_cast<SolveTables<32>*>(tab_buf.p()));
+    cudaStream_t S = c->stream;
+    P.tabs = DBuf(c, 3 * sizeof(SolveTables<32>) / sizeof(double));
+    jacobi_tables_kernel<32><<<3, 256, 0, S>>>(reinterpret_cast<SolveTables<32>*>(P.tabs.p()));
     SVDK_CHECK_LAUNCH();
     c->launches++;
+    const auto* tabs = reinterpret_cast<const SolveTables<32>*>(P.tabs.p());
     const int a_ctas = ks * (ks + 1) / 2;
     const int v_ctas = static_cast<int>(ceil_div(n_pad, static_cast<int64_t>(V64_ROWS))) * ks;
     // solve -> a64 -> solve as programmatic dependent launches (see pdl_trigger)
     const char* pdl_env = std::getenv("SVDK_JACOBI_PDL");
     const bool pdl = !(pdl_env && std::atoi(pdl_env) == 0);
-    const double* a_in = A;
-    int64_t ld = n_pad;
-    // the first launch after jacobi_tables_kernel is plain (the quad solve
-    // copies its tables before griddepcontrol.wait; see run_sweeps)
-    bool after_tables = true;
-    auto launch = [&](auto kern, int grid, int block, size_t smem, auto... args) {
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(static_cast<unsigned>(grid));
-        cfg.blockDim = dim3(static_cast<unsigned>(block));
-        cfg.dynamicSmemBytes = smem;
-        cfg.stream = S;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        at[0].val.programmaticStreamSerializationAllowed = 1;
-        cfg.attrs = at;
-        cfg.numAttrs = (pdl && !after_tables) ? 1 : 0;
-        after_tables = false;
-        SVDK_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
-    };
-    auto enqueue_sweep = [&] {
+    double* A = P.A.p();
+    double* V = P.V.p();
+    const double* skip_p = P.scal.p() + JS_SKIP;
+    double* qbase = P.qbuf.p();
+    P.launches_per_sweep = 3 * rounds;
+    P.enqueue_sweep = [=]() {
+        const cudaStream_t S = c->stream, S2 = c->aux_stream;
+        const cudaEvent_t ev0 = c->aux_ev[0], ev1 = c->aux_ev[1];
+        const double* a_in = A;
+        int64_t ld = n_pad;
+        auto launch = [&](auto kern, int grid, int block, size_t smem, auto... args) {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(static_cast<unsigned>(grid));
+            cfg.blockDim = dim3(static_cast<unsigned>(block));
+            cfg.dynamicSmemBytes = smem;
+            cfg.stream = S;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = pdl ? 1 : 0;
+            SVDK_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
+        };
         for (int r = 0; r < rounds; ++r) {
-            double* qr = qbuf.p() + static_cast<size_t>(r) * ks * 4096;
+            double* qr = qbase + static_cast<size_t>(r) * ks * 4096;
             int* ar = active + static_cast<size_t>(r) * ks;
-            launch(jacobi_quad_solve, ks, Q_THREADS, QUAD_SMEM, a_in, ld, tabs, qr, ar, ns, r, skip_tau,
+            launch(jacobi_quad_solve, ks, Q_THREADS, QUAD_SMEM, a_in, ld, tabs, qr, ar, ns, r, skip_p,
                    r == 0 ? 1 : 0);
-            SVDK_CUDA(cudaEventRecord(c->aux_ev[0], S));
-            SVDK_CUDA(cudaStreamWaitEvent(S2, c->aux_ev[0], 0));
+            SVDK_CUDA(cudaEventRecord(ev0, S));
+            SVDK_CUDA(cudaStreamWaitEvent(S2, ev0, 0));
             jacobi_update_v64<<<v_ctas, 128, 0, S2>>>(V, n_pad, n_pad, qr, ar, ns, r);
             const double* qc = qr;
             const int* ac = ar;
             launch(jacobi_update_a64, a_ctas, A64_THREADS, A64_SMEM, A, ld, qc, ac, ns, r);
         }
-        SVDK_CUDA(cudaEventRecord(c->aux_ev[1], S2));
-        SVDK_CUDA(cudaStreamWaitEvent(S, c->aux_ev[1], 0));
+        SVDK_CUDA(cudaEventRecord(ev1, S2));
+        SVDK_CUDA(cudaStreamWaitEvent(S, ev1, 0));
     };
-    if (off > thr && max_sweeps > 0 &&
-        sweep_loop_graph(c, enqueue_sweep, A, n_pad, thr, max_sweeps, scratch, 3 * rounds, sweeps, off))
-        return;
-    cudaGraphExec_t exec = nullptr;
-    const bool use_graph = S != nullptr;
-    if (use_graph) {
-        cudaGraph_t graph;
-        SVDK_CUDA(cudaStreamBeginCapture(S, cudaStreamCaptureModeThreadLocal));
-        enqueue_sweep();
-        SVDK_CUDA(cudaStreamEndCapture(S, &graph));
-        SVDK_CUDA(cudaGraphInstantiate(&exec, graph, 0));
-        cudaGraphDestroy(graph);
-    }
-    sweeps = 0;
-    try {
-        while (off > thr && sweeps < max_sweeps) {
-            if (use_graph) {
-                SVDK_CUDA(cudaGraphLaunch(exec, S));
-            } else {
-                enqueue_sweep();
-                SVDK_CHECK_LAUNCH();
-            }
-            c->launches += 3 * rounds;
-            ++sweeps;
-            off = std::sqrt(2.0 * device_sumsq(c, A, n_pad, 1, scratch));
-        }
-    } catch (...) {
-        if (exec) cudaGraphExecDestroy(exec);
-        throw;
-    }
-    if (exec) cudaGraphExecDestroy(exec);
+    build_loop_graph(c, P);
 }
 
 }  // namespace
@@ -1998,37 +2059,50 @@ void run_sweeps_quad(Ctx* c, double* A, double* V, int64_t n_pad, int max_sweeps
 // n ~ 3000 the solve chain (not the update traffic) bounds a sweep.
 constexpr int64_t kQuadMinN = 3072;
 
+// The context's sweep plan for (n_pad, TB), built on first use and kept
+// (most recently used last, at most kMaxPlans per context).
+JacobiPlan& jacobi_plan(Ctx* c, int64_t n_pad, int TB) {
+    if (!c->jacobi_cache) c->jacobi_cache = new JacobiCache;
+    auto& plans = c->jacobi_cache->plans;
+    for (size_t i = 0; i < plans.size(); ++i)
+        if (plans[i]->n_pad == n_pad && plans[i]->tb == TB && plans[i]->A.count()) {
+            std::unique_ptr<JacobiPlan> p = std::move(plans[i]);
+            plans.erase(plans.begin() + static_cast<long>(i));
+            plans.push_back(std::move(p));
+            return *plans.back();
+        }
+    if (plans.size() >= kMaxPlans) plans.erase(plans.begin());
+    auto p = std::make_unique<JacobiPlan>();
+    p->n_pad = n_pad;
+    p->tb = TB;
+    p->A = DBuf(c, static_cast<size_t>(n_pad) * n_pad);
+    p->V = DBuf(c, static_cast<size_t>(n_pad) * n_pad);
+    p->blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_pad * n_pad, 256), 2 * c->num_sms)));
+    p->part_all = DBuf(c, 2 * static_cast<size_t>(std::max<int64_t>(p->blocks, 2 * c->num_sms)));
+    p->part_low = DBuf(c, static_cast<size_t>(p->blocks));
+    p->scal = DBuf(c, JS_COUNT);
+    fill(c, p->scal.p(), JS_COUNT, 0.0);
+    JacobiPlan& P = *p;
+    plans.push_back(std::move(p));
+    try {
+        if (TB == 16)
+            build_pair_plan<16>(c, P);
+        else if (TB == 64)
+            build_quad_plan(c, P);
+        else
+            build_pair_plan<32>(c, P);
+    } catch (...) {
+        plans.pop_back();
+        throw;
+    }
+    return P;
+}
+
 void eig_sym(Ctx* c, const double* S, int64_t lds, int64_t n, int max_sweeps, double* w,
              double* Vout, int64_t ldv) {
     if (max_sweeps <= 0) max_sweeps = 30;
     if (n == 0) return;
     PhaseTimer timer(c, "eig_sym");
-    // symmetry check (kernels.cpp:251-262)
-    int pow2 = 0;
-    {
-        const int blocks = static_cast<int>(
-            std::max<int64_t>(1, std::min<int64_t>(ceil_div(n * n, 256), 2 * c->num_sms)));
-        DBuf part(c, 2 * blocks);
-        symcheck_kernel<<<blocks, 256, 0, c->stream>>>(S, lds, n, part.p());
-        SVDK_CHECK_LAUNCH();
-        c->launches++;
-        std::vector<double> h(2 * blocks);
-        d2h(c, h.data(), part.p(), 2 * blocks);
-        double mabs = 0.0, masym = 0.0;
-        for (int b = 0; b < blocks; ++b) {
-            mabs = std::max(mabs, h[2 * b]);
-            masym = std::max(masym, h[2 * b + 1]);
-        }
-        // prescale by a power of two (exact) so the rotation kernels never see
-        // entries whose squares over- or underflow
-        if (mabs > 0.0 && (mabs > 1e100 || mabs < 1e-100)) pow2 = std::ilogb(mabs);
-        if (masym > 1e-8 * mabs) {
-            char buf[96];
-            std::snprintf(buf, sizeof buf, "%f", masym);
-            fail(SVDK_E_PARAM,
-                 std::string("eig_sym: input asymmetric beyond tolerance, max|s-s^T| = ") + buf);
-        }
-    }
     // Block size: measured on B200 (tools/eig_sweep.sh): 2b = 32 with ONE
     // inner sweep per round is fastest for n in [256, 2048]; the outer sweep
     // count (9-12) does not depend on how far each subproblem is pushed.
@@ -2040,47 +2114,57 @@ void eig_sym(Ctx* c, const double* S, int64_t lds, int64_t n, int max_sweeps, do
         if (t == 16 || t == 32 || t == 64) TB = t;
     }
     const int64_t n_pad = round_up(n, TB);
-    DBuf A(c, static_cast<size_t>(n_pad) * n_pad), V(c, static_cast<size_t>(n_pad) * n_pad);
-
-    DBuf scratch(c, 4 * c->num_sms + 8);
+    JacobiPlan& P = jacobi_plan(c, n_pad, TB);
+    double* scal = P.scal.p();
+    // symmetry check + prescale on the device (kernels.cpp:251-269); the
+    // ParamError is raised after the single read-back at the end
     {
         const int blocks = static_cast<int>(
+            std::max<int64_t>(1, std::min<int64_t>(ceil_div(n * n, 256), 2 * c->num_sms)));
+        symcheck_kernel<<<blocks, 256, 0, c->stream>>>(S, lds, n, P.part_all.p());
+        eig_prep_kernel<<<1, 32, 0, c->stream>>>(P.part_all.p(), blocks, max_sweeps, scal);
+        const int iblocks = static_cast<int>(
             std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_pad * n_pad, 256), 4 * c->num_sms)));
-        jacobi_init_kernel<<<blocks, 256, 0, c->stream>>>(S, lds, n, A.p(), V.p(), n_pad,
-                                                          std::ldexp(1.0, -pow2));
+        jacobi_init_kernel<<<iblocks, 256, 0, c->stream>>>(S, lds, n, P.A.p(), P.V.p(), n_pad, scal + JS_SCALE);
         SVDK_CHECK_LAUNCH();
-        c->launches++;
+        c->launches += 3;
     }
-    const double fro = std::sqrt(device_sumsq(c, A.p(), n_pad, 0, scratch));
-    const double thr = 1e-12 * fro;  // kernels.cpp:271
-    double off = std::sqrt(2.0 * device_sumsq(c, A.p(), n_pad, 1, scratch));
-    int sweeps = 0;
-    if (n == 1) off = 0.0;
-    if (TB == 16)
-        run_sweeps<16>(c, A.p(), V.p(), n_pad, max_sweeps, thr, fro, scratch, sweeps, off);
-    else if (TB == 64)
-        run_sweeps_quad(c, A.p(), V.p(), n_pad, max_sweeps, thr, fro, scratch, sweeps, off);
-    else
-        run_sweeps<32>(c, A.p(), V.p(), n_pad, max_sweeps, thr, fro, scratch, sweeps, off);
+    int sweeps = run_plan(c, P);
+    DBuf dest(c, n);  // int storage inside a double buffer
+    eig_sort_kernel<<<static_cast<unsigned>(ceil_div(n, 128)), 128, 0, c->stream>>>(
+        P.A.p(), n_pad, n, scal + JS_UNSCALE, w, reinterpret_cast<int*>(dest.p()));
+    SVDK_CHECK_LAUNCH();
+    dim3 g(static_cast<unsigned>(std::min<int64_t>(ceil_div(n, 128), 64)),
+           static_cast<unsigned>(std::min<int64_t>(n, 65535)));
+    eig_gather_kernel<<<g, 128, 0, c->stream>>>(P.V.p(), n_pad, n,
+                                                reinterpret_cast<const int*>(dest.p()), Vout, ldv);
+    SVDK_CHECK_LAUNCH();
+    c->launches += 2;
+    double h[JS_COUNT];
+    d2h(c, h, scal, JS_COUNT);
+    if (sweeps < 0) {
+        sweeps = static_cast<int>(h[JS_SWEEPS]);
+        c->launches += static_cast<int64_t>(sweeps) * (P.launches_per_sweep + 2) + 3;
+    }
+    if (h[JS_MASYM] > 1e-8 * h[JS_MABS]) {
+        char buf[96];
+        std::snprintf(buf, sizeof buf, "%f", h[JS_MASYM]);
+        fail(SVDK_E_PARAM, std::string("eig_sym: input asymmetric beyond tolerance, max|s-s^T| = ") + buf);
+    }
     c->jacobi_sweeps = sweeps;
-    off = std::ldexp(off, pow2);  // back to the caller's units
+    const double off = h[JS_OFF] * h[JS_UNSCALE];  // back to the caller's units
     c->last_off_norm = off;
-    if (off > std::ldexp(thr, pow2)) {
+    if (off > h[JS_THR] * h[JS_UNSCALE]) {
         char buf[160];
         std::snprintf(buf, sizeof buf, "eig_sym: no convergence in %d sweeps, off-diagonal norm %f",
                       max_sweeps, off);
         fail(SVDK_E_NUMERICAL, buf, off);
     }
-    DBuf dest(c, n);  // int storage inside a double buffer
-    eig_sort_kernel<<<static_cast<unsigned>(ceil_div(n, 128)), 128, 0, c->stream>>>(
-        A.p(), n_pad, n, std::ldexp(1.0, pow2), w, reinterpret_cast<int*>(dest.p()));
-    SVDK_CHECK_LAUNCH();
-    dim3 g(static_cast<unsigned>(std::min<int64_t>(ceil_div(n, 128), 64)),
-           static_cast<unsigned>(std::min<int64_t>(n, 65535)));
-    eig_gather_kernel<<<g, 128, 0, c->stream>>>(V.p(), n_pad, n,
-                                                reinterpret_cast<const int*>(dest.p()), Vout, ldv);
-    SVDK_CHECK_LAUNCH();
-    c->launches += 2;
+}
+
+void jacobi_cache_free(Ctx* c) {
+    delete c->jacobi_cache;
+    c->jacobi_cache = nullptr;
 }
 
 }  // namespace svdk

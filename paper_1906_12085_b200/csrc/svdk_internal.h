@@ -75,7 +75,8 @@ private:
 };
 
 struct Ctx;
-struct HostGroup;  // in-process collective group (comm.cu)
+struct HostGroup;    // in-process collective group (comm.cu)
+struct JacobiCache;  // instantiated eig_sym sweep plans (jacobi.cu)
 
 // RAII device buffer of doubles from the context pool.
 class DBuf {
@@ -144,6 +145,7 @@ struct Ctx {
     size_t events_used = 0;
     // counters for bench/introspection
     int64_t launches = 0;
+    JacobiCache* jacobi_cache = nullptr;
     int jacobi_sweeps = 0;
     double last_off_norm = 0.0;
 };
@@ -231,6 +233,8 @@ void center_cols_are_examples(Ctx* c, const double* A, int64_t lda, int64_t m, i
 // kernels.cpp:241-346 (symmetry check, threshold, sweep cap, stable sort).
 void eig_sym(Ctx* c, const double* S, int64_t lds, int64_t n, int max_sweeps, double* w,
              double* V, int64_t ldv);
+// release the cached sweep plans (before the context's pool is trimmed)
+void jacobi_cache_free(Ctx* c);
 
 // Host <-> device
 void h2d(Ctx* c, double* dst, const double* src, int64_t count);

@@ -9,8 +9,8 @@
 //                 MRRR's dlar1v): T - lambda I = L D L^T (top-down) and
 //                 U P U^T (bottom-up), twist index r = argmin |gamma_r|,
 //                 x_r = 1 and the two one-sided recurrences;
-//   orthonormality one engine CholeskyQR2 of the k x k eigenvector matrix
-//                 (DMMA; R ~ I), which also certifies the basis.
+//   orthonormality S^T S = I to 1e-6 certifies the basis, one Newton-Schulz
+//                 polar step S (3I - S^T S)/2 (two DMMA products) polishes it.
 // Tight clusters (relative gap < 1e-10) and a failed certification return
 // false: the caller then solves T densely with the Jacobi eigensolver. The
 // Lanczos T of BASELINE's configs has relative gaps >= ~1e-7.
@@ -19,9 +19,6 @@
 #include "svdk_methods.h"
 
 namespace svdk {
-int64_t qr_thin(Ctx* c, const double* H, int64_t ldh, int64_t m, int64_t p, double* Q, int64_t ldq,
-                double* R, const RowComm* comm, double* Rinv_last);
-
 namespace {
 
 constexpr int TB_THREADS = 256;   // setup kernel
@@ -172,15 +169,17 @@ __global__ void __launch_bounds__(VEC_THREADS)
     for (int i = 0; i < n; ++i) X[i * ld + t] *= inv;
 }
 
-// flag |= 2 when the CholeskyQR factor of the eigenvector matrix is not ~I
-// (the twisted-factorisation vectors were not numerically orthogonal)
-__global__ void tri_certify_kernel(const double* R, int n, int* flag) {
+// B = (3 I - G) / 2 for one Newton-Schulz polar step S <- S B (G = S^T S);
+// flag |= 2 when G is not I to 1e-6 (the twisted-factorisation vectors were
+// not numerically orthogonal: unresolved cluster).
+__global__ void tri_ns_kernel(const double* G, int n, double* Bm, int* flag) {
     const int64_t nn = static_cast<int64_t>(n) * n;
     for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < nn;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int64_t j = e / n, i = e - j * n;
-        const double v = R[e] - (i == j ? 1.0 : 0.0);
-        if (!(fabs(v) <= 1e-6)) atomicOr(flag, 2);
+        const double d = G[e] - (i == j ? 1.0 : 0.0);
+        if (!(fabs(d) <= 1e-6)) atomicOr(flag, 2);
+        Bm[e] = (i == j ? 1.0 : 0.0) - 0.5 * d;
     }
 }
 
@@ -233,17 +232,18 @@ bool tridiag_eig(Ctx* c, const double* alpha, const double* beta, int64_t k, dou
         SVDK_CHECK_LAUNCH();
         c->launches++;
         Us.reset();
-        DBuf S0(c, static_cast<size_t>(lds) * k), R(c, static_cast<size_t>(k) * k);
+        DBuf S0(c, static_cast<size_t>(lds) * k), G(c, static_cast<size_t>(k) * k), Bm(c, static_cast<size_t>(k) * k);
         transpose(c, X.p(), k, k, k, S0.p(), lds);
         X.reset();
-        // polish orthonormality (R ~ I keeps the eigenvector order and signs) and
-        // certify: R must be I to 1e-6, else the vectors were not resolved
-        const int64_t r = qr_thin(c, S0.p(), lds, k, k, S, lds, R.p(), nullptr, nullptr);
-        if (r != k) return false;
-        tri_certify_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(k * k, 256), 4096)), 256, 0,
-                             c->stream>>>(R.p(), n, fl);
+        // certify (S0^T S0 = I to 1e-6) and polish by one Newton-Schulz step
+        // S = S0 (3 I - S0^T S0) / 2: orthogonality 1e-12 -> rounding level,
+        // order and signs kept (two DMMA products instead of a CholeskyQR2)
+        syrk(c, k, k, S0.p(), lds, G.p(), k);
+        tri_ns_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(k * k, 256), 4096)), 256, 0, c->stream>>>(
+            G.p(), n, Bm.p(), fl);
         SVDK_CHECK_LAUNCH();
         c->launches++;
+        gemm(c, false, k, k, k, S0.p(), lds, Bm.p(), k, S, lds);
         SVDK_CUDA(cudaMemcpyAsync(&bad, fl, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
         SVDK_CUDA(cudaStreamSynchronize(c->stream));
         if (bad) return false;

@@ -120,6 +120,21 @@ def header(cfg, m, n, seed, mix, a_rows_src):
                 mix_sha256=sha(mix), a_rows_idx=rows, a_rows=a_rows_src(rows))
 
 
+def sweep_trajectory(ref, c, cap_max=30):
+    """off(A) after each sweep of the reference eig_sym on c's Gram (kernels.cpp:
+    321-326: the NumericalError residual with max_sweeps = cap), SURVEY 8a."""
+    from oracle.pyoracle import OracleError
+    g = ref.gram(c)
+    offs = []
+    for cap in range(1, cap_max + 1):
+        try:
+            ref.eig_sym(g, cap)
+            return np.array(offs), cap
+        except OracleError as e:
+            offs.append(e.residual)
+    return np.array(offs), -1
+
+
 def finish_lambda(w):
     """truncated_svd's sigma = sqrt(max(lambda, 0)) + rank cut; eigenvalues = sigma^2 (pca.cpp:110-113)."""
     sigma = np.sqrt(np.maximum(w, 0.0))
@@ -130,7 +145,7 @@ def finish_lambda(w):
 
 
 # --------------------------------------------------------------------------- whole-matrix reference runs
-def full(ref, name, cfg, m, seed, methods, full_v=False, force_vk=False):
+def full(ref, name, cfg, m, seed, methods, full_v=False, force_vk=False, trajectory=False):
     n = cfg.n
     t0 = time.time()
     gx = synth.host_gram_x(m, n, seed)
@@ -148,6 +163,10 @@ def full(ref, name, cfg, m, seed, methods, full_v=False, force_vk=False):
     times["total_variance_s"] = time.perf_counter() - t0
     out.update(total=total, mean=mean, oracle="svdkit_ref: center + total_variance + "
                + " / ".join(methods) + " on the whole matrix (compiled reference)")
+    if trajectory:
+        offs, conv = sweep_trajectory(ref, c)
+        out.update(ref_sweep_off=offs, ref_sweeps=conv)
+        log(name, "reference sweep trajectory", offs, "converged at", conv)
     for meth, (l, q, rs) in methods.items():
         t0 = time.perf_counter()
         if meth == "truncated":
@@ -280,7 +299,7 @@ if __name__ == "__main__":
         elif w == "c1":
             full(ref, "c1", C["c1"], C["c1"].m, synth.MATRIX_SEED,
                  {"truncated": (0, 0, 0), "randomized": (256, 2, synth.METHOD_SEED),
-                  "krylov": (128, 1, synth.METHOD_SEED)}, full_v=True)
+                  "krylov": (128, 1, synth.METHOD_SEED)}, full_v=True, trajectory=True)
         elif w == "c2mid":
             # c2's spectrum and method at a height the reference finishes in minutes
             full(ref, "c2mid", C["c2"], 20000, synth.MATRIX_SEED,

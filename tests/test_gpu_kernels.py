@@ -249,3 +249,31 @@ def test_gemv_pair_vs_numpy(form, monkeypatch):
         assert np.max(np.abs(w1 - ref) / scale) < 1e-14, (m, n)
         assert np.array_equal(w1, w2), (m, n)
     torch.cuda.set_stream(torch.cuda.default_stream())
+
+
+def test_jacobi_sweep_trajectory_c1(sk):
+    """SURVEY 8a's regression: off(A) after each sweep on the c1 Gram (the
+    NumericalError residual with max_sweeps = cap, kernels.cpp:321-326) tracks
+    the compiled reference's cyclic-by-row trajectory (tests/golden/c1.npz,
+    same Gram up to summation order): the block-parallel ordering rotates the
+    same pairs once per sweep, so it converges in the same number of sweeps
+    (+-1) and each intermediate off(A) is within 10x of the reference's."""
+    import os
+    from paper_1906_12085_b200 import errors
+    from tests.datagen import config_matrix
+    gz = np.load(os.path.join(os.path.dirname(__file__), "golden", "c1.npz"))
+    ref_off, ref_conv = np.asarray(gz["ref_sweep_off"]), int(gz["ref_sweeps"])
+    c = sk.center(config_matrix("c1"), sk.Orientation.RowsAreExamples).centered
+    g = sk.gram(c)
+    offs, conv = [], None
+    for cap in range(1, 31):
+        try:
+            sk.eig_sym(g, cap)
+            conv = cap
+            break
+        except errors.NumericalError as e:
+            offs.append(e.residual())
+    print("engine trajectory", offs, "converged at", conv, "| reference", ref_off.tolist(), ref_conv)
+    assert conv is not None and abs(conv - ref_conv) <= 1
+    for k in range(min(len(offs), len(ref_off)) - 1):  # the last one sits at the rounding floor
+        assert ref_off[k] / 10 <= offs[k] <= ref_off[k] * 10, (k, offs[k], ref_off[k])

@@ -31,4 +31,36 @@ for cs in ("1", "2", "4"):
     sk.lanczos_svd(np.asfortranarray(rng.standard_normal((333, 150))), 0, sk.RngSeed(3))
     sk.lanczos_svd(b, 0, sk.RngSeed(4))
 os.environ.pop("SVDK_GEMV_CS")
+# rank-deficient qr_thin (eigen-based basis + the small Householder QR)
+h = np.asfortranarray(np.hstack([b[:, :5], b[:, :2] @ rng.standard_normal((2, 3))]))
+sk.qr_thin(h)
+# Lanczos tridiagonal solver, then its dense fallback
+a = np.asfortranarray(rng.standard_normal((900, 200)))
+sk.lanczos_svd(a, 0, sk.RngSeed(6))
+os.environ["SVDK_LANCZOS_TRIDIAG"] = "0"
+sk.lanczos_svd(a, 0, sk.RngSeed(6))
+os.environ.pop("SVDK_LANCZOS_TRIDIAG")
+# the synthetic generator (device) and the host-staged sharded path (2 ranks, threads)
+import threading  # noqa: E402
+
+import torch  # noqa: E402
+
+from paper_1906_12085_b200 import synth  # noqa: E402
+from paper_1906_12085_b200._lib import HostGroup  # noqa: E402
+from paper_1906_12085_b200.engine import Engine, colmajor  # noqa: E402
+eng = Engine(0)
+a_dev = synth.device_matrix(eng, 2002, 64, np.linspace(1.0, 0.1, 64), 1e-3)
+grp = HostGroup(2)
+engs = [Engine(0) for _ in range(2)]
+shards = []
+for r, e in enumerate(engs):
+    e.ctx.attach_host_group(grp, r)
+    s_ = colmajor(1001, 64)
+    s_.copy_(a_dev[1001 * r:1001 * (r + 1)])
+    shards.append(s_)
+torch.cuda.synchronize()
+ths = [threading.Thread(target=lambda r=r: engs[r].pca(shards[r], method=1, l=32, q=1, seed=3))
+       for r in range(2)]
+[t.start() for t in ths]
+[t.join() for t in ths]
 print("sanitize probe done")
