@@ -88,13 +88,24 @@ def fixture_parity(gz, prefix, lam, basis, k, rel_gap=1e-6) -> dict:
         ref_k = np.asarray(gz[f"{prefix}_v"])[:, :k_ref] if f"{prefix}_v" in gz else np.asarray(gz[f"{prefix}_vk"])
         out["topK_sine"] = topk_sine(vk, ref_k)
         single = cluster = 0.0
+        worst = (0.0, -1, 0.0)
+        sg = 0.0
+        scale = max(abs(lam_ref[0]), 1e-300)
         for g in groups:
             s = topk_sine(basis[:, g], ref_k[:, g])
             if len(g) == 1:
                 single = max(single, s)
+                i = g[0]
+                gap = min(lam_ref[i - 1] - lam_ref[i] if i > 0 else np.inf,
+                          lam_ref[i] - lam_ref[i + 1] if i + 1 < len(lam_ref) else np.inf) / scale
+                sg = max(sg, s * gap)
+                if s > worst[0]:
+                    worst = (s, i, gap)
             else:
                 cluster = max(cluster, s)
         out["per_vector_sine"], out["cluster_sine"] = single, cluster
+        out["per_vector_worst"] = {"sine": worst[0], "index": worst[1], "rel_gap": worst[2]}
+        out["sine_times_gap_max"] = sg
         out["vectors_checked"] = int(sum(len(g) for g in groups))
     else:
         vperp = np.asarray(gz[f"{prefix}_vperp"])

@@ -80,7 +80,9 @@ def test_config_parity(eng, name, method, l, q):
     lam = sigma * sigma  # fit_pca's eigenvalues (pca.cpp:110-113)
     basis = out.v[:, :out.rank].cpu().numpy()
     total = float(gz["total"])
-    assert abs(out.total - total) <= 1e-12 * total
+    # the total variance is a sum of m n squares: two summation orders differ by
+    # ~sqrt(m n) eps relative (c4: 8.6e9 terms); it only matters through K
+    assert abs(out.total - total) <= 1e-10 * total
     p = fixture_parity(gz, "truncated", lam, basis, out.k)
     print(name, method, p)
     assert parity_ok(p), p
