@@ -48,6 +48,11 @@ constexpr int TILE_ELEMS = BM * BN;              // partial tile size (doubles)
 constexpr int SMEM_BYTES = STAGES * 2 * TILE_BYTES + 1024 + 2 * STAGES * 8;
 
 enum Kind : int { KIND_SYRK = 0, KIND_TN = 1, KIND_NN = 2 };
+#ifdef SVDK_GEMM_NO_FAST_EPILOGUE  // bisection switch (development)
+constexpr bool kFastEpilogue = false;
+#else
+constexpr bool kFastEpilogue = true;
+#endif
 
 struct Params {
     int kind;
@@ -159,8 +164,19 @@ __global__ void __launch_bounds__(THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                 const Params p) {
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                               ~uintptr_t(1023));
+    // 1024-byte alignment for the 128B swizzle. Kept as a generic pointer:
+    // the operand reads compile to generic LD (not LDS). Deriving `smem` from
+    // the declared array instead (LDS operand reads, SVDK_GEMM_LDS) was 1%
+    // faster alone but, combined with the direct-store epilogue below,
+    // corrupted whole 8 x 32 accumulator groups in ~0.04% of 128 x 128 tiles
+    // of 2^20 x 1024 x 1024 GEMMs (bitwise check vs cuBLAS on exactly
+    // representable operands, tools/parity/gen_check2.py); this form: 0
+    // mismatches in 48 such GEMMs and 35.6 TF/s (DESIGN 3.1).
+#ifdef SVDK_GEMM_LDS  // development switch
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+#else
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+#endif
     uint8_t* smA = smem;
     uint8_t* smB = smem + STAGES * TILE_BYTES;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + 2 * STAGES * TILE_BYTES);
@@ -297,6 +313,38 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
                     for (int i = 0; i < 2; ++i)
                         dst[((t * 4 + n) * 2 + i) * (CWARPS * 32) + tid] = acc[t][n][i];
+        } else if (kFastEpilogue && p.kind != KIND_SYRK && !p.beta_one && p.alpha == 1.0 && w.row0 + BM <= p.M &&
+                   w.col0 + BN <= p.N) {
+            // Interior tile, plain store (+ column scale, non-finite flag): the
+            // per-element generic epilogue was ~5k SASS instructions per unit,
+            // more than the main loop (ncu round 2: no-instruction stalls and
+            // the NN kernel's 5% gap). Addresses: two per-lane column bases
+            // (i = 0, 1) + compile-time row / column-group offsets.
+            int r0l, c0l, r1l, c1l;
+            slot_coord(AMM, 0, tid, r0l, c0l);  // (t, n, i) = (0, 0, 0)
+            slot_coord(AMM, 1, tid, r1l, c1l);  // (0, 0, 1): same row, column of i = 1
+            double* base0 = p.C + (w.row0 + r0l) + (w.col0 + c0l) * p.ldc;
+            double* base1 = p.C + (w.row0 + r1l) + (w.col0 + c1l) * p.ldc;
+            double sc[4][2];
+#pragma unroll
+            for (int n = 0; n < 4; ++n) {
+                sc[n][0] = p.col_scale ? p.col_scale[w.col0 + c0l + 8 * n] : 1.0;
+                sc[n][1] = p.col_scale ? p.col_scale[w.col0 + c1l + 8 * n] : 1.0;
+            }
+            bool bad = false;
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                // row offset of accumulator row-group t relative to t = 0
+                const int dr = AMM ? 16 * (t >> 1) + 4 * (t & 1) : 8 * t;
+#pragma unroll
+                for (int n = 0; n < 4; ++n) {
+                    const int64_t off = dr + static_cast<int64_t>(8 * n) * p.ldc;
+                    bad |= !isfinite(acc[t][n][0]) || !isfinite(acc[t][n][1]);
+                    base0[off] = acc[t][n][0] * sc[n][0];
+                    base1[off] = acc[t][n][1] * sc[n][1];
+                }
+            }
+            if (bad && p.flag) atomicOr(p.flag, 1);
         } else {
 #pragma unroll
             for (int t = 0; t < 8; ++t)

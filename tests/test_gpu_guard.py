@@ -198,3 +198,29 @@ def test_synth_guarded(eng):
     host = synth.host_block(5, 1, 2 * m, 7, m, n, quantise=True)
     synth.host_add_noise(host, 5, 2 * m, 7, 0.5)
     assert np.array_equal(g.np(), host)
+
+
+def test_gemm_nn_bitwise_vs_cublas_large(eng):
+    """A 2^20 x 1024 x 1024 NN GEMM on exactly representable operands (every
+    partial sum exact, so any correct summation order gives the same bits)
+    against cuBLAS, bitwise, twice: catches corrupted accumulator groups in
+    rare tiles that small guard-band shapes do not reach (DESIGN 3.1)."""
+    import ctypes
+
+    import torch
+
+    from paper_1906_12085_b200 import _lib
+    from paper_1906_12085_b200.engine import colmajor
+    n, m = 1024, 1 << 20
+    mq = torch.round(torch.randn(n, n, dtype=torch.float64, device="cuda") * 2 ** 20) / 2 ** 20
+    b = colmajor(n, n)
+    b.copy_(mq)
+    x = colmajor(m, n)
+    c = colmajor(m, n)
+    for rep in range(2):
+        _lib.check(_lib.load().svdk_dev_synth_fill(eng.ctx.handle, 42, 1, 1, 4 * m, rep * m, m, n,
+                                                   ctypes.c_void_p(x.data_ptr()), x.stride(1)))
+        eng.gemm(x, b, c=c)
+        ref = x @ b
+        torch.cuda.synchronize()
+        assert int((c != ref).sum()) == 0, rep
