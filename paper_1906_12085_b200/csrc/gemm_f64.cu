@@ -465,7 +465,9 @@ void launch(Ctx* c, Params& p, const CUtensorMap& ma, const CUtensorMap& mb) {
     const double bytes = p.kind == KIND_SYRK ? 8.0 * (p.K * p.M + p.M * p.M)
                                              : 8.0 * (p.M * p.K + p.K * p.N + p.M * p.N);
     {
-        PhaseTimer timer(c, "dmma_gemm", flops, bytes);
+        // one phase per kernel form, so bench.py can report the dominant one
+        PhaseTimer timer(c, p.kind == KIND_SYRK ? "dmma_syrk" : (p.a_mmajor ? "dmma_gemm_nn" : "dmma_gemm_tn"),
+                         flops, bytes);
         if (p.a_mmajor)
             gemm_kernel<true><<<grid, THREADS, SMEM_BYTES, c->stream>>>(ma, mb, p);
         else
@@ -587,7 +589,7 @@ void launch_small(Ctx* c, int kind, int64_t M, int64_t N, int64_t K, const doubl
     const int tiles_m = static_cast<int>(ceil_div(M, ST)), tiles_n = static_cast<int>(ceil_div(N, ST));
     const double flops = kind == KIND_SYRK ? static_cast<double>(K) * M * (M + 1) : 2.0 * M * N * K;
     const double bytes = kind == KIND_SYRK ? 8.0 * (K * M + M * M) : 8.0 * (M * K + K * N + M * N);
-    PhaseTimer timer(c, "dmma_gemm", flops, bytes);
+    PhaseTimer timer(c, "dmma_gemm_small", flops, bytes);
     gemm_small_kernel<<<tiles_m * tiles_n, 128, 0, c->stream>>>(kind, M, N, K, A, lda, B, ldb, C, ldc, alpha,
                                                                 beta_one ? 1 : 0, col_scale, flag, tiles_n);
     SVDK_CHECK_LAUNCH();

@@ -9,20 +9,27 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import bench  # noqa: E402
-from paper_1906_12085_b200.engine import Engine, colmajor  # noqa: E402
+from paper_1906_12085_b200 import synth  # noqa: E402
+from paper_1906_12085_b200.engine import Engine  # noqa: E402
 
-name = sys.argv[1] if len(sys.argv) > 1 else "c2"
-cfg = dict(bench.CONFIGS[name])
-m, n = cfg["m"], cfg["n"]
+name = sys.argv[1] if len(sys.argv) > 1 else "c4"
+cfg = bench.config(name)
 eng = Engine(0)
 torch.cuda.set_stream(eng.stream)
-A = bench.generate(cfg, m, torch.device("cuda", 0), 0)
+A, _ = bench.generate(eng, cfg, 1, 0)
 mid = bench.METHOD_ID[cfg["method"]]
-out = eng.pca(A, method=mid, l=cfg["l"], q=cfg["q"], seed=4242, center=2, threshold=cfg["t"])
-out = eng.pca(A, method=mid, l=cfg["l"], q=cfg["q"], seed=4242, center=2, threshold=cfg["t"], out=out)
+
+
+def step(out=None):
+    return eng.pca(A, method=mid, l=cfg["l"], q=cfg["q"], seed=synth.METHOD_SEED, center=2, threshold=cfg["t"],
+                   out=out)
+
+
+out = step()
+out = step(out)
 torch.cuda.synchronize()
 torch.cuda.cudart().cudaProfilerStart()
-out = eng.pca(A, method=mid, l=cfg["l"], q=cfg["q"], seed=4242, center=2, threshold=cfg["t"], out=out)
+out = step(out)
 torch.cuda.synchronize()
 torch.cuda.cudart().cudaProfilerStop()
 print("K", out.k, "rank", out.rank)
