@@ -241,6 +241,7 @@ int svdk_ctx_destroy(svdk_ctx* ctx) {
         destroy_comm(ctx);
         release_host_staging(ctx);
         jacobi_cache_free(ctx);
+        release_upload_staging(ctx);
         ctx->pool.trim();
         if (ctx->d_flags) cudaFree(ctx->d_flags);
         for (cudaEvent_t e : ctx->event_pool) cudaEventDestroy(e);

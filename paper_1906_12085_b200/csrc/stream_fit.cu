@@ -163,14 +163,18 @@ bool streamed_sketch_rows(Ctx* c, const double* host, int64_t m, int64_t n, int6
         // Omega goes through the copy engine right after chunk 0 (both on the
         // copy stream; queued on the context stream it would wait behind every
         // chunk of A in the engine's FIFO), while the host joins its sampler.
-        for (int64_t k = 0; k < C; ++k) {
+        // Each chunk's copy is enqueued right before its compute: with a
+        // pageable host buffer the enqueue packs the chunk through pinned
+        // staging on this thread (HostUploader), which then overlaps the DMA
+        // and compute of the chunks before it.
+        HostUploader up(c, host);
+        auto enqueue_copy = [&](int64_t k) {
             const int64_t r0 = k * rows, mk = std::min(rows, m - r0);
-            SVDK_CUDA(cudaMemcpy2DAsync(dA.p() + r0, lda * sizeof(double), host + r0, m * sizeof(double),
-                                        mk * sizeof(double), n, cudaMemcpyHostToDevice, c->copy_stream));
+            up.copy2d(dA.p() + r0, lda * sizeof(double), host + r0, m * sizeof(double), mk * sizeof(double), n);
             if (k == 0) omega_upload(c, n, l, seed, Om.p(), c->copy_stream);
             SVDK_CUDA(cudaEventCreateWithFlags(&landed[k], cudaEventDisableTiming));
             SVDK_CUDA(cudaEventRecord(landed[k], c->copy_stream));
-        }
+        };
         const bool trace = std::getenv("SVDK_STREAM_TRACE") != nullptr;
         std::vector<cudaEvent_t> tev;
         auto mark = [&](cudaStream_t st) {
@@ -185,6 +189,7 @@ bool streamed_sketch_rows(Ctx* c, const double* host, int64_t m, int64_t n, int6
             const int64_t r0 = k * rows, mk = std::min(rows, m - r0);
             double* Ak = dA.p() + r0;
             double* muk = mu_k.p() + k * n;
+            enqueue_copy(k);
             SVDK_CUDA(cudaStreamWaitEvent(S, landed[k], 0));
             mark(S);
             column_sums(c, Ak, lda, mk, n, static_cast<double>(mk), muk);
@@ -281,7 +286,6 @@ bool fit_pca_streamed(Ctx* c, const double* host, int64_t m, int64_t n, int meth
     reset_nonfinite(c);
     {
         PhaseTimer timer(c, "streamed_upload");
-        // every chunk's copy is enqueued first (one event each)
         std::vector<cudaEvent_t> landed(static_cast<size_t>(C), nullptr);
         struct Events {
             std::vector<cudaEvent_t>& v;
@@ -293,21 +297,17 @@ bool fit_pca_streamed(Ctx* c, const double* host, int64_t m, int64_t n, int meth
         // the copy stream may only overwrite dA once it is ours on S (pool reuse)
         SVDK_CUDA(cudaEventRecord(c->copy_ev, S));
         SVDK_CUDA(cudaStreamWaitEvent(c->copy_stream, c->copy_ev, 0));
-        for (int64_t k = 0; k < C; ++k) {
-            const int64_t j0 = k * nc, cols = std::min(nc, n - j0);
-            if (lda == m)
-                SVDK_CUDA(cudaMemcpyAsync(dA.p() + j0 * lda, host + j0 * m, sizeof(double) * m * cols,
-                                          cudaMemcpyHostToDevice, c->copy_stream));
-            else
-                SVDK_CUDA(cudaMemcpy2DAsync(dA.p() + j0 * lda, lda * sizeof(double), host + j0 * m,
-                                            m * sizeof(double), m * sizeof(double), cols, cudaMemcpyHostToDevice,
-                                            c->copy_stream));
-            SVDK_CUDA(cudaEventCreateWithFlags(&landed[k], cudaEventDisableTiming));
-            SVDK_CUDA(cudaEventRecord(landed[k], c->copy_stream));
-        }
+        HostUploader up(c, host);  // see streamed_sketch_rows: copy k is enqueued right before compute k
         for (int64_t k = 0; k < C; ++k) {
             const int64_t j0 = k * nc, cols = std::min(nc, n - j0), j1 = j0 + cols;
             double* Ak = dA.p() + j0 * lda;
+            if (lda == m)
+                up.copy2d(Ak, sizeof(double) * m * cols, host + j0 * m, sizeof(double) * m * cols,
+                          sizeof(double) * m * cols, 1);
+            else
+                up.copy2d(Ak, lda * sizeof(double), host + j0 * m, m * sizeof(double), m * sizeof(double), cols);
+            SVDK_CUDA(cudaEventCreateWithFlags(&landed[k], cudaEventDisableTiming));
+            SVDK_CUDA(cudaEventRecord(landed[k], c->copy_stream));
             SVDK_CUDA(cudaStreamWaitEvent(S, landed[k], 0));
             // whole columns: mean, subtract and sum of squares exactly as for the full matrix
             column_sums(c, Ak, lda, m, cols, static_cast<double>(m), mu.p() + j0);

@@ -77,6 +77,7 @@ private:
 struct Ctx;
 struct HostGroup;    // in-process collective group (comm.cu)
 struct JacobiCache;  // instantiated eig_sym sweep plans (jacobi.cu)
+struct UploadStaging;  // pinned staging slots + packing threads (host_upload.cu)
 
 // RAII device buffer of doubles from the context pool.
 class DBuf {
@@ -146,6 +147,7 @@ struct Ctx {
     // counters for bench/introspection
     int64_t launches = 0;
     JacobiCache* jacobi_cache = nullptr;
+    UploadStaging* upload = nullptr;
     int jacobi_sweeps = 0;
     double last_off_norm = 0.0;
 };
@@ -235,6 +237,23 @@ void eig_sym(Ctx* c, const double* S, int64_t lds, int64_t n, int max_sweeps, do
              double* V, int64_t ldv);
 // release the cached sweep plans (before the context's pool is trimmed)
 void jacobi_cache_free(Ctx* c);
+
+// Host -> device copies from a caller's buffer on ctx->copy_stream: direct DMA
+// for page-locked memory, packed through pinned staging slots by host threads
+// for pageable memory (host_upload.cu). copy2d may block the calling thread
+// (pageable: while it packs), so callers interleave it with their compute
+// enqueues.
+class HostUploader {
+public:
+    HostUploader(Ctx* c, const void* base);
+    void copy2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t height);
+    bool pageable() const { return pageable_; }
+
+private:
+    Ctx* c_;
+    bool pageable_;
+};
+void release_upload_staging(Ctx* c);
 
 // Host <-> device
 void h2d(Ctx* c, double* dst, const double* src, int64_t count);
