@@ -124,7 +124,7 @@ HostUploader::HostUploader(Ctx* c, const void* base) : c_(c), pageable_(!host_is
             SVDK_CUDA(cudaEventCreateWithFlags(&u->ev[i], cudaEventDisableTiming));
         }
         const unsigned hw = std::thread::hardware_concurrency();
-        u->pool = new CopyPool(static_cast<int>(std::clamp(hw / 2, 1u, 16u)));
+        u->pool = new CopyPool(static_cast<int>(std::clamp(hw > 2 ? hw - 2 : 1u, 1u, 24u)));
     }
 }
 

@@ -143,3 +143,63 @@ def test_sharded_sketch_param_error_everywhere(base):
     m = a.shape[0]
     outs = run_sharded(a, [0, m // 3, m], "randomized", cfg.t, {0: dict(l=512), 1: dict(l=512)})
     assert all(isinstance(o, errors.ParamError) for o in outs), outs
+
+
+def test_c4_world2_vs_reference_fixture(sk):
+    """BASELINE c4 itself, row-sharded over 2 ranks (host-staged group, both on
+    this GPU): each rank generates ITS half of the rows (synth.device_rows with
+    the allreduced X^T X), runs svdk_dev_pca on it (centre in place), and the
+    result must meet the full-size reference bars of tests/golden/c4.npz."""
+    import os
+
+    import torch
+
+    from paper_1906_12085_b200._lib import HostGroup
+    from paper_1906_12085_b200.engine import Engine
+    from tests.parity import fixture_parity, parity_ok
+    path = os.path.join(os.path.dirname(__file__), "golden", "c4.npz")
+    if not os.path.exists(path):
+        pytest.skip("c4 fixture not generated")
+    free, _ = torch.cuda.mem_get_info()
+    if free < 150e9:
+        pytest.skip("needs ~140 GB of free HBM")
+    gz = np.load(path)
+    cfg = synth.CONFIGS["c4"]
+    world = 2
+    bounds = [cfg.m * r // world for r in range(world + 1)]
+    group = HostGroup(world)
+    engines = [Engine(0) for _ in range(world)]
+    for r, e in enumerate(engines):
+        e.ctx.attach_host_group(group, r)
+    # the allreduce of the per-rank partial X^T X (exact on the generator's grid)
+    parts = [synth.device_gram_x(engines[r], cfg.m, cfg.n, row0=bounds[r], rows=bounds[r + 1] - bounds[r])
+             for r in range(world)]
+    g = parts[0] + parts[1]
+    mix, _ = synth.mixing(g.cpu().numpy(), cfg.spectrum(), synth.MATRIX_SEED)
+    del parts, g
+    shards = [synth.device_rows(engines[r], mix, cfg.m, cfg.n, cfg.sigma, row0=bounds[r],
+                                rows=bounds[r + 1] - bounds[r]) for r in range(world)]
+    torch.cuda.synchronize()
+    outs = [None] * world
+
+    def work(r):
+        try:
+            outs[r] = engines[r].pca(shards[r], method=0, center=2, threshold=cfg.t)
+        except Exception as e:
+            outs[r] = e
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+    [t.start() for t in th]
+    [t.join(timeout=900) for t in th]
+    assert not any(t.is_alive() for t in th)
+    for o in outs:
+        assert not isinstance(o, Exception), o
+    o = outs[1]
+    s = o.sigma[:o.rank].cpu().numpy()
+    p = fixture_parity(gz, "truncated", s * s, o.v[:, :o.rank].cpu().numpy(), o.k)
+    print("c4 world 2", p)
+    assert abs(o.total - float(gz["total"])) <= 1e-10 * float(gz["total"])
+    assert parity_ok(p), p
+    for e in engines:
+        e.ctx.detach_comm()
+    group.close()
