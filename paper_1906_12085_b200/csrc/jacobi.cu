@@ -1123,13 +1123,14 @@ __global__ void jacobi_init_kernel(const double* S, int64_t lds, int64_t n, doub
 }
 
 // partial sums of squares: mode 0 = all entries, mode 1 = strictly lower.
+// Block b sums the columns b, b + grid, ... (rows i > j in mode 1), coalesced
+// along the column, with a fixed order: deterministic partials.
 __global__ void jacobi_sumsq_kernel(const double* A, int64_t n, int mode, double* partial) {
     __shared__ double red[32];
     double s = 0.0;
-    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n * n;
-         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t j = e / n, i = e - j * n;
-        if (mode == 0 || i > j) s = fma(A[e], A[e], s);
+    for (int64_t j = blockIdx.x; j < n; j += gridDim.x) {
+        const double* col = A + j * n;
+        for (int64_t i = (mode ? j + 1 : 0) + threadIdx.x; i < n; i += blockDim.x) s = fma(col[i], col[i], s);
     }
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
@@ -1177,6 +1178,15 @@ __global__ void eig_gather_kernel(const double* V, int64_t n_pad, int64_t n, con
 enum { JS_THR = 0, JS_SKIP, JS_OFF, JS_SWEEPS, JS_SCALE, JS_UNSCALE, JS_MABS, JS_MASYM, JS_MAXSW, JS_FRO,
        JS_POLISH, JS_CONT, JS_POLISH_ON, JS_COUNT };
 
+// Fixed-order warp sum / max of count partials (lane-strided sequential sums
+// then a fixed xor tree: deterministic, ~30x shorter than one thread's loop).
+__device__ __forceinline__ double warp_sum_fixed(const double* partial, int count) {
+    double s = 0.0;
+    for (int i = threadIdx.x; i < count; i += 32) s += partial[i];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    return s;
+}
+
 // After a sweep: off(A) from the partials; continue while off > thr and
 // sweeps < max_sweeps (kernels.cpp:274-326). Once converged, ONE polish sweep
 // follows (JS_POLISH 0 -> 1 -> 2): the block-parallel order leaves its last
@@ -1187,13 +1197,13 @@ enum { JS_THR = 0, JS_SKIP, JS_OFF, JS_SWEEPS, JS_SCALE, JS_UNSCALE, JS_MABS, JS
 // sweep trajectory are the reference's.
 __global__ void jacobi_decide_kernel(cudaGraphConditionalHandle h, const double* partial, int count,
                                      double* scal, int use_cond) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (blockIdx.x != 0) return;
+    const double s = warp_sum_fixed(partial, count);  // all 32 lanes
+    if (threadIdx.x != 0) return;
     double cont = 0.0;
     if (scal[JS_POLISH] != 0.0) {
         scal[JS_POLISH] = 2.0;  // the polish sweep ran
     } else {
-        double s = 0.0;
-        for (int i = 0; i < count; ++i) s += partial[i];
         const double off = sqrt(2.0 * s);
         const double sw = scal[JS_SWEEPS] + 1.0;
         scal[JS_OFF] = off;
@@ -1214,10 +1224,9 @@ __global__ void jacobi_decide_kernel(cudaGraphConditionalHandle h, const double*
 // strictly-lower partials; sweep only if off > thr (and max_sweeps > 0).
 __global__ void jacobi_start_kernel(cudaGraphConditionalHandle h, const double* p_all, const double* p_low,
                                     int count, double n_pad, double* scal, int use_cond) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    double s0 = 0.0, s1 = 0.0;
-    for (int i = 0; i < count; ++i) s0 += p_all[i];
-    for (int i = 0; i < count; ++i) s1 += p_low[i];
+    if (blockIdx.x != 0) return;
+    const double s0 = warp_sum_fixed(p_all, count), s1 = warp_sum_fixed(p_low, count);
+    if (threadIdx.x != 0) return;
     const double fro = sqrt(s0), off = sqrt(2.0 * s1);
     scal[JS_FRO] = fro;
     scal[JS_THR] = 1e-12 * fro;
@@ -1234,12 +1243,17 @@ __global__ void jacobi_start_kernel(cudaGraphConditionalHandle h, const double* 
 // power-of-two prescale (entries whose squares cannot over/underflow) and
 // the sweep cap, all on the device (no host round trip before the sweeps).
 __global__ void eig_prep_kernel(const double* partial, int count, int max_sweeps, int polish, double* scal) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (blockIdx.x != 0) return;
     double mabs = 0.0, masym = 0.0;
-    for (int b = 0; b < count; ++b) {
+    for (int b = threadIdx.x; b < count; b += 32) {
         mabs = fmax(mabs, partial[2 * b]);
         masym = fmax(masym, partial[2 * b + 1]);
     }
+    for (int o = 16; o > 0; o >>= 1) {
+        mabs = fmax(mabs, __shfl_xor_sync(0xffffffffu, mabs, o));
+        masym = fmax(masym, __shfl_xor_sync(0xffffffffu, masym, o));
+    }
+    if (threadIdx.x != 0) return;
     int pow2 = 0;
     if (mabs > 0.0 && (mabs > 1e100 || mabs < 1e-100)) pow2 = ilogb(mabs);
     scal[JS_SCALE] = ldexp(1.0, -pow2);
@@ -2099,7 +2113,7 @@ JacobiPlan& jacobi_plan(Ctx* c, int64_t n_pad, int TB) {
     p->tb = TB;
     p->A = DBuf(c, static_cast<size_t>(n_pad) * n_pad);
     p->V = DBuf(c, static_cast<size_t>(n_pad) * n_pad);
-    p->blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_pad * n_pad, 256), 2 * c->num_sms)));
+    p->blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(n_pad, 2 * c->num_sms)));  // column-strided sumsq
     p->part_all = DBuf(c, 2 * static_cast<size_t>(std::max<int64_t>(p->blocks, 2 * c->num_sms)));
     p->part_low = DBuf(c, static_cast<size_t>(p->blocks));
     p->scal = DBuf(c, JS_COUNT);
