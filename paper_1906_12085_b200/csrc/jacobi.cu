@@ -287,12 +287,14 @@ __device__ __forceinline__ void look_finish(const LookRead& r, double skip_tau, 
 //               holding p and q, their roles and their (row, col) indices —
 //               bits 0-4 bp, 5-9 bq, 10 role_p, 11 role_q, 12-16 p_bp,
 //               17-21 q_bp, 22-26 p_bq, 27-31 q_bq (one LDS for the lookahead)
+//   part[r][x]  the index paired with x in round r | role << 7
 template <int TB>
 struct __align__(16) SolveTables {
     static constexpr int kNP = TB / 2;
     unsigned long long look[TB - 1][TB / 2];
     int ptab[TB - 1][TB / 2];
     unsigned char pinv[TB - 1][TB];
+    unsigned char part[TB - 1][TB];  // partner of index x in round r | role << 7 (one-sided solve)
 };
 static_assert(sizeof(SolveTables<32>) % 16 == 0 && sizeof(SolveTables<16>) % 16 == 0, "uint4 copy");
 
@@ -307,7 +309,10 @@ __global__ void jacobi_tables_kernel(SolveTables<TB>* out) {
         t.ptab[e / NP][e % NP] = 0;
         t.look[e / NP][e % NP] = 0;
     }
-    for (int e = threadIdx.x; e < (TB - 1) * TB; e += blockDim.x) t.pinv[e / TB][e % TB] = 0;
+    for (int e = threadIdx.x; e < (TB - 1) * TB; e += blockDim.x) {
+        t.pinv[e / TB][e % TB] = 0;
+        t.part[e / TB][e % TB] = 0;
+    }
     __syncthreads();
     for (int e = threadIdx.x; e < R * NP; e += blockDim.x) {
         int p, q;
@@ -341,6 +346,11 @@ __global__ void jacobi_tables_kernel(SolveTables<TB>* out) {
             (static_cast<unsigned long long>(t.ptab[rr][bp] >> 8) << 17) |
             (static_cast<unsigned long long>(t.ptab[rr][bq] & 255) << 22) |
             (static_cast<unsigned long long>(t.ptab[rr][bq] >> 8) << 27);
+    }
+    for (int e = threadIdx.x; e < R * TB; e += blockDim.x) {
+        const int r = e / TB, x = e % TB;
+        const int code = t.pinv[r][x], role = code >> 7, pq = t.ptab[r][code & 127];
+        t.part[r][x] = static_cast<unsigned char>((role ? (pq & 255) : (pq >> 8)) | (role << 7));
     }
     __syncthreads();
     const uint4* src = reinterpret_cast<const uint4*>(&t);
@@ -560,6 +570,233 @@ __global__ void __launch_bounds__(solve_threads<TB>())
     jacobi_pair_solve(const double* A, int64_t lda, const SolveTables<TB>* tabs, double* Qbuf,
                       int* active, int nb, int round, const double* skip_tau_p, int max_inner, int mode) {
     solve_pair<TB>(A, lda, tabs, Qbuf, active, nb, round, skip_tau_p, max_inner, mode, blockIdx.x);
+}
+
+
+// ---------------------------------------------------------------------------
+// 1b. one-sided pair solve (2b = 32, the default for every n > 64)
+// ---------------------------------------------------------------------------
+// The same rotations in the same order as solve_pair, but the subproblem is
+// never updated two-sidedly. The CTA keeps Q (starts at I) and W = M Q (starts
+// at M) and applies every rotation as a COLUMN operation to both, so that the
+// three numbers a rotation needs are dot products,
+//     (Q^T M Q)_pp = q_p . w_p,   (Q^T M Q)_qq = q_q . w_q,   (Q^T M Q)_pq = q_p . w_q
+// (the symmetric-eigenproblem form of Hestenes' one-sided method; M may be
+// indefinite). Lane l of every warp owns column l, warp h the rows
+// [h QR, (h+1) QR) of both matrices: 2 QR registers per lane, the partner
+// column arrives by warp shuffles, and the only cross-warp traffic of an inner
+// round is the QW partial sums per dot product through shared memory (summed
+// in warp order by every lane, so all warps form bit-identical (c, s)) behind
+// ONE block barrier. The serial chain of a round is
+//     shuffle -> partial dots -> STS | barrier | LDS -> sum -> rotation -> apply
+// with QW warps instead of 13, no M threads, no lookahead and ~100 instead of
+// ~390 shared-memory wavefronts (solve_pair: ~1230 cycles per inner round,
+// §3.2 of DESIGN.md). a_pq is formed with an absolute error of a few
+// eps ||M||, the same floor the DMMA similarity Q^T A Q of the update kernels
+// has; the convergence test stays on the explicitly updated A.
+// 1 / sqrt(x) for normal x > 0 from the hardware seed (rsqrt.approx.ftz.f64, ~2^-22) and
+// one third-order step y (1 + e/2 + 3e^2/8), e = 1 - x y^2: a 4-DFMA chain behind the
+// MUFU instead of rsqrt()'s ~100 cycles (its special-case handling is not needed:
+// eig_sym prescales so that d^2 + e^2 stays normal).
+__device__ __forceinline__ double rsqrt_seed(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    return y;
+}
+__device__ __forceinline__ double rsqrt_refine(double x, double y0) {
+    const double t = x * y0;
+    const double e = fma(-t, y0, 1.0);
+    return fma(y0 * e, fma(0.375, e, 0.5), y0);
+}
+// rotation() with the second square root's seed formed speculatively from the
+// first one's seed, so the two refinements are the only dependent DFMA chains
+// (~140 instead of ~210 cycles; same formulas, results equal to a few ulps).
+__device__ __forceinline__ void rotation_fast(double app, double aqq, double apq, double& c, double& s) {
+    const double d = aqq - app, e = 2.0 * apq, e2 = e * e, ad = fabs(d);
+    const double r2 = fma(d, d, e2);
+    const double y0 = rsqrt_seed(r2);
+    const double Dt = ad + r2 * y0;
+    const double z0 = rsqrt_seed(fma(Dt, Dt, e2));  // seed of the second root, off the precise chain
+    const double D = ad + r2 * rsqrt_refine(r2, y0);  // |d| + sqrt(d^2 + e^2)
+    const double inv = rsqrt_refine(fma(D, D, e2), z0);
+    c = D * inv;
+    s = (d > 0.0 ? e : (d < 0.0 ? -e : fabs(e))) * inv;  // tau = +-0 -> t = +1
+}
+
+__device__ __forceinline__ double4 ld_cg4(const double* p);
+__device__ __forceinline__ void st4(double* p, double a, double b, double c, double d);
+
+template <int QW, bool NS, bool FAST>
+__global__ void __launch_bounds__(32 * QW)
+    jacobi_pair_solve_os(const double* A, int64_t lda, const SolveTables<32>* tabs, double* Qbuf,
+                         int* active, int nb, int round, const double* skip_tau_p, int max_inner, int mode) {
+    constexpr int TB = 32, B = 16, LD = TB + 4, QR = TB / QW;
+    static_assert(QR % 4 == 0 && QR <= 16, "row slabs are 32-byte vectors inside one 16-index block");
+    __shared__ __align__(16) unsigned char sched[TB - 1][TB];
+    __shared__ double pd[2][QW][TB], px[2][QW][TB];
+    __shared__ double Qs[TB * LD], Ms[TB * LD], Ts[TB * LD];
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, pair = blockIdx.x;
+    const int R = mode == 0 ? TB - 1 : (mode == 1 ? B - 1 : B);
+    const bool probe = pair == 0 && round == 5 && tid == 0;
+    const long long t0 = SVDK_CLOCK();
+    int I, J;
+    circle_pair(nb, round, pair, I, J);
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(&tabs[mode].part[0][0]);
+        uint4* dst = reinterpret_cast<uint4*>(&sched[0][0]);
+        pdl_trigger();
+        for (int e = tid; e < static_cast<int>(sizeof(sched) / 16); e += 32 * QW) dst[e] = src[e];
+    }
+    pdl_wait();  // A (and the Q / active slots) of the previous round's update
+    const double skip_tau = *skip_tau_p;
+    const int row0 = w * QR;
+    double wreg[QR], qreg[QR];
+    bool big = false;
+    {
+        const double* col = A + gidx(B, I, J, row0) + gidx(B, I, J, lane) * lda;
+#pragma unroll
+        for (int v = 0; v < QR / 4; ++v) {
+            const double4 x = ld_cg4(col + 4 * v);
+            wreg[4 * v] = x.x; wreg[4 * v + 1] = x.y; wreg[4 * v + 2] = x.z; wreg[4 * v + 3] = x.w;
+        }
+#pragma unroll
+        for (int i = 0; i < QR; ++i) {
+            big |= (row0 + i != lane) && fabs(wreg[i]) > skip_tau;
+            qreg[i] = (row0 + i == lane) ? 1.0 : 0.0;
+        }
+    }
+    const bool work = __syncthreads_or(big) != 0;
+    if (probe && work) {
+        SVDK_PROBE_STORE(g_jprobe, 0, t0);
+        SVDK_PROBE_STORE(g_jprobe, 1, SVDK_CLOCK());
+    }
+    if (work) {
+        const int total = max_inner * R;
+        int code = sched[0][lane], rr = 0;
+        for (int it = 0; it < total; ++it) {
+            const int partner = code & 31, role = code >> 7, buf = it & 1;
+            rr = rr + 1 == R ? 0 : rr + 1;
+            code = sched[rr][lane];  // next round's pairing, off the chain
+#ifdef SVDK_PROBES
+            const bool pr = probe && it == 10;
+            long long ta = 0;
+            if (pr) ta = clock64();
+#endif
+            double oq[QR], ow[QR];
+#pragma unroll
+            for (int i = 0; i < QR; ++i) {
+                oq[i] = __shfl_sync(0xffffffffu, qreg[i], partner);
+                ow[i] = __shfl_sync(0xffffffffu, wreg[i], partner);
+            }
+            // partial dots over this warp's rows: own diagonal and (role p) q_p . w_q
+            double d0 = qreg[0] * wreg[0], d1 = qreg[1] * wreg[1];
+            double x0 = qreg[0] * ow[0], x1 = qreg[1] * ow[1];
+#pragma unroll
+            for (int i = 2; i < QR; i += 2) {
+                d0 = fma(qreg[i], wreg[i], d0);
+                d1 = fma(qreg[i + 1], wreg[i + 1], d1);
+                x0 = fma(qreg[i], ow[i], x0);
+                x1 = fma(qreg[i + 1], ow[i + 1], x1);
+            }
+            pd[buf][w][lane] = d0 + d1;
+            px[buf][w][lane] = x0 + x1;
+#ifdef SVDK_PROBES
+            if (pr) g_jprobe[4] = clock64() - ta;  // shuffles + dots issued
+#endif
+            __syncthreads();
+#ifdef SVDK_PROBES
+            if (pr) g_jprobe[5] = clock64() - ta;  // past the barrier
+#endif
+            const int pl = role ? partner : lane;  // the pair's p column
+            double ds = 0.0, dp = 0.0, xs = 0.0;
+#pragma unroll
+            for (int h = 0; h < QW; h += 2) {  // fixed order: identical bits in every warp
+                ds += pd[buf][h][lane] + pd[buf][h + 1][lane];
+                dp += pd[buf][h][partner] + pd[buf][h + 1][partner];
+                xs += px[buf][h][pl] + px[buf][h + 1][pl];
+            }
+#ifdef SVDK_PROBES
+            if (pr) {
+                double u;
+                asm volatile("add.f64 %0, %1, %2;" : "=d"(u) : "d"(ds + dp), "d"(xs));
+                g_jprobe[6] = clock64() - ta;  // partial sums landed
+                g_jprobe[13] = static_cast<long long>(u);
+            }
+#endif
+            double c = 1.0, s = 0.0;
+            if (fabs(xs) > skip_tau) {
+                if (FAST)
+                    rotation_fast(role ? dp : ds, role ? ds : dp, xs, c, s);
+                else
+                    rotation(role ? dp : ds, role ? ds : dp, xs, c, s);
+            }
+#ifdef SVDK_PROBES
+            if (pr) {
+                double u;
+                asm volatile("add.f64 %0, %1, %2;" : "=d"(u) : "d"(c), "d"(s));
+                g_jprobe[7] = clock64() - ta;  // rotation done
+                g_jprobe[14] = static_cast<long long>(u);
+            }
+#endif
+            const double b = role ? s : -s;  // column p: c q_p - s q_q; column q: s q_p + c q_q
+#pragma unroll
+            for (int i = 0; i < QR; ++i) {
+                qreg[i] = fma(b, oq[i], c * qreg[i]);
+                wreg[i] = fma(b, ow[i], c * wreg[i]);
+            }
+#ifdef SVDK_PROBES
+            if (pr) {
+                double u;
+                asm volatile("add.f64 %0, %1, %2;" : "=d"(u) : "d"(qreg[0]), "d"(wreg[QR - 1]));
+                g_jprobe[8] = clock64() - ta;  // applied
+                g_jprobe[15] = static_cast<long long>(u);
+            }
+#endif
+        }
+        if (probe) SVDK_PROBE_STORE(g_jprobe, 2, SVDK_CLOCK());
+        if (NS) {
+#pragma unroll
+            for (int i = 0; i < QR; ++i) Qs[(row0 + i) + lane * LD] = qreg[i];
+            __syncthreads();
+            // Newton-Schulz step Q <- Q (3I - Q^T Q) / 2 (see solve_pair)
+            smem_mma<TB, true>(Qs, Qs, Ms);
+            __syncthreads();
+            for (int e = tid; e < TB * TB; e += 32 * QW) {
+                const int i = e % TB, j = e / TB;
+                Ms[i + j * LD] = (i == j ? 1.5 : 0.0) - 0.5 * Ms[i + j * LD];
+            }
+            __syncthreads();
+            smem_mma<TB, false>(Qs, Ms, Ts);
+            __syncthreads();
+            for (int e = tid; e < TB * TB; e += 32 * QW)
+                Qbuf[static_cast<size_t>(pair) * TB * TB + e] = Ts[(e % TB) + (e / TB) * LD];
+        } else {
+            // A rotation with c^2 + s^2 = 1 + delta scales its two columns and keeps
+            // them orthogonal (J^T J = (1 + delta) I), so the accumulated Q departs
+            // from orthogonality in its column norms only (plus unbiased rounding of
+            // the column operations): one Newton step on each column's norm,
+            // q <- q (3 - |q|^2) / 2, replaces the Newton-Schulz products.
+            double n0 = qreg[0] * qreg[0], n1 = qreg[1] * qreg[1];
+#pragma unroll
+            for (int i = 2; i < QR; i += 2) {
+                n0 = fma(qreg[i], qreg[i], n0);
+                n1 = fma(qreg[i + 1], qreg[i + 1], n1);
+            }
+            const int buf = total & 1;
+            pd[buf][w][lane] = n0 + n1;
+            __syncthreads();
+            double nn = 0.0;
+#pragma unroll
+            for (int h = 0; h < QW; h += 2) nn += pd[buf][h][lane] + pd[buf][h + 1][lane];
+            const double f = fma(-0.5, nn, 1.5);
+            double* out = Qbuf + static_cast<size_t>(pair) * TB * TB + row0 + lane * TB;
+#pragma unroll
+            for (int v = 0; v < QR / 4; ++v)
+                st4(out + 4 * v, f * qreg[4 * v], f * qreg[4 * v + 1], f * qreg[4 * v + 2], f * qreg[4 * v + 3]);
+        }
+    }
+    if (tid == 0) active[pair] = work ? 1 : 0;
+    if (probe && work) SVDK_PROBE_STORE(g_jprobe, 3, SVDK_CLOCK());
 }
 
 
@@ -1486,6 +1723,19 @@ void build_pair_plan(Ctx* c, JacobiPlan& P) {
     // tables kernel, which completed before any sweep was enqueued.
     const char* pdl_env = std::getenv("SVDK_JACOBI_PDL");
     const bool pdl = !(pdl_env && std::atoi(pdl_env) == 0);
+    // Pair solve: the one-sided kernel with SVDK_JACOBI_OS warps (2 / 4 / 8; 0 =
+    // the two-sided solve_pair with its M threads and lookahead warp).
+    const char* os_env = std::getenv("SVDK_JACOBI_OS");
+    const int os_warps = os_env ? std::atoi(os_env) : 4;
+    // SVDK_JACOBI_NS=1: Newton-Schulz on the accumulated rotation instead of the column-norm step
+    const char* ns_env = std::getenv("SVDK_JACOBI_NS");
+    const bool os_ns = ns_env && std::atoi(ns_env) != 0;
+    const char* fast_env = std::getenv("SVDK_JACOBI_FASTROT");
+    const bool os_fast = !(fast_env && std::atoi(fast_env) == 0);
+    // timing-only development switches (results are wrong): bit 0 drops the A
+    // update from the chain, bit 1 the V update
+    const char* dbg_env = std::getenv("SVDK_JACOBI_DBG");
+    const int dbg = dbg_env ? std::atoi(dbg_env) : 0;
     P.tabs = DBuf(c, 3 * sizeof(SolveTables<TB>) / sizeof(double));
     jacobi_tables_kernel<TB><<<3, 256, 0, S>>>(reinterpret_cast<SolveTables<TB>*>(P.tabs.p()));
     SVDK_CHECK_LAUNCH();
@@ -1515,8 +1765,10 @@ void build_pair_plan(Ctx* c, JacobiPlan& P) {
         };
         auto launch_updates = [&](const double* qr, const int* ar, int r) {
             if (reg_upd) {
-                jacobi_update_v_reg<<<v_warp_ctas, UPD_WARPS * 32, 0, S2>>>(V, n_pad, n_pad, qr, ar, nb, r);
+                if (!(dbg & 2))
+                    jacobi_update_v_reg<<<v_warp_ctas, UPD_WARPS * 32, 0, S2>>>(V, n_pad, n_pad, qr, ar, nb, r);
                 int64_t ld = n_pad;
+                if (dbg & 1) return;
                 if (a_q4)
                     launch(jacobi_update_a_q4, a_ctas, 128, 0, true, A, ld, qr, ar, nb, r);
                 else if (a_vec == 1)
@@ -1535,6 +1787,23 @@ void build_pair_plan(Ctx* c, JacobiPlan& P) {
         auto launch_solve = [&](double* qr, int* ar, int r, int mode) {
             const double* a = A;
             int64_t ld = n_pad;
+            if constexpr (TB == 32) {
+                auto go = [&](auto kern, int threads) {
+                    launch(kern, k, threads, 0, true, a, ld, tabs, qr, ar, nb, r, skip_p, max_inner, mode);
+                };
+                if (os_warps == 8) {
+                    go(os_ns ? (os_fast ? jacobi_pair_solve_os<8, true, true> : jacobi_pair_solve_os<8, true, false>)
+                             : (os_fast ? jacobi_pair_solve_os<8, false, true> : jacobi_pair_solve_os<8, false, false>),
+                       256);
+                    return;
+                }
+                if (os_warps == 4) {
+                    go(os_ns ? (os_fast ? jacobi_pair_solve_os<4, true, true> : jacobi_pair_solve_os<4, true, false>)
+                             : (os_fast ? jacobi_pair_solve_os<4, false, true> : jacobi_pair_solve_os<4, false, false>),
+                       128);
+                    return;
+                }
+            }
             launch(jacobi_pair_solve<TB>, k, nthreads_solve, smem_solve, true, a, ld, tabs, qr, ar, nb, r, skip_p,
                    max_inner, mode);
         };
