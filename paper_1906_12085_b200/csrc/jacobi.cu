@@ -626,6 +626,68 @@ __device__ __forceinline__ void rotation_fast(double app, double aqq, double apq
 __device__ __forceinline__ double4 ld_cg4(const double* p);
 __device__ __forceinline__ void st4(double* p, double a, double b, double c, double d);
 
+// `total` inner rounds of the one-sided solve on this lane's column slabs
+// (QR rows of Q and of W = M Q) for one 32-column subproblem shared by QW
+// warps that meet at named barrier `bar` (see jacobi_pair_solve_os).
+// sched[r][lane] = partner lane | role << 7 for the R rounds of the schedule;
+// pd / px = [2][QW][32] partial-sum buffers of this subproblem. Returns
+// whether this lane applied any rotation.
+template <int QR, int QW, bool FAST>
+__device__ __forceinline__ bool os_rounds(double (&qreg)[QR], double (&wreg)[QR],
+                                          const unsigned char (*sched)[32], int R, int total,
+                                          double (*pd)[QW][32], double (*px)[QW][32], int w, int lane,
+                                          int bar, double skip_tau) {
+    int code = sched[0][lane], rr = 0;
+    bool rotated = false;
+    for (int it = 0; it < total; ++it) {
+        const int partner = code & 31, role = code >> 7, buf = it & 1;
+        rr = rr + 1 == R ? 0 : rr + 1;
+        code = sched[rr][lane];  // next round's pairing, off the chain
+        double oq[QR], ow[QR];
+#pragma unroll
+        for (int i = 0; i < QR; ++i) {
+            oq[i] = __shfl_sync(0xffffffffu, qreg[i], partner);
+            ow[i] = __shfl_sync(0xffffffffu, wreg[i], partner);
+        }
+        // partial dots over this warp's rows: own diagonal and (role p) q_p . w_q
+        double d0 = qreg[0] * wreg[0], d1 = qreg[1] * wreg[1];
+        double x0 = qreg[0] * ow[0], x1 = qreg[1] * ow[1];
+#pragma unroll
+        for (int i = 2; i < QR; i += 2) {
+            d0 = fma(qreg[i], wreg[i], d0);
+            d1 = fma(qreg[i + 1], wreg[i + 1], d1);
+            x0 = fma(qreg[i], ow[i], x0);
+            x1 = fma(qreg[i + 1], ow[i + 1], x1);
+        }
+        pd[buf][w][lane] = d0 + d1;
+        px[buf][w][lane] = x0 + x1;
+        named_bar(bar, 32 * QW);
+        const int pl = role ? partner : lane;  // the pair's p column
+        double ds = 0.0, dp = 0.0, xs = 0.0;
+#pragma unroll
+        for (int h = 0; h < QW; h += 2) {  // fixed order: identical bits in every warp
+            ds += pd[buf][h][lane] + pd[buf][h + 1][lane];
+            dp += pd[buf][h][partner] + pd[buf][h + 1][partner];
+            xs += px[buf][h][pl] + px[buf][h + 1][pl];
+        }
+        double c = 1.0, s = 0.0;
+        if (fabs(xs) > skip_tau) {
+            rotated = true;
+            if (FAST)
+                rotation_fast(role ? dp : ds, role ? ds : dp, xs, c, s);
+            else
+                rotation(role ? dp : ds, role ? ds : dp, xs, c, s);
+        }
+        const double b = role ? s : -s;  // column p: c q_p - s q_q; column q: s q_p + c q_q
+#pragma unroll
+        for (int i = 0; i < QR; ++i) {
+            qreg[i] = fma(b, oq[i], c * qreg[i]);
+            wreg[i] = fma(b, ow[i], c * wreg[i]);
+        }
+    }
+    return rotated;
+}
+
 template <int QW, bool NS, bool FAST>
 __global__ void __launch_bounds__(32 * QW)
     jacobi_pair_solve_os(const double* A, int64_t lda, const SolveTables<32>* tabs, double* Qbuf,
@@ -672,87 +734,7 @@ __global__ void __launch_bounds__(32 * QW)
     }
     if (work) {
         const int total = max_inner * R;
-        int code = sched[0][lane], rr = 0;
-        for (int it = 0; it < total; ++it) {
-            const int partner = code & 31, role = code >> 7, buf = it & 1;
-            rr = rr + 1 == R ? 0 : rr + 1;
-            code = sched[rr][lane];  // next round's pairing, off the chain
-#ifdef SVDK_PROBES
-            const bool pr = probe && it == 10;
-            long long ta = 0;
-            if (pr) ta = clock64();
-#endif
-            double oq[QR], ow[QR];
-#pragma unroll
-            for (int i = 0; i < QR; ++i) {
-                oq[i] = __shfl_sync(0xffffffffu, qreg[i], partner);
-                ow[i] = __shfl_sync(0xffffffffu, wreg[i], partner);
-            }
-            // partial dots over this warp's rows: own diagonal and (role p) q_p . w_q
-            double d0 = qreg[0] * wreg[0], d1 = qreg[1] * wreg[1];
-            double x0 = qreg[0] * ow[0], x1 = qreg[1] * ow[1];
-#pragma unroll
-            for (int i = 2; i < QR; i += 2) {
-                d0 = fma(qreg[i], wreg[i], d0);
-                d1 = fma(qreg[i + 1], wreg[i + 1], d1);
-                x0 = fma(qreg[i], ow[i], x0);
-                x1 = fma(qreg[i + 1], ow[i + 1], x1);
-            }
-            pd[buf][w][lane] = d0 + d1;
-            px[buf][w][lane] = x0 + x1;
-#ifdef SVDK_PROBES
-            if (pr) g_jprobe[4] = clock64() - ta;  // shuffles + dots issued
-#endif
-            __syncthreads();
-#ifdef SVDK_PROBES
-            if (pr) g_jprobe[5] = clock64() - ta;  // past the barrier
-#endif
-            const int pl = role ? partner : lane;  // the pair's p column
-            double ds = 0.0, dp = 0.0, xs = 0.0;
-#pragma unroll
-            for (int h = 0; h < QW; h += 2) {  // fixed order: identical bits in every warp
-                ds += pd[buf][h][lane] + pd[buf][h + 1][lane];
-                dp += pd[buf][h][partner] + pd[buf][h + 1][partner];
-                xs += px[buf][h][pl] + px[buf][h + 1][pl];
-            }
-#ifdef SVDK_PROBES
-            if (pr) {
-                double u;
-                asm volatile("add.f64 %0, %1, %2;" : "=d"(u) : "d"(ds + dp), "d"(xs));
-                g_jprobe[6] = clock64() - ta;  // partial sums landed
-                g_jprobe[13] = static_cast<long long>(u);
-            }
-#endif
-            double c = 1.0, s = 0.0;
-            if (fabs(xs) > skip_tau) {
-                if (FAST)
-                    rotation_fast(role ? dp : ds, role ? ds : dp, xs, c, s);
-                else
-                    rotation(role ? dp : ds, role ? ds : dp, xs, c, s);
-            }
-#ifdef SVDK_PROBES
-            if (pr) {
-                double u;
-                asm volatile("add.f64 %0, %1, %2;" : "=d"(u) : "d"(c), "d"(s));
-                g_jprobe[7] = clock64() - ta;  // rotation done
-                g_jprobe[14] = static_cast<long long>(u);
-            }
-#endif
-            const double b = role ? s : -s;  // column p: c q_p - s q_q; column q: s q_p + c q_q
-#pragma unroll
-            for (int i = 0; i < QR; ++i) {
-                qreg[i] = fma(b, oq[i], c * qreg[i]);
-                wreg[i] = fma(b, ow[i], c * wreg[i]);
-            }
-#ifdef SVDK_PROBES
-            if (pr) {
-                double u;
-                asm volatile("add.f64 %0, %1, %2;" : "=d"(u) : "d"(qreg[0]), "d"(wreg[QR - 1]));
-                g_jprobe[8] = clock64() - ta;  // applied
-                g_jprobe[15] = static_cast<long long>(u);
-            }
-#endif
-        }
+        os_rounds<QR, QW, FAST>(qreg, wreg, sched, R, total, pd, px, w, lane, 0, skip_tau);
         if (probe) SVDK_PROBE_STORE(g_jprobe, 2, SVDK_CLOCK());
         if (NS) {
 #pragma unroll
@@ -2103,6 +2085,118 @@ __global__ void __launch_bounds__(Q_THREADS, 1)
     if (probe) SVDK_PROBE_STORE(g_jprobe, 7, SVDK_CLOCK());
 }
 
+// One-sided quad solve (default): the one-sided rounds of jacobi_pair_solve_os
+// on the 64 x 64 subproblem. Q (64 x 64, starts at I) and W = M Q (starts at the
+// subproblem) only ever see column operations, so the sub-stages compose by
+// themselves: a sub-stage is 16 (31 for the in-super-block stage) more rounds
+// with another pairing of the 64 columns, and the two-sided 64 x 64 transforms
+// between sub-stages of jacobi_quad_solve (and its per-sub-stage Newton-Schulz
+// products) disappear. 8 warps: half h = the sub-stage's h-th 32-column
+// subproblem, run by 4 warps (16 of the 64 rows each, lane = column) that meet
+// at their own named barrier; between sub-stages the columns change hands
+// through shared memory. active[pair] = 0 when the subproblem was diagonal to
+// skip_tau on entry or no rotation was applied.
+constexpr int QOS_THREADS = 256;
+constexpr size_t QOS_SMEM = 2 * 64 * L64 * sizeof(double);
+
+template <bool FAST>
+__global__ void __launch_bounds__(QOS_THREADS, 1)
+    jacobi_quad_solve_os(const double* A, int64_t lda, const SolveTables<32>* tabs, double* Qbuf,
+                         int* active, int ns, int round, const double* skip_tau_p, int stage0) {
+    constexpr int QR = 16;
+    extern __shared__ double sm[];
+    double* Qs = sm;
+    double* Ws = sm + 64 * L64;
+    __shared__ __align__(16) unsigned char sched[2][31][32];  // mode 0, mode 2
+    __shared__ double pd[2][2][4][32], px[2][2][4][32];       // [half][buffer][warp][lane]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, h = warp >> 2, w4 = warp & 3;
+    const int row0 = QR * w4;
+    int a, b;
+    circle_pair(ns, round, blockIdx.x, a, b);
+    auto g = [&](int i) -> int64_t {
+        return i < 32 ? static_cast<int64_t>(a) * 32 + i : static_cast<int64_t>(b) * 32 + (i - 32);
+    };
+    const bool probe = blockIdx.x == 0 && tid == 0 && round == 5;
+    const long long t0 = SVDK_CLOCK();
+    {
+        constexpr int N16 = 31 * 32 / 16;
+        const uint4* s0 = reinterpret_cast<const uint4*>(&tabs[0].part[0][0]);
+        const uint4* s2 = reinterpret_cast<const uint4*>(&tabs[2].part[0][0]);
+        uint4* dst = reinterpret_cast<uint4*>(&sched[0][0][0]);
+        for (int e = tid; e < 2 * N16; e += QOS_THREADS) dst[e] = e < N16 ? s0[e] : s2[e - N16];
+    }
+    pdl_wait();  // A of the previous round's a64 update
+    const double skip_tau = *skip_tau_p;
+    const int nsub = stage0 ? 3 : 2;
+    int col = quad_idx(stage0 ? 0 : 1, h, lane);  // this lane's column (local 64-index)
+    double wreg[QR], qreg[QR];
+    bool big = false;
+    {
+        const double* src = A + g(row0) + g(col) * lda;  // 16 rows inside one super-block
+#pragma unroll
+        for (int v = 0; v < QR / 4; ++v) {
+            const double4 x = ld_cg4(src + 4 * v);
+            wreg[4 * v] = x.x; wreg[4 * v + 1] = x.y; wreg[4 * v + 2] = x.z; wreg[4 * v + 3] = x.w;
+        }
+#pragma unroll
+        for (int i = 0; i < QR; ++i) {
+            big |= (row0 + i != col) && fabs(wreg[i]) > skip_tau;
+            qreg[i] = (row0 + i == col) ? 1.0 : 0.0;
+        }
+    }
+    if (!__syncthreads_or(big)) {  // already diagonal to skip_tau
+        if (tid == 0) active[blockIdx.x] = 0;
+        return;
+    }
+    if (probe) {
+        SVDK_PROBE_STORE(g_jprobe, 0, t0);
+        SVDK_PROBE_STORE(g_jprobe, 1, SVDK_CLOCK());
+    }
+    bool rotated = false;
+    for (int s = 0; s < nsub; ++s) {
+        const int kind = stage0 ? s : s + 1;
+        if (s > 0) {
+            col = quad_idx(kind, h, lane);
+#pragma unroll
+            for (int i = 0; i < QR; ++i) {
+                qreg[i] = Qs[(row0 + i) + col * L64];
+                wreg[i] = Ws[(row0 + i) + col * L64];
+            }
+        }
+        const int R = kind == 0 ? 31 : 16;
+        rotated |= os_rounds<QR, 4, FAST>(qreg, wreg, sched[kind == 0 ? 0 : 1], R, R, pd[h], px[h], w4, lane,
+                                          1 + h, skip_tau);
+        if (s + 1 < nsub) {  // the columns change hands
+#pragma unroll
+            for (int i = 0; i < QR; ++i) {
+                Qs[(row0 + i) + col * L64] = qreg[i];
+                Ws[(row0 + i) + col * L64] = wreg[i];
+            }
+            __syncthreads();
+        }
+        if (probe) SVDK_PROBE_STORE(g_jprobe, 2 + s, SVDK_CLOCK());
+    }
+    // column-norm Newton step (see jacobi_pair_solve_os); the last sub-stage ran 16 rounds
+    double n0 = qreg[0] * qreg[0], n1 = qreg[1] * qreg[1];
+#pragma unroll
+    for (int i = 2; i < QR; i += 2) {
+        n0 = fma(qreg[i], qreg[i], n0);
+        n1 = fma(qreg[i + 1], qreg[i + 1], n1);
+    }
+    pd[h][0][w4][lane] = n0 + n1;
+    const bool any = __syncthreads_or(rotated) != 0;
+    if (any) {
+        const double nn = (pd[h][0][0][lane] + pd[h][0][1][lane]) + (pd[h][0][2][lane] + pd[h][0][3][lane]);
+        const double f = fma(-0.5, nn, 1.5);
+        double* out = Qbuf + static_cast<size_t>(blockIdx.x) * 4096 + row0 + col * 64;
+#pragma unroll
+        for (int v = 0; v < QR / 4; ++v)
+            st4(out + 4 * v, f * qreg[4 * v], f * qreg[4 * v + 1], f * qreg[4 * v + 2], f * qreg[4 * v + 3]);
+    }
+    if (tid == 0) active[blockIdx.x] = any ? 1 : 0;
+    if (probe) SVDK_PROBE_STORE(g_jprobe, 7, SVDK_CLOCK());
+}
+
 // A[ST_p, ST_q] <- Q_p^T A[ST_p, ST_q] Q_q for one super-pair block (p <= q)
 // per CTA of 4 warps; X and Q_q are staged in shared memory, warp w computes
 // rows [16 w, 16 w + 16) of U = Q_p^T X (its Q_p fragments in registers) and
@@ -2295,7 +2389,14 @@ void build_quad_plan(Ctx* c, JacobiPlan& P) {
     const int64_t n_pad = P.n_pad;
     const int ns = static_cast<int>(n_pad / 32), ks = ns / 2, rounds = ns - 1;
     ensure_smem_attr(reinterpret_cast<const void*>(jacobi_quad_solve), QUAD_SMEM);
+    ensure_smem_attr(reinterpret_cast<const void*>(jacobi_quad_solve_os<true>), QOS_SMEM);
+    ensure_smem_attr(reinterpret_cast<const void*>(jacobi_quad_solve_os<false>), QOS_SMEM);
     ensure_smem_attr(reinterpret_cast<const void*>(jacobi_update_a64), A64_SMEM);
+    // SVDK_JACOBI_OS=0: the two-sided quad solve; SVDK_JACOBI_FASTROT=0: rsqrt()-based rotation
+    const char* os_env = std::getenv("SVDK_JACOBI_OS");
+    const bool qos = !(os_env && std::atoi(os_env) == 0);
+    const char* fast_env = std::getenv("SVDK_JACOBI_FASTROT");
+    const bool os_fast = !(fast_env && std::atoi(fast_env) == 0);
     P.qbuf = DBuf(c, static_cast<size_t>(rounds) * ks * 4096);
     P.act = DBuf(c, static_cast<size_t>(rounds) * ks);
     int* active = reinterpret_cast<int*>(P.act.p());
@@ -2341,8 +2442,12 @@ void build_quad_plan(Ctx* c, JacobiPlan& P) {
         for (int r = 0; r < rounds; ++r) {
             double* qr = qbase + static_cast<size_t>(r) * ks * 4096;
             int* ar = active + static_cast<size_t>(r) * ks;
-            launch(jacobi_quad_solve, ks, Q_THREADS, QUAD_SMEM, a_in, ld, tabs, qr, ar, ns, r, skip_p,
-                   r == 0 ? 1 : 0);
+            if (qos)
+                launch(os_fast ? jacobi_quad_solve_os<true> : jacobi_quad_solve_os<false>, ks, QOS_THREADS, QOS_SMEM,
+                       a_in, ld, tabs, qr, ar, ns, r, skip_p, r == 0 ? 1 : 0);
+            else
+                launch(jacobi_quad_solve, ks, Q_THREADS, QUAD_SMEM, a_in, ld, tabs, qr, ar, ns, r, skip_p,
+                       r == 0 ? 1 : 0);
             SVDK_CUDA(cudaEventRecord(ev0, S));
             SVDK_CUDA(cudaStreamWaitEvent(S2, ev0, 0));
             jacobi_update_v64<<<v_ctas, 128, 0, S2>>>(V, n_pad, n_pad, qr, ar, ns, r);
