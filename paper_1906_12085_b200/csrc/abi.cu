@@ -251,6 +251,9 @@ int svdk_ctx_destroy(svdk_ctx* ctx) {
         if (ctx->copy_ev) cudaEventDestroy(ctx->copy_ev);
         for (cudaEvent_t e : ctx->aux_ev)
             if (e) cudaEventDestroy(e);
+        if (ctx->aux_stream2) cudaStreamDestroy(ctx->aux_stream2);
+        for (cudaEvent_t e : ctx->aux_ev2)
+            if (e) cudaEventDestroy(e);
         delete ctx;
     });
 }

@@ -782,6 +782,7 @@ __global__ void __launch_bounds__(32 * QW)
 }
 
 
+
 // ---------------------------------------------------------------------------
 // 2. the round's similarity on A, and its accumulation into V
 // ---------------------------------------------------------------------------
@@ -1017,8 +1018,11 @@ __device__ __forceinline__ void st2(double* p, double a, double b) {
 // [32 part / MS, 32 (part + 1) / MS) of X' (its rows of U stay in its own
 // accumulators) and reads all of X and Q_q; the warps of a CTA meet at a
 // barrier between the last read of X and the first store.
-template <int MS>
-__device__ __forceinline__ void upd_a_unit_vec(double* A, int64_t lda, const double* Qbuf,
+// !INPLACE (solve-ahead ping-pong, Aout != A): every block is written, also
+// where both rotations are the identity, and the warps of a unit need no
+// barrier between their reads and stores.
+template <int MS, bool INPLACE = true>
+__device__ __forceinline__ void upd_a_unit_vec(const double* A, double* Aout, int64_t lda, const double* Qbuf,
                                                const int* active, int nb, int round, int u, int part) {
     constexpr int B = 16, MW = 4 / MS;  // m-tiles (8 rows each) per warp
     const int lane = threadIdx.x & 31, r = lane >> 2, kq = lane & 3;
@@ -1034,7 +1038,7 @@ __device__ __forceinline__ void upd_a_unit_vec(double* A, int64_t lda, const dou
         p = u - q * (q + 1) / 2;
     }
     const bool ap = live && __ldcg(&active[p]) != 0, aq = live && __ldcg(&active[q]) != 0;
-    live = live && (ap | aq);  // both rotations the identity: nothing to do
+    live = live && ((ap | aq) || !INPLACE);  // in place, both rotations the identity: nothing to do
     int Ip, Jp, Iq, Jq;
     circle_pair(nb, round, p, Ip, Jp);
     circle_pair(nb, round, q, Iq, Jq);
@@ -1104,7 +1108,7 @@ __device__ __forceinline__ void upd_a_unit_vec(double* A, int64_t lda, const dou
                     dmma(out[m][t][0], out[m][t][1], acc[m][a2][i2], i2 ? qb[a2][t].y : qb[a2][t].x);
         }
     }
-    if (MS > 1) __syncthreads();  // every warp of the CTA has read its X
+    if (MS > 1 && INPLACE) __syncthreads();  // every warp of the CTA has read its X
     if (!live) return;
     if (p == q) {  // diagonal pair block: upper triangle and its mirror, scalar
 #pragma unroll
@@ -1118,8 +1122,8 @@ __device__ __forceinline__ void upd_a_unit_vec(double* A, int64_t lda, const dou
                     const int lj = 8 * t + 2 * kq + i;
                     if (li > lj) continue;
                     const int64_t gj = gidx(B, Iq, Jq, lj);
-                    A[gi + gj * lda] = out[m][t][i];
-                    A[gj + gi * lda] = out[m][t][i];
+                    Aout[gi + gj * lda] = out[m][t][i];
+                    Aout[gj + gi * lda] = out[m][t][i];
                 }
         }
         return;
@@ -1130,19 +1134,19 @@ __device__ __forceinline__ void upd_a_unit_vec(double* A, int64_t lda, const dou
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
             const int64_t gj = gidx(B, Iq, Jq, 8 * t + 2 * kq);  // and gj + 1 (same 16-index block)
-            A[gi + gj * lda] = out[m][t][0];
-            A[gi + (gj + 1) * lda] = out[m][t][1];
-            st2(A + gj + gi * lda, out[m][t][0], out[m][t][1]);
+            Aout[gi + gj * lda] = out[m][t][0];
+            Aout[gi + (gj + 1) * lda] = out[m][t][1];
+            st2(Aout + gj + gi * lda, out[m][t][0], out[m][t][1]);
         }
     }
 }
 
 template <int MS>
 __global__ void __launch_bounds__(UPD_WARPS * 32)
-    jacobi_update_a_vec(double* A, int64_t lda, const double* Qbuf, const int* active, int nb,
-                        int round) {
+    jacobi_update_a_vec(const double* A, double* Aout, int64_t lda, const double* Qbuf, const int* active,
+                        int nb, int round) {
     const int w = threadIdx.x >> 5;
-    upd_a_unit_vec<MS>(A, lda, Qbuf, active, nb, round, blockIdx.x * (UPD_WARPS / MS) + w / MS, w % MS);
+    upd_a_unit_vec<MS>(A, Aout, lda, Qbuf, active, nb, round, blockIdx.x * (UPD_WARPS / MS) + w / MS, w % MS);
 }
 
 // The same update split over the four warps of a CTA (one unit per CTA):
@@ -1228,14 +1232,14 @@ constexpr int VT_ROWS = 128;
 
 __device__ __forceinline__ void upd_v_unit(double* V, int64_t ldv, int64_t n_rows,
                                            const double* Qbuf, const int* active, int nb, int round,
-                                           int64_t u) {
+                                           int64_t u, int vt_rows = VT_ROWS) {
     constexpr int B = 16;
     const int lane = threadIdx.x & 31, r = lane >> 2, kq = lane & 3;
     const int k = nb / 2;
     const int q = static_cast<int>(u % k);
-    const int64_t row_begin = (u / k) * VT_ROWS;
+    const int64_t row_begin = (u / k) * vt_rows;
     if (row_begin >= n_rows || !__ldcg(&active[q])) return;
-    const int64_t row_end = min(n_rows, row_begin + VT_ROWS);
+    const int64_t row_end = min(n_rows, row_begin + vt_rows);
     int Iq, Jq;
     circle_pair(nb, round, q, Iq, Jq);
     const double* Qb = Qbuf + static_cast<size_t>(q) * 1024;
@@ -1292,6 +1296,220 @@ __global__ void __launch_bounds__(UPD_WARPS * 32)
                         const int* active, int nb, int round) {
     upd_v_unit(V, ldv, n_rows, Qbuf, active, nb, round,
                static_cast<int64_t>(blockIdx.x) * UPD_WARPS + (threadIdx.x >> 5));
+}
+
+// ---------------------------------------------------------------------------
+// 2b. fused round kernel (solve-ahead), n_pad <= kAheadMaxN
+// ---------------------------------------------------------------------------
+// For small and medium n a round is a latency chain, solve -> A update ->
+// solve. Here the pair solve of round j does not wait for round j-1's A
+// update: it reads A_{j-2} (the matrix BEFORE round j-1's similarity, the
+// other half of a ping-pong pair) and round j-1's rotations and forms its own
+// 32 x 32 subproblem
+//     M = T^T X T,   X = A_{j-2}[P, P] (64 x 64),   T = diag(T_I, T_J) (64 x 32),
+// where block I sat in round j-1's pair p_I (T_I = the 16 columns of Q_{p_I}
+// that belong to I), block J in p_J, and P = the four blocks of p_I and p_J.
+// One kernel per round then holds three roles, all depending only on the
+// previous kernel (one programmatic dependent launch chain on one stream):
+//   CTAs [0, n_solve)            solve_j          (A_{j-2}, Q_{j-1} -> Q_j)
+//   CTAs [.., + n_upd_a)         A update j-1     (A_{j-2}, Q_{j-1} -> A_{j-1}, other buffer)
+//   CTAs [.., + n_upd_v)         V update j-1     (V <- V Q_{j-1})
+// Every CTA asks for more than half an SM's shared memory, so each runs alone
+// on its SM: the latency-bound solve CTAs do not share issue slots with the
+// DMMA-bound update CTAs (sharing cost the solve ~5 us per round when the
+// updates ran beside it as separate kernels), and for n <= 1024 the whole
+// round fits in one wave of 148 CTAs. The round's duration is the solve's.
+constexpr int AH_LX = 68, AH_LT = 36;
+constexpr int FR_THREADS = 256;
+constexpr size_t FR_SMEM_USED = (64 * AH_LX + 32 * AH_LT + 32 * AH_LX + 32 * AH_LT) * sizeof(double);
+constexpr size_t FR_SMEM = 116 * 1024;  // > 227 KB / 2: one CTA per SM
+static_assert(FR_SMEM >= FR_SMEM_USED, "fused-round shared memory");
+
+template <bool FAST>
+__device__ __forceinline__ void fused_solve_role(const double* A, int64_t lda, const SolveTables<32>* tabs,
+                                                 double* Qbuf, int* active, int nb, int round,
+                                                 const double* skip_tau_p, int mode, const double* Qprev,
+                                                 const int* act_prev, int rprev, int pair) {
+    constexpr int TB = 32, B = 16, QW = 4, QR = 8;
+    extern __shared__ double dsm[];
+    double* X = dsm;                 // 64 x 64, ld AH_LX
+    double* Tc = X + 64 * AH_LX;     // 32 x 32, ld AH_LT: columns 0-15 = T_I, 16-31 = T_J
+    double* Y = Tc + 32 * AH_LT;     // 64 x 32, ld AH_LX
+    double* Ms = Y + 32 * AH_LX;     // 32 x 32, ld AH_LT
+    __shared__ __align__(16) unsigned char sched[TB - 1][TB];
+    __shared__ double pd[2][QW][TB], px[2][QW][TB];
+    __shared__ int prev[4];  // p_I, offset of I in it, p_J, offset of J
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int r = lane >> 2, kq = lane & 3;
+    const int R = mode == 0 ? TB - 1 : (mode == 1 ? B - 1 : B);
+    const bool probe = pair == 0 && round == 5 && tid == 0;
+    const long long t0 = SVDK_CLOCK();
+    int I, J;
+    circle_pair(nb, round, pair, I, J);
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(&tabs[mode].part[0][0]);
+        uint4* dst = reinterpret_cast<uint4*>(&sched[0][0]);
+        for (int e = tid; e < static_cast<int>(sizeof(sched) / 16); e += FR_THREADS) dst[e] = src[e];
+        if (rprev >= 0) {  // where I and J sat in the previous round (independent of its results)
+            for (int i = tid; i < nb / 2; i += FR_THREADS) {
+                int a, b;
+                circle_pair(nb, rprev, i, a, b);
+                if (a == I) { prev[0] = i; prev[1] = 0; }
+                if (b == I) { prev[0] = i; prev[1] = B; }
+                if (a == J) { prev[2] = i; prev[3] = 0; }
+                if (b == J) { prev[2] = i; prev[3] = B; }
+            }
+        }
+    }
+    __syncthreads();
+    pdl_wait();  // the previous kernel: Q_{j-1}, its active flags and A_{j-2}
+    const long long t1 = SVDK_CLOCK();
+    const double skip_tau = *skip_tau_p;
+    const int row0 = (w & 3) * QR;
+    double wreg[QR], qreg[QR];
+    if (rprev < 0) {
+        if (w < QW) {
+            const double* col = A + gidx(B, I, J, row0) + gidx(B, I, J, lane) * lda;
+#pragma unroll
+            for (int v = 0; v < QR / 4; ++v) {
+                const double4 x = ld_cg4(col + 4 * v);
+                wreg[4 * v] = x.x; wreg[4 * v + 1] = x.y; wreg[4 * v + 2] = x.z; wreg[4 * v + 3] = x.w;
+            }
+        }
+    } else {
+        const int pI = prev[0], oI = prev[1], pJ = prev[2], oJ = prev[3];
+        int bl[4];
+        circle_pair(nb, rprev, pI, bl[0], bl[1]);
+        circle_pair(nb, rprev, pJ, bl[2], bl[3]);
+        // X = A_{j-2}[P, P]: 1024 four-row vectors, 4 per thread, all in flight; T: 256, 1 per thread
+        double4 xv[4], tv;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int e = tid + FR_THREADS * k, c = e >> 4, r4 = (e & 15) * 4;
+            xv[k] = ld_cg4(A + static_cast<int64_t>(bl[r4 >> 4]) * B + (r4 & 15) +
+                           (static_cast<int64_t>(bl[c >> 4]) * B + (c & 15)) * lda);
+        }
+        {
+            const int c = tid >> 3, r4 = (tid & 7) * 4;
+            const int pp = c < B ? pI : pJ, cc = c < B ? oI + c : oJ + (c - B);
+            tv = __ldcg(&act_prev[pp]) ? ld_cg4(Qprev + static_cast<size_t>(pp) * 1024 + r4 + cc * 32)
+                                       : make_double4(r4 == cc, r4 + 1 == cc, r4 + 2 == cc, r4 + 3 == cc);
+            double* d = Tc + r4 + c * AH_LT;
+            d[0] = tv.x; d[1] = tv.y; d[2] = tv.z; d[3] = tv.w;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int e = tid + FR_THREADS * k, c = e >> 4, r4 = (e & 15) * 4;
+            double* d = X + r4 + c * AH_LX;
+            d[0] = xv[k].x; d[1] = xv[k].y; d[2] = xv[k].z; d[3] = xv[k].w;
+        }
+        __syncthreads();
+        {  // Y = X T: warp w forms rows [8w, 8w + 8); n-tiles 0, 1 contract over P's first pair, 2, 3 over its second
+            double acc[4][2];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) acc[t][0] = acc[t][1] = 0.0;
+#pragma unroll
+            for (int s8 = 0; s8 < 8; ++s8) {
+                const int k = 4 * s8 + kq;
+                const double a0 = X[(8 * w + r) + k * AH_LX], a1 = X[(8 * w + r) + (32 + k) * AH_LX];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) dmma(acc[t][0], acc[t][1], t < 2 ? a0 : a1, Tc[k + (8 * t + r) * AH_LT]);
+            }
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+#pragma unroll
+                for (int i = 0; i < 2; ++i) Y[(8 * w + r) + (8 * t + 2 * kq + i) * AH_LX] = acc[t][i];
+        }
+        __syncthreads();
+        {  // M = T^T Y: warp w forms rows [8 (w & 3), + 8) x columns [16 (w >> 2), + 16)
+            const int mw = w & 3, nh = w >> 2;
+            double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+            const int yoff = mw < 2 ? 0 : 32;  // rows < 16: T_I^T Y[0:32], else T_J^T Y[32:64]
+#pragma unroll
+            for (int s8 = 0; s8 < 8; ++s8) {
+                const int k = 4 * s8 + kq;
+                const double af = Tc[k + (8 * mw + r) * AH_LT];
+#pragma unroll
+                for (int t = 0; t < 2; ++t)
+                    dmma(acc[t][0], acc[t][1], af, Y[(yoff + k) + (8 * (2 * nh + t) + r) * AH_LX]);
+            }
+#pragma unroll
+            for (int t = 0; t < 2; ++t)
+#pragma unroll
+                for (int i = 0; i < 2; ++i) Ms[(8 * mw + r) + (8 * (2 * nh + t) + 2 * kq + i) * AH_LT] = acc[t][i];
+        }
+        __syncthreads();
+        if (w < QW) {
+#pragma unroll
+            for (int i = 0; i < QR; ++i) wreg[i] = Ms[(row0 + i) + lane * AH_LT];
+        }
+    }
+    bool big = false;
+    if (w < QW) {
+#pragma unroll
+        for (int i = 0; i < QR; ++i) {
+            big |= (row0 + i != lane) && fabs(wreg[i]) > skip_tau;
+            qreg[i] = (row0 + i == lane) ? 1.0 : 0.0;
+        }
+    }
+    const bool work = __syncthreads_or(big) != 0;
+    if (tid == 0) active[pair] = work ? 1 : 0;
+    if (w >= QW || !work) return;  // warps 4-7 only helped with the subproblem
+    if (probe) {
+        SVDK_PROBE_STORE(g_jprobe, 0, t0);
+        SVDK_PROBE_STORE(g_jprobe, 1, t1);
+        SVDK_PROBE_STORE(g_jprobe, 2, SVDK_CLOCK());
+    }
+    os_rounds<QR, QW, FAST>(qreg, wreg, sched, R, R, pd, px, w, lane, 1, skip_tau);
+    if (probe) SVDK_PROBE_STORE(g_jprobe, 3, SVDK_CLOCK());
+    // column-norm Newton step (see jacobi_pair_solve_os)
+    double n0 = qreg[0] * qreg[0], n1 = qreg[1] * qreg[1];
+#pragma unroll
+    for (int i = 2; i < QR; i += 2) {
+        n0 = fma(qreg[i], qreg[i], n0);
+        n1 = fma(qreg[i + 1], qreg[i + 1], n1);
+    }
+    const int buf = R & 1;
+    pd[buf][w][lane] = n0 + n1;
+    named_bar(1, 32 * QW);
+    const double nn = (pd[buf][0][lane] + pd[buf][1][lane]) + (pd[buf][2][lane] + pd[buf][3][lane]);
+    const double f = fma(-0.5, nn, 1.5);
+    double* out = Qbuf + static_cast<size_t>(pair) * TB * TB + row0 + lane * TB;
+#pragma unroll
+    for (int v = 0; v < QR / 4; ++v)
+        st4(out + 4 * v, f * qreg[4 * v], f * qreg[4 * v + 1], f * qreg[4 * v + 2], f * qreg[4 * v + 3]);
+    if (probe) SVDK_PROBE_STORE(g_jprobe, 4, SVDK_CLOCK());
+}
+
+template <bool FAST>
+__global__ void __launch_bounds__(FR_THREADS, 1)
+    jacobi_round_fused(const double* Ain, double* Aout, double* V, int64_t ld, const SolveTables<32>* tabs,
+                       double* Qcur, int* act_cur, const double* Qprev, const int* act_prev, int nb, int round,
+                       int rprev, int mode, const double* skip_tau_p, int n_solve, int a_tasks, int v_tasks) {
+    const int b = blockIdx.x, w = threadIdx.x >> 5;
+    if (b < n_solve) {
+        fused_solve_role<FAST>(Ain, ld, tabs, Qcur, act_cur, nb, round, skip_tau_p, mode, Qprev, act_prev, rprev, b);
+        return;
+    }
+    // worker CTAs: warp tasks of round j-1's updates, grid-strided. A task: one
+    // half (16 rows) of a 32 x 32 unit of A_{j-1} = Q^T A_{j-2} Q; V task: one
+    // (pair, 32-row chunk) of V <- V Q.
+    const bool probe = b == n_solve && threadIdx.x == 0 && round == 5;
+    const long long t0 = SVDK_CLOCK();
+    pdl_wait();
+    if (probe) {
+        SVDK_PROBE_STORE(g_jprobe, 8, t0);
+        SVDK_PROBE_STORE(g_jprobe, 9, SVDK_CLOCK());
+    }
+    const int nw = (gridDim.x - n_solve) * (FR_THREADS / 32);
+    for (int t = (b - n_solve) * (FR_THREADS / 32) + w; t < a_tasks + v_tasks; t += nw) {
+        if (t < a_tasks)
+            upd_a_unit_vec<2, false>(Ain, Aout, ld, Qprev, act_prev, nb, rprev, t >> 1, t & 1);
+        else
+            upd_v_unit(V, ld, ld, Qprev, act_prev, nb, rprev, t - a_tasks, 32);
+        if (probe && t < nw) SVDK_PROBE_STORE(g_jprobe, 10, SVDK_CLOCK());
+    }
+    if (probe) SVDK_PROBE_STORE(g_jprobe, 11, SVDK_CLOCK());
 }
 
 // ---------------------------------------------------------------------------
@@ -1498,6 +1716,7 @@ struct JacobiPlan {
     int64_t n_pad = 0;
     int tb = 0;  // 16 / 32: pair scheme, 64: quad scheme
     DBuf A, V, qbuf, act, tabs, part_all, part_low, scal;
+    DBuf A2;  // solve-ahead: the other half of the A ping-pong pair
     int blocks = 0;  // sum-of-squares partial blocks
     int launches_per_sweep = 0;
     std::function<void()> enqueue_sweep;  // one sweep on (stream, aux stream)
@@ -1637,6 +1856,9 @@ int run_plan(Ctx* c, JacobiPlan& P) {
     return static_cast<int>(h[JS_SWEEPS]);
 }
 
+// Largest n_pad that runs the solve-ahead chain by default (see jacobi_pair_solve_ahead).
+constexpr int64_t kAheadMaxN = 1024;
+
 template <int TB>
 void build_pair_plan(Ctx* c, JacobiPlan& P) {
     constexpr int B = TB / 2;
@@ -1750,15 +1972,16 @@ void build_pair_plan(Ctx* c, JacobiPlan& P) {
                 if (!(dbg & 2))
                     jacobi_update_v_reg<<<v_warp_ctas, UPD_WARPS * 32, 0, S2>>>(V, n_pad, n_pad, qr, ar, nb, r);
                 int64_t ld = n_pad;
+                const double* ac = A;
                 if (dbg & 1) return;
                 if (a_q4)
                     launch(jacobi_update_a_q4, a_ctas, 128, 0, true, A, ld, qr, ar, nb, r);
                 else if (a_vec == 1)
-                    launch(jacobi_update_a_vec<1>, a_warp_ctas, UPD_WARPS * 32, 0, true, A, ld, qr, ar, nb, r);
+                    launch(jacobi_update_a_vec<1>, a_warp_ctas, UPD_WARPS * 32, 0, true, ac, A, ld, qr, ar, nb, r);
                 else if (a_vec == 2)
-                    launch(jacobi_update_a_vec<2>, a_ctas2, UPD_WARPS * 32, 0, true, A, ld, qr, ar, nb, r);
+                    launch(jacobi_update_a_vec<2>, a_ctas2, UPD_WARPS * 32, 0, true, ac, A, ld, qr, ar, nb, r);
                 else if (a_vec == 4)
-                    launch(jacobi_update_a_vec<4>, a_ctas, UPD_WARPS * 32, 0, true, A, ld, qr, ar, nb, r);
+                    launch(jacobi_update_a_vec<4>, a_ctas, UPD_WARPS * 32, 0, true, ac, A, ld, qr, ar, nb, r);
                 else
                     launch(jacobi_update_a_reg, a_warp_ctas, UPD_WARPS * 32, 0, true, A, ld, qr, ar, nb, r);
             } else {
@@ -1809,6 +2032,75 @@ void build_pair_plan(Ctx* c, JacobiPlan& P) {
         SVDK_CUDA(cudaEventRecord(ev1, S2));
         SVDK_CUDA(cudaStreamWaitEvent(S, ev1, 0));
     };
+    // Fused round kernels (jacobi_round_fused, solve-ahead): default for
+    // n_pad <= kAheadMaxN, where a round is a latency chain; SVDK_JACOBI_AHEAD=0/1 overrides.
+    bool ahead = TB == 32 && split && nb > 2 && n_pad <= kAheadMaxN;
+    if (const char* e = std::getenv("SVDK_JACOBI_AHEAD")) ahead = TB == 32 && split && nb > 2 && std::atoi(e) != 0;
+    if constexpr (TB == 32) {
+        if (ahead) {
+            ensure_smem_attr(reinterpret_cast<const void*>(jacobi_round_fused<true>), FR_SMEM);
+            ensure_smem_attr(reinterpret_cast<const void*>(jacobi_round_fused<false>), FR_SMEM);
+            P.A2 = DBuf(c, static_cast<size_t>(n_pad) * n_pad);
+            double* A2 = P.A2.p();
+            const int a_tasks = 2 * a_ctas;  // half units
+            const int v_tasks = static_cast<int>(n_pad / 32) * k;
+            // worker CTAs: the SMs the solve CTAs leave free (every CTA runs alone on its SM), at
+            // least `wtasks` warp tasks each (a task is DMMA-bound on its SM quadrant: one per quadrant)
+            const char* wt_env = std::getenv("SVDK_JACOBI_FRTASKS");
+            const int wtasks = wt_env ? std::max(1, std::atoi(wt_env)) : 4;
+            int n_workers = static_cast<int>(std::max<int64_t>(
+                1, std::min<int64_t>(c->num_sms - k, ceil_div(static_cast<int64_t>(a_tasks + v_tasks), wtasks))));
+            if (const char* e = std::getenv("SVDK_JACOBI_FRWORKERS")) n_workers = std::max(1, std::atoi(e));  // tuning
+            P.launches_per_sweep = slots + 1;
+            const char* frs = std::getenv("SVDK_JACOBI_FRSMEM");  // KB, tuning: below 114 the roles share SMs
+            const size_t fr_smem = frs ? std::max<size_t>(FR_SMEM_USED, static_cast<size_t>(std::atoi(frs)) * 1024) : FR_SMEM;
+            P.enqueue_sweep = [=]() {
+                const cudaStream_t S = c->stream;
+                double* bufs[2] = {A, A2};
+                const double* qprev = nullptr;
+                const int* aprev = nullptr;
+                int rprev = -1;
+                int64_t ld = n_pad;
+                // kernel j = {solve j, A and V updates j-1}; slots is even, so A is current at the end
+                for (int j = 0; j <= slots; ++j) {
+                    const bool has_solve = j < slots;
+                    const int r = j == 0 ? 0 : j - 1, mode = j == 0 ? 1 : 2;
+                    const size_t slot = j == 0 ? static_cast<size_t>(rounds) : static_cast<size_t>(r);
+                    double* qr = qbase + slot * k * TB * TB;
+                    int* ar = active + slot * k;
+                    const int ns = (has_solve && !(dbg & 4)) ? k : 0, na = (j && !(dbg & 1)) ? a_tasks : 0,
+                              nv = (j && !(dbg & 2)) ? v_tasks : 0, nwk = (na + nv) ? n_workers : 0;
+                    if (ns + nwk == 0) {
+                        qprev = qr;
+                        aprev = ar;
+                        rprev = r;
+                        continue;
+                    }
+                    const double* a_in = j == 0 ? bufs[0] : bufs[(j - 1) & 1];
+                    double* a_out = bufs[j & 1];
+                    cudaLaunchConfig_t cfg = {};
+                    cfg.gridDim = dim3(static_cast<unsigned>(ns + nwk));
+                    cfg.blockDim = dim3(FR_THREADS);
+                    cfg.dynamicSmemBytes = fr_smem;
+                    cfg.stream = S;
+                    cudaLaunchAttribute at[1];
+                    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+                    at[0].val.programmaticStreamSerializationAllowed = 1;
+                    cfg.attrs = at;
+                    cfg.numAttrs = pdl ? 1 : 0;
+                    if (os_fast)
+                        SVDK_CUDA(cudaLaunchKernelEx(&cfg, jacobi_round_fused<true>, a_in, a_out, V, ld, tabs, qr, ar, qprev,
+                                                     aprev, nb, r, rprev, mode, skip_p, ns, na, nv));
+                    else
+                        SVDK_CUDA(cudaLaunchKernelEx(&cfg, jacobi_round_fused<false>, a_in, a_out, V, ld, tabs, qr, ar,
+                                                     qprev, aprev, nb, r, rprev, mode, skip_p, ns, na, nv));
+                    qprev = qr;
+                    aprev = ar;
+                    rprev = r;
+                }
+            };
+        }
+    }
     if (nb > 2) build_loop_graph(c, P);
 }
 

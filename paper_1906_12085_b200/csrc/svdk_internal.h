@@ -124,6 +124,8 @@ struct Ctx {
     cudaStream_t copy_stream = nullptr;  // host-buffer uploads streamed under compute
     cudaEvent_t copy_ev = nullptr;
     cudaEvent_t aux_ev[2] = {nullptr, nullptr};
+    cudaStream_t aux_stream2 = nullptr;  // Jacobi solve-ahead: the A updates' own stream
+    cudaEvent_t aux_ev2[3] = {nullptr, nullptr, nullptr};
     Pool pool;
     // scratch: small pinned host buffer for scalars / flags
     void* host_scratch = nullptr;
