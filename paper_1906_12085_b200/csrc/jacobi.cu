@@ -226,6 +226,16 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 __device__ __forceinline__ void named_bar(int id, int n) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
+// barrier over n threads that also ORs a predicate across them
+__device__ __forceinline__ bool named_bar_or(int id, int n, bool pred) {
+    unsigned out;
+    asm volatile(
+        "{\n .reg .pred p, q;\n setp.ne.u32 p, %1, 0;\n bar.red.or.pred q, %2, %3, p;\n selp.u32 %0, 1, 0, q;\n}\n"
+        : "=r"(out)
+        : "r"(static_cast<unsigned>(pred)), "r"(id), "r"(n)
+        : "memory");
+    return out != 0;
+}
 
 // The lookahead warp's part of an inner round: look_load fetches what
 // rotation `lane` of round rr+1 needs from M_rr and round rr's rotations;
@@ -1320,7 +1330,8 @@ __global__ void __launch_bounds__(UPD_WARPS * 32)
 // updates ran beside it as separate kernels), and for n <= 1024 the whole
 // round fits in one wave of 148 CTAs. The round's duration is the solve's.
 constexpr int AH_LX = 68, AH_LT = 36;
-constexpr int FR_THREADS = 256;
+constexpr int FR_THREADS = 384;        // worker CTAs: 12 warps (3 per SM quadrant; 16 spill and ran slower)
+constexpr int FR_SOLVE_THREADS = 256;  // solve CTAs: 8 warps form the subproblem, 4 of them run the rounds
 constexpr size_t FR_SMEM_USED = (64 * AH_LX + 32 * AH_LT + 32 * AH_LX + 32 * AH_LT) * sizeof(double);
 constexpr size_t FR_SMEM = 116 * 1024;  // > 227 KB / 2: one CTA per SM
 static_assert(FR_SMEM >= FR_SMEM_USED, "fused-round shared memory");
@@ -1340,6 +1351,7 @@ __device__ __forceinline__ void fused_solve_role(const double* A, int64_t lda, c
     __shared__ double pd[2][QW][TB], px[2][QW][TB];
     __shared__ int prev[4];  // p_I, offset of I in it, p_J, offset of J
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    if (tid >= FR_SOLVE_THREADS) return;  // the role's barriers count FR_SOLVE_THREADS threads
     const int r = lane >> 2, kq = lane & 3;
     const int R = mode == 0 ? TB - 1 : (mode == 1 ? B - 1 : B);
     const bool probe = pair == 0 && round == 5 && tid == 0;
@@ -1349,9 +1361,9 @@ __device__ __forceinline__ void fused_solve_role(const double* A, int64_t lda, c
     {
         const uint4* src = reinterpret_cast<const uint4*>(&tabs[mode].part[0][0]);
         uint4* dst = reinterpret_cast<uint4*>(&sched[0][0]);
-        for (int e = tid; e < static_cast<int>(sizeof(sched) / 16); e += FR_THREADS) dst[e] = src[e];
+        for (int e = tid; e < static_cast<int>(sizeof(sched) / 16); e += FR_SOLVE_THREADS) dst[e] = src[e];
         if (rprev >= 0) {  // where I and J sat in the previous round (independent of its results)
-            for (int i = tid; i < nb / 2; i += FR_THREADS) {
+            for (int i = tid; i < nb / 2; i += FR_SOLVE_THREADS) {
                 int a, b;
                 circle_pair(nb, rprev, i, a, b);
                 if (a == I) { prev[0] = i; prev[1] = 0; }
@@ -1361,7 +1373,7 @@ __device__ __forceinline__ void fused_solve_role(const double* A, int64_t lda, c
             }
         }
     }
-    __syncthreads();
+    named_bar(2, FR_SOLVE_THREADS);
     pdl_wait();  // the previous kernel: Q_{j-1}, its active flags and A_{j-2}
     const long long t1 = SVDK_CLOCK();
     const double skip_tau = *skip_tau_p;
@@ -1385,7 +1397,7 @@ __device__ __forceinline__ void fused_solve_role(const double* A, int64_t lda, c
         double4 xv[4], tv;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            const int e = tid + FR_THREADS * k, c = e >> 4, r4 = (e & 15) * 4;
+            const int e = tid + FR_SOLVE_THREADS * k, c = e >> 4, r4 = (e & 15) * 4;
             xv[k] = ld_cg4(A + static_cast<int64_t>(bl[r4 >> 4]) * B + (r4 & 15) +
                            (static_cast<int64_t>(bl[c >> 4]) * B + (c & 15)) * lda);
         }
@@ -1399,11 +1411,11 @@ __device__ __forceinline__ void fused_solve_role(const double* A, int64_t lda, c
         }
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            const int e = tid + FR_THREADS * k, c = e >> 4, r4 = (e & 15) * 4;
+            const int e = tid + FR_SOLVE_THREADS * k, c = e >> 4, r4 = (e & 15) * 4;
             double* d = X + r4 + c * AH_LX;
             d[0] = xv[k].x; d[1] = xv[k].y; d[2] = xv[k].z; d[3] = xv[k].w;
         }
-        __syncthreads();
+        named_bar(2, FR_SOLVE_THREADS);
         {  // Y = X T: warp w forms rows [8w, 8w + 8); n-tiles 0, 1 contract over P's first pair, 2, 3 over its second
             double acc[4][2];
 #pragma unroll
@@ -1420,7 +1432,7 @@ __device__ __forceinline__ void fused_solve_role(const double* A, int64_t lda, c
 #pragma unroll
                 for (int i = 0; i < 2; ++i) Y[(8 * w + r) + (8 * t + 2 * kq + i) * AH_LX] = acc[t][i];
         }
-        __syncthreads();
+        named_bar(2, FR_SOLVE_THREADS);
         {  // M = T^T Y: warp w forms rows [8 (w & 3), + 8) x columns [16 (w >> 2), + 16)
             const int mw = w & 3, nh = w >> 2;
             double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
@@ -1438,7 +1450,7 @@ __device__ __forceinline__ void fused_solve_role(const double* A, int64_t lda, c
 #pragma unroll
                 for (int i = 0; i < 2; ++i) Ms[(8 * mw + r) + (8 * (2 * nh + t) + 2 * kq + i) * AH_LT] = acc[t][i];
         }
-        __syncthreads();
+        named_bar(2, FR_SOLVE_THREADS);
         if (w < QW) {
 #pragma unroll
             for (int i = 0; i < QR; ++i) wreg[i] = Ms[(row0 + i) + lane * AH_LT];
@@ -1452,7 +1464,7 @@ __device__ __forceinline__ void fused_solve_role(const double* A, int64_t lda, c
             qreg[i] = (row0 + i == lane) ? 1.0 : 0.0;
         }
     }
-    const bool work = __syncthreads_or(big) != 0;
+    const bool work = named_bar_or(2, FR_SOLVE_THREADS, big);
     if (tid == 0) active[pair] = work ? 1 : 0;
     if (w >= QW || !work) return;  // warps 4-7 only helped with the subproblem
     if (probe) {
