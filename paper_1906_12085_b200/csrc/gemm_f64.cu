@@ -31,6 +31,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <vector>
 
 #include "svdk_internal.h"
 #include "tma_util.h"
@@ -71,6 +72,11 @@ struct Params {
     int beta_one;
     int b_upper;   // B is upper triangular: tile (., col0) only needs k < col0 + BN
     int a_tma3;    // M-major A via one 3-D box per stage (M % 16 == 0) instead of 8 2-D boxes
+    // SYRK work line (see build_syrk_line): unit u = (tile, k0, k1) triples, the contiguous unit
+    // range of every CTA and of every tile. Null: the uniform tiles x splits grid.
+    const long long* utab;
+    const long long* cfirst;
+    const long long* tfirst;
 };
 
 // 3-D box: (m_lo 16, k 16, m_hi 8) lands as m_lo*8 + k*128 + m_hi*2048 bytes,
@@ -103,6 +109,20 @@ struct Unit {
 
 __device__ __forceinline__ Unit decode(const Params& p, int u) {
     Unit w;
+    if (p.utab) {  // SYRK work line: explicit (tile, k0, k1)
+        const long long* e = p.utab + 3 * static_cast<size_t>(u);
+        const int t = static_cast<int>(e[0]);
+        int tj = static_cast<int>((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
+        while ((tj + 1) * (tj + 2) / 2 <= t) ++tj;
+        while (tj * (tj + 1) / 2 > t) --tj;
+        const int ti = t - tj * (tj + 1) / 2;
+        w.row0 = static_cast<int64_t>(ti) * BM;
+        w.col0 = static_cast<int64_t>(tj) * BN;
+        w.diag = ti == tj;
+        w.k0 = e[1];
+        w.k1 = e[2];
+        return w;
+    }
     const int split = u / p.n_tiles;
     const int t = u - split * p.n_tiles;
     int ti, tj;
@@ -142,6 +162,17 @@ __device__ __forceinline__ void slot_coord(int a_mmajor, int idx, int tid, int& 
     c = wn * 32 + tn * 8 + perm8(2 * (lane & 3) + i);
 }
 
+// The same for a diagonal SYRK tile of the work line, where consumer warp w
+// holds the 8-row groups w and 15 - w against the column groups on or above
+// the diagonal (17 of the tile's 136 upper 8 x 8 blocks per warp): slot
+// (which, n, i) = acc[4 which + n / 4][n % 4][i].
+__device__ __forceinline__ void slot_coord_diag(int idx, int tid, int& r, int& c) {
+    const int warp = tid >> 5, lane = tid & 31;
+    const int which = idx >> 5, n = (idx >> 1) & 15, i = idx & 1;
+    r = (which ? 15 - warp : warp) * 8 + perm8(lane >> 2);
+    c = n * 8 + perm8(2 * (lane & 3) + i);
+}
+
 __device__ __forceinline__ void store_out(const Params& p, int64_t row, int64_t col, double v) {
     if (row >= p.M || col >= p.N) return;
     if (p.kind == KIND_SYRK) {
@@ -157,6 +188,42 @@ __device__ __forceinline__ void store_out(const Params& p, int64_t row, int64_t 
     if (p.alpha != 1.0) v *= p.alpha;
     if (p.beta_one) v += p.C[row + col * p.ldc];
     p.C[row + col * p.ldc] = v;
+}
+
+// The k loop of a diagonal SYRK tile for consumer warp W (compile-time, so the
+// block selection below costs no branches and the operand loads are hoisted
+// like in the main loop): row groups W and 15 - W against the column groups on
+// or above the diagonal, 16 - W and W + 1 blocks = 17 DMMAs per k4-step for
+// every warp (the four SM sub-partitions stay balanced); both operands come
+// from the A stage. acc[4 which + n / 4][n % 4] = block (row group, n).
+template <int W>
+__device__ __forceinline__ void diag_unit(double (&acc)[8][4][2], const uint8_t* smA, uint64_t* full,
+                                          uint64_t* empty, int& stage, uint32_t& phase, int64_t k0, int64_t k1,
+                                          const uint32_t (&koff)[4], int lane) {
+    constexpr int RB1 = W, RB2 = 15 - W, NMIN = RB1 < RB2 ? RB1 : RB2;
+    for (int64_t k = k0; k < k1; k += BK) {
+        mbar_wait(&full[stage], phase);
+        const uint8_t* st = smA + stage * TILE_BYTES;
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+            const double a1 = *reinterpret_cast<const double*>(st + RB1 * 1024 + koff[s]);
+            const double a2 = *reinterpret_cast<const double*>(st + RB2 * 1024 + koff[s]);
+            double bf[16];
+#pragma unroll
+            for (int n = NMIN; n < 16; ++n) bf[n] = *reinterpret_cast<const double*>(st + n * 1024 + koff[s]);
+#pragma unroll
+            for (int n = NMIN; n < 16; ++n) {
+                if (n >= RB1) dmma(acc[n >> 2][n & 3][0], acc[n >> 2][n & 3][1], a1, bf[n]);
+                if (n >= RB2) dmma(acc[4 + (n >> 2)][n & 3][0], acc[4 + (n >> 2)][n & 3][1], a2, bf[n]);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+        if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+        }
+    }
 }
 
 template <bool AMM>
@@ -204,7 +271,10 @@ __global__ void __launch_bounds__(THREADS, 1)
                          : "memory");
             int stage = 0;
             uint32_t phase = 0;
-            for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+            const int u_begin = p.utab ? static_cast<int>(p.cfirst[blockIdx.x]) : static_cast<int>(blockIdx.x);
+            const int u_end = p.utab ? static_cast<int>(p.cfirst[blockIdx.x + 1]) : p.units;
+            const int u_step = p.utab ? 1 : static_cast<int>(gridDim.x);
+            for (int u = u_begin; u < u_end; u += u_step) {
                 const Unit w = decode(p, u);
                 for (int64_t k = w.k0; k < w.k1; k += BK) {
                     mbar_wait(&empty[stage], phase ^ 1);
@@ -262,13 +332,30 @@ __global__ void __launch_bounds__(THREADS, 1)
     double acc[8][4][2];
     int stage = 0;
     uint32_t phase = 0;
-    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+    const int u_begin = p.utab ? static_cast<int>(p.cfirst[blockIdx.x]) : static_cast<int>(blockIdx.x);
+    const int u_end = p.utab ? static_cast<int>(p.cfirst[blockIdx.x + 1]) : p.units;
+    const int u_step = p.utab ? 1 : static_cast<int>(gridDim.x);
+    for (int u = u_begin; u < u_end; u += u_step) {
         const Unit w = decode(p, u);
 #pragma unroll
         for (int t = 0; t < 8; ++t)
 #pragma unroll
             for (int n = 0; n < 4; ++n) acc[t][n][0] = acc[t][n][1] = 0.0;
 
+        if (!AMM && p.utab && w.diag) {
+            // Diagonal tile of the SYRK work line: only the 136 upper 8 x 8 blocks
+            // (diag_unit, one branch-free instantiation per consumer warp).
+            switch (warp) {
+                case 0: diag_unit<0>(acc, smA, full, empty, stage, phase, w.k0, w.k1, koff, lane); break;
+                case 1: diag_unit<1>(acc, smA, full, empty, stage, phase, w.k0, w.k1, koff, lane); break;
+                case 2: diag_unit<2>(acc, smA, full, empty, stage, phase, w.k0, w.k1, koff, lane); break;
+                case 3: diag_unit<3>(acc, smA, full, empty, stage, phase, w.k0, w.k1, koff, lane); break;
+                case 4: diag_unit<4>(acc, smA, full, empty, stage, phase, w.k0, w.k1, koff, lane); break;
+                case 5: diag_unit<5>(acc, smA, full, empty, stage, phase, w.k0, w.k1, koff, lane); break;
+                case 6: diag_unit<6>(acc, smA, full, empty, stage, phase, w.k0, w.k1, koff, lane); break;
+                default: diag_unit<7>(acc, smA, full, empty, stage, phase, w.k0, w.k1, koff, lane); break;
+            }
+        } else
         for (int64_t k = w.k0; k < w.k1; k += BK) {
             mbar_wait(&full[stage], phase);
             const uint8_t* sa = smA + stage * TILE_BYTES + a_row_base;
@@ -365,6 +452,21 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const Params p) {
     const int t = blockIdx.x;
     const int tid = threadIdx.x;
     Params q = p;
+    if (p.utab) {  // work line: the tile's units are contiguous, summed in unit order
+        const int u0 = static_cast<int>(p.tfirst[t]), u1 = static_cast<int>(p.tfirst[t + 1]);
+        const Unit w = decode(q, u0);
+        for (int idx = blockIdx.y * 8; idx < blockIdx.y * 8 + 8; ++idx) {
+            double s = 0.0;
+            for (int u = u0; u < u1; ++u) s += p.partial[static_cast<size_t>(u) * TILE_ELEMS + idx * 256 + tid];
+            int r, c;
+            if (w.diag)
+                slot_coord_diag(idx, tid, r, c);
+            else
+                slot_coord(p.a_mmajor, idx, tid, r, c);
+            store_out(p, w.row0 + r, w.col0 + c, s);
+        }
+        return;
+    }
     // Recover the tile origin from any unit of this tile (split 0).
     const Unit w = decode(q, t);
     for (int idx = blockIdx.y * 8; idx < blockIdx.y * 8 + 8; ++idx) {
@@ -445,6 +547,60 @@ int choose_splits(int n_tiles, int64_t K, int sms) {
     return best;
 }
 
+// Work line of a tall SYRK (see syrk): [units, (tile, k0, k1) x units, first unit
+// of CTA 0..ctas, first unit of tile 0..n_tiles]. Tiles in the kernel's upper
+// column-by-column order; a k-step of a diagonal tile weighs 17, of any other 32.
+constexpr int64_t kSyrkLineMinRows = 32768;
+// Weight of a diagonal tile's k-step against 32 for a full tile. The DMMA count says 17; measured on
+// B200 (2^20 x 1024 Gram: 17 -> 33.8 ms, 18 -> 31.2, 19 -> 31.4, 20 -> 31.6, 23 -> 32.4, 32 -> 34.5; uniform
+// split-K grid 35.4 ms) a diagonal k-step costs ~0.59 of a full one (18 operand loads for 17 DMMAs).
+constexpr int kSyrkDiagWeight = 19;
+std::vector<long long> build_syrk_line(int tiles, int64_t K, int ctas, int diag_weight) {
+    const int n_tiles = tiles * (tiles + 1) / 2;
+    const long long ks = ceil_div(K, BK);
+    std::vector<int> weight(static_cast<size_t>(n_tiles), 32);
+    for (int tj = 0; tj < tiles; ++tj) weight[static_cast<size_t>(tj * (tj + 1) / 2 + tj)] = diag_weight;
+    long long total = 0;
+    for (int w : weight) total += ks * w;
+    // boundary b of the line, as (tile, k-step): the tile holding weight position b * total / ctas
+    std::vector<long long> out;
+    std::vector<long long> utab, cfirst(static_cast<size_t>(ctas) + 1), tfirst(static_cast<size_t>(n_tiles) + 1, -1);
+    int tile = 0;
+    long long step = 0, before = 0;  // weight before `tile`
+    for (int b = 0; b < ctas; ++b) {
+        cfirst[static_cast<size_t>(b)] = static_cast<long long>(utab.size() / 3);
+        const long long hi = b + 1 == ctas ? total : static_cast<long long>((static_cast<__int128>(total) * (b + 1)) / ctas);
+        while (tile < n_tiles) {
+            const long long wt = weight[static_cast<size_t>(tile)];
+            const long long tile_end = before + ks * wt;
+            // last k-step of this tile that belongs to CTA b (rounded to a whole step)
+            long long stop = hi >= tile_end ? ks : (hi - before + wt / 2) / wt;
+            stop = std::max(stop, step);
+            if (stop > step) {
+                if (tfirst[static_cast<size_t>(tile)] < 0) tfirst[static_cast<size_t>(tile)] = static_cast<long long>(utab.size() / 3);
+                utab.push_back(tile);
+                utab.push_back(std::min<long long>(step * BK, K));
+                utab.push_back(std::min<long long>(stop * BK, K));
+                step = stop;
+            }
+            if (step < ks) break;  // the rest of this tile goes to the next CTA
+            before = tile_end;
+            ++tile;
+            step = 0;
+            if (hi <= before) break;
+        }
+    }
+    cfirst[static_cast<size_t>(ctas)] = static_cast<long long>(utab.size() / 3);
+    tfirst[static_cast<size_t>(n_tiles)] = static_cast<long long>(utab.size() / 3);
+    for (int t = n_tiles - 1; t >= 0; --t)
+        if (tfirst[static_cast<size_t>(t)] < 0) tfirst[static_cast<size_t>(t)] = tfirst[static_cast<size_t>(t) + 1];
+    out.push_back(static_cast<long long>(utab.size() / 3));
+    out.insert(out.end(), utab.begin(), utab.end());
+    out.insert(out.end(), cfirst.begin(), cfirst.end());
+    out.insert(out.end(), tfirst.begin(), tfirst.end());
+    return out;
+}
+
 bool tma_ok(const void* p, int64_t ld) {
     return (reinterpret_cast<uintptr_t>(p) % 16 == 0) && (ld % 2 == 0);
 }
@@ -457,7 +613,7 @@ void launch(Ctx* c, Params& p, const CUtensorMap& ma, const CUtensorMap& mb) {
         partial = DBuf(c, static_cast<size_t>(p.units) * TILE_ELEMS);
         p.partial = partial.p();
     }
-    const int grid = std::min(p.units, c->num_sms);
+    const int grid = p.utab ? c->num_sms : std::min(p.units, c->num_sms);
     // algorithmic work: Gram m n (n+1); GEMM 2 M N K
     const double flops = p.kind == KIND_SYRK ? static_cast<double>(p.K) * p.M * (p.M + 1)
                          : p.b_upper      ? 1.0 * p.M * p.N * (p.N + 1)  // triangular B: M N (N+1)
@@ -648,6 +804,27 @@ void syrk(Ctx* c, int64_t m, int64_t n, const double* A, int64_t lda, double* G,
     p.ldc = ldg;
     p.alpha = alpha;
     p.beta_one = beta_one ? 1 : 0;
+    // Tall Gram (the c2 / c4 / c5 shapes): one work line over all SMs. A diagonal
+    // tile only needs its 136 upper 8 x 8 blocks (17 / 32 of a tile's DMMAs), so
+    // the line weighs its k-steps kSyrkDiagWeight against 32 for the other tiles and every CTA
+    // gets the same weight as a contiguous piece of it (pieces may straddle two
+    // tiles); the per-piece partial tiles are summed per tile in piece order.
+    DBuf line;
+    const char* sk_env = std::getenv("SVDK_SYRK_LINE");
+    if (m >= kSyrkLineMinRows && !(sk_env && std::atoi(sk_env) == 0)) {
+        const char* dw_env = std::getenv("SVDK_SYRK_DIAGW");
+        const int diag_w = dw_env ? std::min(32, std::max(1, std::atoi(dw_env))) : kSyrkDiagWeight;
+        std::vector<long long> host = build_syrk_line(p.tiles_m, m, c->num_sms, diag_w);
+        const size_t units = static_cast<size_t>(host[0]);
+        line = DBuf(c, host.size());
+        h2d(c, line.p(), reinterpret_cast<const double*>(host.data()), static_cast<int64_t>(host.size()));
+        const long long* base = reinterpret_cast<const long long*>(line.p());
+        p.utab = base + 1;
+        p.cfirst = p.utab + 3 * units;
+        p.tfirst = p.cfirst + c->num_sms + 1;
+        p.units = static_cast<int>(units);
+        p.splits = 2;  // partial tiles + the reduction kernel
+    }
     const CUtensorMap ma = make_map(A, m, n, lda, BK, BM);
     launch(c, p, ma, ma);
 }

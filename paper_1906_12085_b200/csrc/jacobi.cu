@@ -31,6 +31,7 @@
 #include <cstdlib>
 #include <functional>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -1748,6 +1749,17 @@ struct JacobiCache {
 namespace {
 constexpr size_t kMaxPlans = 4;
 
+// Contexts of one process may be driven by several host threads (the host-staged
+// group runs one rank per thread, and every rank of a sketch method solves its own
+// small eigenproblem). Building a plan (stream capture into a conditional-node
+// graph + instantiation) and launching one are serialised across threads: with
+// them concurrent, tests/test_gpu_sharded.py's sketch cases died with SIGSEGV
+// inside svdk_dev_pca in ~8% of runs.
+std::mutex& graph_mutex() {
+    static std::mutex mu;
+    return mu;
+}
+
 cudaGraphNode_t add_kernel_node(cudaGraph_t g, const cudaGraphNode_t* deps, size_t ndeps, const void* func,
                                 dim3 grid, dim3 block, void** args) {
     cudaKernelNodeParams kp = {};
@@ -1817,18 +1829,28 @@ void build_loop_graph(Ctx* c, JacobiPlan& P) {
         cudaGraphDestroy(outer);
         return;
     }
+    // A capture can be invalidated from outside (e.g. another host thread calls
+    // cudaDeviceSynchronize while this stream captures): any failure here leaves
+    // P.exec null and eig_sym drives the same kernels from the host instead.
     cudaGraph_t captured = nullptr;
+    bool captured_ok = true;
     try {
         P.enqueue_sweep();
         jacobi_sumsq_kernel<<<blocks, 256, 0, S>>>(A, n, 1, pl);
         jacobi_decide_kernel<<<1, 32, 0, S>>>(h, pl, blocks, scal, 1);
+    } catch (const Failure&) {
+        captured_ok = false;
     } catch (...) {  // leave the stream out of capture mode
         cudaStreamEndCapture(S, &captured);
         cudaGetLastError();
         cudaGraphDestroy(outer);
         throw;
     }
-    SVDK_CUDA(cudaStreamEndCapture(S, &captured));
+    if (cudaStreamEndCapture(S, &captured) != cudaSuccess || !captured_ok) {
+        cudaGetLastError();
+        cudaGraphDestroy(outer);
+        return;
+    }
     const cudaError_t ie = cudaGraphInstantiate(&P.exec, outer, 0);
     cudaGraphDestroy(outer);
     if (ie != cudaSuccess) {
@@ -1843,6 +1865,7 @@ void build_loop_graph(Ctx* c, JacobiPlan& P) {
 int run_plan(Ctx* c, JacobiPlan& P) {
     cudaStream_t S = c->stream;
     if (P.exec) {
+        std::lock_guard<std::mutex> lock(graph_mutex());
         SVDK_CUDA(cudaGraphLaunch(P.exec, S));
         return -1;  // read from scal by the caller
     }
@@ -2798,6 +2821,7 @@ JacobiPlan& jacobi_plan(Ctx* c, int64_t n_pad, int TB) {
     fill(c, p->scal.p(), JS_COUNT, 0.0);
     JacobiPlan& P = *p;
     plans.push_back(std::move(p));
+    std::lock_guard<std::mutex> lock(graph_mutex());
     try {
         if (TB == 16)
             build_pair_plan<16>(c, P);

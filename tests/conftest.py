@@ -24,6 +24,17 @@ def _has_gpu() -> bool:
 HAS_GPU = _has_gpu()
 
 
+@pytest.fixture(scope="session", autouse=True)
+def _segv_trace():
+    """Development: native backtrace on SIGSEGV (tools/debug/segv_trace.c), installed after
+    pytest's faulthandler so both print. SVDK_SEGV_TRACE=<path to libsegv_trace.so>."""
+    path = os.environ.get("SVDK_SEGV_TRACE")
+    if path:
+        import ctypes
+        ctypes.CDLL(path).segv_trace_install()
+    yield
+
+
 @pytest.fixture(scope="session")
 def port():
     from oracle.pyoracle import Oracle

@@ -64,7 +64,9 @@ def run_sharded(a, bounds, method, threshold, args_override=None):
             if args_override and r in args_override:
                 kw.update(args_override[r])
             results[r] = engines[r].pca(shards[r], **kw)
-            torch.cuda.synchronize()
+            # this rank's stream only: a device-wide synchronize is illegal while another
+            # rank's thread is capturing its sweep graph (it invalidates that capture)
+            engines[r].ctx.sync()
         except Exception as e:  # collected and asserted by the caller
             results[r] = e
 
