@@ -893,3 +893,14 @@ void gemm(Ctx* c, bool transa, int64_t m, int64_t n, int64_t k, const double* A,
 }
 
 }  // namespace svdk
+
+// Development / test hook (not part of the public ABI): the SYRK work line
+// for `tiles` x `tiles` upper tiles, K rows and `ctas` CTAs. Returns the
+// table's length in 64-bit words; copies it when it fits `cap`.
+extern "C" long long svdk_debug_syrk_line(int tiles, long long K, int ctas, int diag_weight, long long* out,
+                                          long long cap) {
+    if (tiles < 1 || K < 1 || ctas < 1) return -1;
+    const std::vector<long long> t = svdk::build_syrk_line(tiles, K, ctas, diag_weight > 0 ? diag_weight : svdk::kSyrkDiagWeight);
+    if (out && static_cast<long long>(t.size()) <= cap) std::copy(t.begin(), t.end(), out);
+    return static_cast<long long>(t.size());
+}

@@ -312,3 +312,45 @@ def test_facade_tools_host_match_reference(rt):
     assert widths == [(n, rt.sketch_width_for(0.5, n)) for n in (1, 3, 784, 1001)]
     assert csv_text == rt.bench_csv(TOOL_RECORDS)
     assert report_text == rt.ordering_report(TOOL_RECORDS)[0]
+
+
+# --------------------------------------------------------------------------- SYRK work line (host logic)
+@pytest.mark.parametrize("tiles,rows,ctas", [(8, 8388608, 148), (8, 200000, 148), (32, 65536, 148), (16, 500000, 148),
+                                             (2, 32768, 148), (1, 40000, 148), (3, 33001, 148), (8, 1 << 20, 7)])
+def test_syrk_work_line_table(tiles, rows, ctas):
+    """build_syrk_line (csrc/gemm_f64.cu): every upper tile's k range [0, K) is covered exactly once by
+    contiguous pieces in piece order, a tile's pieces and a CTA's pieces are contiguous in the table, and the
+    CTAs' weights (32 per full k-step, 19 per diagonal one) are equal to within one k-step per piece."""
+    import ctypes as C
+    from paper_1906_12085_b200 import _lib
+    lib = C.CDLL(_lib.LIB_PATH)
+    lib.svdk_debug_syrk_line.restype = C.c_longlong
+    lib.svdk_debug_syrk_line.argtypes = [C.c_int, C.c_longlong, C.c_int, C.c_int, C.POINTER(C.c_longlong), C.c_longlong]
+    need = lib.svdk_debug_syrk_line(tiles, rows, ctas, 0, None, 0)
+    buf = (C.c_longlong * need)()
+    assert lib.svdk_debug_syrk_line(tiles, rows, ctas, 0, buf, need) == need
+    t = list(buf)
+    units, n_tiles = t[0], tiles * (tiles + 1) // 2
+    utab = [tuple(t[1 + 3 * u:4 + 3 * u]) for u in range(units)]
+    cfirst = t[1 + 3 * units:1 + 3 * units + ctas + 1]
+    tfirst = t[1 + 3 * units + ctas + 1:]
+    assert len(tfirst) == n_tiles + 1 and cfirst[0] == 0 and cfirst[-1] == units and tfirst[-1] == units
+    assert all(a <= b for a, b in zip(cfirst, cfirst[1:]))
+    diag = {tj * (tj + 1) // 2 + tj for tj in range(tiles)}
+    for tile in range(n_tiles):
+        pieces = utab[tfirst[tile]:tfirst[tile + 1]]
+        assert pieces and all(p[0] == tile for p in pieces)
+        assert pieces[0][1] == 0 and pieces[-1][2] == rows
+        assert all(a[2] == b[1] and a[2] % 16 == 0 for a, b in zip(pieces, pieces[1:]))
+        assert all(p[2] > p[1] for p in pieces)
+    assert sorted(u[0] for u in utab) == [u[0] for u in utab]  # tile order
+    loads = []
+    for b in range(ctas):
+        w = 0
+        for tile, k0, k1 in utab[cfirst[b]:cfirst[b + 1]]:
+            w += -(-(k1 - k0) // 16) * (19 if tile in diag else 32)
+        loads.append(w)
+    mean = sum(loads) / ctas
+    pieces_max = max(cfirst[b + 1] - cfirst[b] for b in range(ctas))
+    assert max(loads) - mean <= 32 * (pieces_max + 1), (max(loads), mean)
+    assert mean - min(loads) <= 32 * (pieces_max + 1), (min(loads), mean)
