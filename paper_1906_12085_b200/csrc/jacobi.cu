@@ -1405,8 +1405,10 @@ __device__ __forceinline__ void fused_solve_role(const double* A, int64_t lda, c
         {
             const int c = tid >> 3, r4 = (tid & 7) * 4;
             const int pp = c < B ? pI : pJ, cc = c < B ? oI + c : oJ + (c - B);
-            tv = __ldcg(&act_prev[pp]) ? ld_cg4(Qprev + static_cast<size_t>(pp) * 1024 + r4 + cc * 32)
-                                       : make_double4(r4 == cc, r4 + 1 == cc, r4 + 2 == cc, r4 + 3 == cc);
+            // the slot is read unconditionally (always allocated), beside the flag instead of behind it
+            const int act = __ldcg(&act_prev[pp]);
+            tv = ld_cg4(Qprev + static_cast<size_t>(pp) * 1024 + r4 + cc * 32);
+            if (!act) tv = make_double4(r4 == cc, r4 + 1 == cc, r4 + 2 == cc, r4 + 3 == cc);
             double* d = Tc + r4 + c * AH_LT;
             d[0] = tv.x; d[1] = tv.y; d[2] = tv.z; d[3] = tv.w;
         }
@@ -1417,44 +1419,60 @@ __device__ __forceinline__ void fused_solve_role(const double* A, int64_t lda, c
             d[0] = xv[k].x; d[1] = xv[k].y; d[2] = xv[k].z; d[3] = xv[k].w;
         }
         named_bar(2, FR_SOLVE_THREADS);
-        {  // Y = X T: warp w forms rows [8w, 8w + 8); n-tiles 0, 1 contract over P's first pair, 2, 3 over its second
+        {  // Y = X T: warp w forms rows [8w, 8w + 8); n-tiles 0, 1 contract over P's first pair, 2, 3 over its
+           // second. M's lower-left block is the mirror of its upper-right one, so rows 32.. of Y (warps 4-7)
+           // only need the n-tiles 2, 3.
+            const int t0 = w < 4 ? 0 : 2;
             double acc[4][2];
 #pragma unroll
             for (int t = 0; t < 4; ++t) acc[t][0] = acc[t][1] = 0.0;
 #pragma unroll
             for (int s8 = 0; s8 < 8; ++s8) {
                 const int k = 4 * s8 + kq;
-                const double a0 = X[(8 * w + r) + k * AH_LX], a1 = X[(8 * w + r) + (32 + k) * AH_LX];
+                const double a1 = X[(8 * w + r) + (32 + k) * AH_LX];
+                if (t0 == 0) {
+                    const double a0 = X[(8 * w + r) + k * AH_LX];
 #pragma unroll
-                for (int t = 0; t < 4; ++t) dmma(acc[t][0], acc[t][1], t < 2 ? a0 : a1, Tc[k + (8 * t + r) * AH_LT]);
+                    for (int t = 0; t < 2; ++t) dmma(acc[t][0], acc[t][1], a0, Tc[k + (8 * t + r) * AH_LT]);
+                }
+#pragma unroll
+                for (int t = 2; t < 4; ++t) dmma(acc[t][0], acc[t][1], a1, Tc[k + (8 * t + r) * AH_LT]);
             }
 #pragma unroll
             for (int t = 0; t < 4; ++t)
 #pragma unroll
-                for (int i = 0; i < 2; ++i) Y[(8 * w + r) + (8 * t + 2 * kq + i) * AH_LX] = acc[t][i];
+                for (int i = 0; i < 2; ++i)
+                    if (t >= t0) Y[(8 * w + r) + (8 * t + 2 * kq + i) * AH_LX] = acc[t][i];
         }
         named_bar(2, FR_SOLVE_THREADS);
-        {  // M = T^T Y: warp w forms rows [8 (w & 3), + 8) x columns [16 (w >> 2), + 16)
+        {  // M = T^T Y: warp w forms rows [8 (w & 3), + 8) x columns [16 (w >> 2), + 16); the lower-left block
+           // (rows >= 16, columns < 16) is read as the mirror of the upper-right one below
             const int mw = w & 3, nh = w >> 2;
-            double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-            const int yoff = mw < 2 ? 0 : 32;  // rows < 16: T_I^T Y[0:32], else T_J^T Y[32:64]
+            if (!(mw >= 2 && nh == 0)) {
+                double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+                const int yoff = mw < 2 ? 0 : 32;  // rows < 16: T_I^T Y[0:32], else T_J^T Y[32:64]
 #pragma unroll
-            for (int s8 = 0; s8 < 8; ++s8) {
-                const int k = 4 * s8 + kq;
-                const double af = Tc[k + (8 * mw + r) * AH_LT];
+                for (int s8 = 0; s8 < 8; ++s8) {
+                    const int k = 4 * s8 + kq;
+                    const double af = Tc[k + (8 * mw + r) * AH_LT];
+#pragma unroll
+                    for (int t = 0; t < 2; ++t)
+                        dmma(acc[t][0], acc[t][1], af, Y[(yoff + k) + (8 * (2 * nh + t) + r) * AH_LX]);
+                }
 #pragma unroll
                 for (int t = 0; t < 2; ++t)
-                    dmma(acc[t][0], acc[t][1], af, Y[(yoff + k) + (8 * (2 * nh + t) + r) * AH_LX]);
+#pragma unroll
+                    for (int i = 0; i < 2; ++i)
+                        Ms[(8 * mw + r) + (8 * (2 * nh + t) + 2 * kq + i) * AH_LT] = acc[t][i];
             }
-#pragma unroll
-            for (int t = 0; t < 2; ++t)
-#pragma unroll
-                for (int i = 0; i < 2; ++i) Ms[(8 * mw + r) + (8 * (2 * nh + t) + 2 * kq + i) * AH_LT] = acc[t][i];
         }
         named_bar(2, FR_SOLVE_THREADS);
         if (w < QW) {
 #pragma unroll
-            for (int i = 0; i < QR; ++i) wreg[i] = Ms[(row0 + i) + lane * AH_LT];
+            for (int i = 0; i < QR; ++i) {
+                const int rw = row0 + i;
+                wreg[i] = (rw >= 16 && lane < 16) ? Ms[lane + rw * AH_LT] : Ms[rw + lane * AH_LT];
+            }
         }
     }
     bool big = false;
