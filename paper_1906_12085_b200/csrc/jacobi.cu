@@ -157,6 +157,15 @@ __device__ __forceinline__ void smem_mma(const double* A, const double* Bm, doub
 // Development probe: clock64 stamps of CTA 0 in the last pair solve (read by
 // svdk_debug_jacobi_probe; not part of the public ABI).
 __device__ long long g_jprobe[16];
+// %globaltimer stamps of the fused round kernels' roles per round (SVDK_PROBES builds, tools/fr_timeline.py)
+__device__ unsigned long long g_jtimeline[16 * 8];
+#ifdef SVDK_PROBES
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#endif
 
 template <int TB>
 constexpr int solve_q_warps() {
@@ -1357,6 +1366,10 @@ __device__ __forceinline__ void fused_solve_role(const double* A, int64_t lda, c
     const int R = mode == 0 ? TB - 1 : (mode == 1 ? B - 1 : B);
     const bool probe = pair == 0 && round == 5 && tid == 0;
     const long long t0 = SVDK_CLOCK();
+#ifdef SVDK_PROBES
+    const bool tl = pair == 0 && tid == 0 && round < 16 && mode == 2;
+    if (tl) g_jtimeline[round * 8 + 0] = gtime();
+#endif
     int I, J;
     circle_pair(nb, round, pair, I, J);
     {
@@ -1377,6 +1390,9 @@ __device__ __forceinline__ void fused_solve_role(const double* A, int64_t lda, c
     named_bar(2, FR_SOLVE_THREADS);
     pdl_wait();  // the previous kernel: Q_{j-1}, its active flags and A_{j-2}
     const long long t1 = SVDK_CLOCK();
+#ifdef SVDK_PROBES
+    if (tl) g_jtimeline[round * 8 + 1] = gtime();
+#endif
     const double skip_tau = *skip_tau_p;
     const int row0 = (w & 3) * QR;
     double wreg[QR], qreg[QR];
@@ -1510,6 +1526,9 @@ __device__ __forceinline__ void fused_solve_role(const double* A, int64_t lda, c
     for (int v = 0; v < QR / 4; ++v)
         st4(out + 4 * v, f * qreg[4 * v], f * qreg[4 * v + 1], f * qreg[4 * v + 2], f * qreg[4 * v + 3]);
     if (probe) SVDK_PROBE_STORE(g_jprobe, 4, SVDK_CLOCK());
+#ifdef SVDK_PROBES
+    if (tl) g_jtimeline[round * 8 + 2] = gtime();
+#endif
 }
 
 template <bool FAST>
@@ -1527,7 +1546,14 @@ __global__ void __launch_bounds__(FR_THREADS, 1)
     // (pair, 32-row chunk) of V <- V Q.
     const bool probe = b == n_solve && threadIdx.x == 0 && round == 5;
     const long long t0 = SVDK_CLOCK();
+#ifdef SVDK_PROBES
+    const bool tl = threadIdx.x == 0 && round < 16 && mode == 2 && n_solve > 0;
+    if (tl && b == n_solve) g_jtimeline[round * 8 + 3] = gtime();
+#endif
     pdl_wait();
+#ifdef SVDK_PROBES
+    if (tl && b == n_solve) g_jtimeline[round * 8 + 4] = gtime();
+#endif
     if (probe) {
         SVDK_PROBE_STORE(g_jprobe, 8, t0);
         SVDK_PROBE_STORE(g_jprobe, 9, SVDK_CLOCK());
@@ -1541,6 +1567,10 @@ __global__ void __launch_bounds__(FR_THREADS, 1)
         if (probe && t < nw) SVDK_PROBE_STORE(g_jprobe, 10, SVDK_CLOCK());
     }
     if (probe) SVDK_PROBE_STORE(g_jprobe, 11, SVDK_CLOCK());
+#ifdef SVDK_PROBES
+    if (tl && b == n_solve) g_jtimeline[round * 8 + 5] = gtime();
+    if (tl) atomicMax(&g_jtimeline[round * 8 + 6], gtime());
+#endif
 }
 
 // ---------------------------------------------------------------------------
@@ -2927,6 +2957,10 @@ void jacobi_cache_free(Ctx* c) {
 }
 
 }  // namespace svdk
+
+extern "C" int svdk_debug_jacobi_timeline(unsigned long long* out) {
+    return cudaMemcpyFromSymbol(out, svdk::g_jtimeline, 16 * 8 * sizeof(unsigned long long)) == cudaSuccess ? 0 : 4;
+}
 
 extern "C" int svdk_debug_jacobi_probe(long long* out) {
     return cudaMemcpyFromSymbol(out, svdk::g_jprobe, 16 * sizeof(long long)) == cudaSuccess ? 0 : 4;
