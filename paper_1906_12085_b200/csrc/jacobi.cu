@@ -1537,6 +1537,10 @@ __global__ void __launch_bounds__(FR_THREADS, 1)
                        double* Qcur, int* act_cur, const double* Qprev, const int* act_prev, int nb, int round,
                        int rprev, int mode, const double* skip_tau_p, int n_solve, int a_tasks, int v_tasks) {
     const int b = blockIdx.x, w = threadIdx.x >> 5;
+    // Every CTA lets the next round's kernel launch at once: its CTAs take the SMs this kernel leaves
+    // free (one CTA per SM, so they crowd nobody), run their prologue up to griddepcontrol.wait and
+    // absorb the launch latency (n = 256: 0.8 us gap + 0.5 us prologue per round, tools/fr_timeline.py).
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (b < n_solve) {
         fused_solve_role<FAST>(Ain, ld, tabs, Qcur, act_cur, nb, round, skip_tau_p, mode, Qprev, act_prev, rprev, b);
         return;
