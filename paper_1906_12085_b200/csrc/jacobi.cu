@@ -2843,10 +2843,10 @@ void build_quad_plan(Ctx* c, JacobiPlan& P) {
 }  // namespace
 
 // Smallest n that uses the quad scheme by default. Measured on B200
-// (tools/jacobi_eval.sh, Gram spectra): n = 1024 / 2048 / 4096 take 17.2 / 61.1
-// / 396 ms with 2b = 32 and 20.5 / 68.7 / 338 ms with the quad scheme — below
-// n ~ 3000 the solve chain (not the update traffic) bounds a sweep.
-constexpr int64_t kQuadMinN = 3072;
+// (tools/eig_time.py with SVDK_JACOBI_TB, Gram spectra, one-sided solves): n = 1536 / 2048 / 2560 /
+// 3072 take 26.0 / 45.7 / 100.0 / 167.6 ms with 2b = 32 and 29.2 / 48.7 / 85.4 / 142.1 ms with the
+// quad scheme — below n ~ 2300 the solve chain (not the update traffic) bounds a sweep.
+constexpr int64_t kQuadMinN = 2304;
 
 // The context's sweep plan for (n_pad, TB), built on first use and kept
 // (most recently used last, at most kMaxPlans per context).
