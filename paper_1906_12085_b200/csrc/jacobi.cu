@@ -2121,7 +2121,7 @@ void build_pair_plan(Ctx* c, JacobiPlan& P) {
     };
     // Fused round kernels (jacobi_round_fused, solve-ahead): default for
     // n_pad <= kAheadMaxN, where a round is a latency chain; SVDK_JACOBI_AHEAD=0/1 overrides.
-    bool ahead = TB == 32 && split && nb > 2 && n_pad <= kAheadMaxN;
+    bool ahead = TB == 32 && split && nb > 2 && n_pad <= kAheadMaxN && os_warps == 4 && !os_ns;
     if (const char* e = std::getenv("SVDK_JACOBI_AHEAD")) ahead = TB == 32 && split && nb > 2 && std::atoi(e) != 0;
     if constexpr (TB == 32) {
         if (ahead) {
