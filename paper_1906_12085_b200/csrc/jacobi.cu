@@ -1065,6 +1065,24 @@ __device__ __forceinline__ void upd_a_unit_vec(const double* A, double* Aout, in
     const double* Qa = Qbuf + static_cast<size_t>(p) * 1024;
     const double* Qb = Qbuf + static_cast<size_t>(q) * 1024;
     const int m0 = part * MW;
+    if (!INPLACE && MS == 2 && live && !(ap | aq)) {
+        // ping-pong and both rotations the identity (late sweeps, the polish sweep): this half of the
+        // block and its mirror are copied, no DMMA work
+        const int64_t gi0 = static_cast<int64_t>(part ? Jp : Ip) * B + 4 * kq;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int64_t gc = gidx(B, Iq, Jq, 8 * t + r);
+            const double4 v = ld_cg4(A + gi0 + gc * lda);
+            st4(Aout + gi0 + gc * lda, v.x, v.y, v.z, v.w);
+            if (p != q) {
+                Aout[gc + gi0 * lda] = v.x;
+                Aout[gc + (gi0 + 1) * lda] = v.y;
+                Aout[gc + (gi0 + 2) * lda] = v.z;
+                Aout[gc + (gi0 + 3) * lda] = v.w;
+            }
+        }
+        return;
+    }
     double out[MW][4][2];
     if (live) {
         // global row of local index 16h + 4kq (h = 0: block I_p, 1: J_p) and
