@@ -1281,21 +1281,30 @@ __device__ __forceinline__ void upd_v_unit(double* V, int64_t ldv, int64_t n_row
     int Iq, Jq;
     circle_pair(nb, round, q, Iq, Jq);
     const double* Qb = Qbuf + static_cast<size_t>(q) * 1024;
+    // The contraction index of k-step s is k(s, kq) = 16 (s >> 2) + 4 kq + (s & 3) (a permutation of
+    // 0..31, the same in both operands), so a lane's Q_q fragments of four k-steps are four consecutive
+    // rows of one column: 8 32-byte loads instead of 32 8-byte ones.
     double qb[8][4];
 #pragma unroll
-    for (int s = 0; s < 8; ++s)
+    for (int h = 0; h < 2; ++h)
 #pragma unroll
-        for (int t = 0; t < 4; ++t) qb[s][t] = __ldcg(&Qb[(4 * s + kq) + (8 * t + r) * 32]);
+        for (int t = 0; t < 4; ++t) {
+            const double4 q4 = ld_cg4(Qb + 16 * h + 4 * kq + (8 * t + r) * 32);
+            qb[4 * h][t] = q4.x; qb[4 * h + 1][t] = q4.y; qb[4 * h + 2][t] = q4.z; qb[4 * h + 3][t] = q4.w;
+        }
     double* vb = V + 4 * r;
+    int64_t vcol[8];  // column of V for k-step s
+#pragma unroll
+    for (int s = 0; s < 8; ++s) vcol[s] = gidx(B, Iq, Jq, 16 * (s >> 2) + 4 * kq + (s & 3)) * ldv;
     double4 va[8];
 #pragma unroll
-    for (int s = 0; s < 8; ++s) va[s] = ld_cg4(vb + row_begin + gidx(B, Iq, Jq, 4 * s + kq) * ldv);
+    for (int s = 0; s < 8; ++s) va[s] = ld_cg4(vb + row_begin + vcol[s]);
     for (int64_t row0 = row_begin; row0 < row_end; row0 += 32) {
         const bool more = row0 + 32 < row_end;
         double4 vn[8];
         if (more) {
 #pragma unroll
-            for (int s = 0; s < 8; ++s) vn[s] = ld_cg4(vb + row0 + 32 + gidx(B, Iq, Jq, 4 * s + kq) * ldv);
+            for (int s = 0; s < 8; ++s) vn[s] = ld_cg4(vb + row0 + 32 + vcol[s]);
         }
         double acc[4][4][2];
 #pragma unroll
