@@ -1100,8 +1100,9 @@ __device__ __forceinline__ void upd_a_unit_vec(const double* A, double* Aout, in
             for (int m = 0; m < MW; ++m) {
                 // Q_p[16h + 4kq + j][8(m0 + m) + r]; identity when inactive
                 const int k0 = 16 * h + 4 * kq, c = 8 * (m0 + m) + r;
-                qa[h][m] = ap ? ld_cg4(Qa + k0 + c * 32)
-                              : make_double4(k0 == c, k0 + 1 == c, k0 + 2 == c, k0 + 3 == c);
+                // the slot is read beside the active flag, not behind it (always allocated)
+                qa[h][m] = ld_cg4(Qa + k0 + c * 32);
+                if (!ap) qa[h][m] = make_double4(k0 == c, k0 + 1 == c, k0 + 2 == c, k0 + 3 == c);
             }
         }
         double2 qb[4][4];  // Q_q[8a + 2kq + {0,1}][8t + r]
@@ -1110,7 +1111,8 @@ __device__ __forceinline__ void upd_a_unit_vec(const double* A, double* Aout, in
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
                 const int k0 = 8 * a + 2 * kq, c = 8 * t + r;
-                qb[a][t] = aq ? ld_cg2(Qb + k0 + c * 32) : make_double2(k0 == c, k0 + 1 == c);
+                qb[a][t] = ld_cg2(Qb + k0 + c * 32);
+                if (!aq) qb[a][t] = make_double2(k0 == c, k0 + 1 == c);
             }
         double acc[MW][4][2];
 #pragma unroll
