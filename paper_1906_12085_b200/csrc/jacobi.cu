@@ -2648,8 +2648,9 @@ __global__ void __launch_bounds__(A64_THREADS)
         const int e = tid + it * A64_THREADS;
         const int i = (e & 31) * 2, j = e >> 5;
         const double2 x = __ldcg(reinterpret_cast<const double2*>(&A[gp(i) + gq(j) * lda]));
-        const double2 y = aq ? __ldcg(reinterpret_cast<const double2*>(&Qq[i + j * 64]))
-                             : make_double2(i == j ? 1.0 : 0.0, i + 1 == j ? 1.0 : 0.0);
+        // the rotation slots are read beside the active flags, not behind them (always allocated)
+        double2 y = __ldcg(reinterpret_cast<const double2*>(&Qq[i + j * 64]));
+        if (!aq) y = make_double2(i == j ? 1.0 : 0.0, i + 1 == j ? 1.0 : 0.0);
         *reinterpret_cast<double2*>(&Xs[i + j * L64]) = x;
         *reinterpret_cast<double2*>(&Qs[i + j * L64]) = y;
     }
@@ -2660,7 +2661,8 @@ __global__ void __launch_bounds__(A64_THREADS)
 #pragma unroll
         for (int mt = 0; mt < 2; ++mt) {
             const int k = 4 * s + kq, m = 16 * w + 8 * mt + r;
-            qpf[s][mt] = ap ? __ldcg(&Qp[k + m * 64]) : (k == m ? 1.0 : 0.0);
+            qpf[s][mt] = __ldcg(&Qp[k + m * 64]);
+            if (!ap) qpf[s][mt] = k == m ? 1.0 : 0.0;
         }
     __syncthreads();
     double U[2][8][2];
