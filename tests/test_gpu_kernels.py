@@ -138,6 +138,30 @@ def test_eig_quad_default_ragged(sk):
     assert np.max(np.abs(v.T @ v - np.eye(n))) <= 1e-12
 
 
+@pytest.mark.parametrize("n,env", [(1300, {}), (2400, {}), (300, {"SVDK_JACOBI_AHEAD": "0"}),
+                                   (360, {"SVDK_JACOBI_OS": "0"}), (420, {"SVDK_JACOBI_FASTROT": "0"}),
+                                   (460, {"SVDK_JACOBI_AHEAD": "0", "SVDK_JACOBI_NS": "1"})])
+def test_eig_solver_paths(sk, monkeypatch, n, env):
+    """Every Jacobi path against LAPACK on a Gram spectrum: the separate-kernel one-sided chain
+    (1024 < n < 2304 by default: n = 1300), the quad scheme from its new threshold (n = 2400), and at
+    small n the paths behind the switches — separate kernels instead of the fused rounds, the
+    two-sided round-1 solve, the rsqrt()-based rotation, Newton-Schulz instead of the column-norm
+    step. The sizes are used by no other test: a context keeps its sweep plan per padded n, and the
+    switches are read when the plan is built."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    rng = np.random.default_rng(7000 + n)
+    x = rng.standard_normal((n + 200, n))
+    s = np.asfortranarray(x.T @ x)
+    e = sk.eig_sym(s)
+    w, v = e.eigenvalues, e.eigenvectors
+    fro = np.linalg.norm(s)
+    assert np.all(np.diff(w) <= 0)
+    assert np.max(np.abs(w - np.linalg.eigvalsh(s)[::-1])) <= 1e-13 * fro
+    assert np.linalg.norm(s @ v - v * w) <= 1e-10 * fro
+    assert np.max(np.abs(v.T @ v - np.eye(n))) <= 1e-12
+
+
 def test_eig_errors(sk):
     with pytest.raises(errors.DimensionError):
         sk.eig_sym(np.ones((2, 3)))
