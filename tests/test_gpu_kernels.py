@@ -71,7 +71,7 @@ def test_eig_kats(sk):
     assert e.eigenvalues.tolist() == [3, 1] and np.array_equal(np.abs(e.eigenvectors), [[0, 1], [1, 0]])
 
 
-@pytest.mark.parametrize("n", [3, 17, 64, 100, 256, 513, 1024])
+@pytest.mark.parametrize("n", [3, 17, 64, 70, 100, 256, 513, 1024])
 def test_eig_random_symmetric(sk, n):
     rng = np.random.default_rng(n)
     x = rng.standard_normal((n, n))
