@@ -162,6 +162,45 @@ def test_eig_solver_paths(sk, monkeypatch, n, env):
     assert np.max(np.abs(v.T @ v - np.eye(n))) <= 1e-12
 
 
+@pytest.mark.parametrize("kind", ["identity", "diagonal", "rank_one", "ones", "huge", "tiny", "degenerate", "zero"])
+def test_eig_edge_spectra(sk, kind):
+    """Edge spectra on the fused one-sided rounds (n = 200): already diagonal inputs (no rotation is
+    applied), rank one and all-ones (n - 1 zero eigenvalues), entries near 1e150 / 1e-150 (the power-of-
+    two prescale), a spectrum of three exactly repeated values, and the zero matrix."""
+    n = 200
+    rng = np.random.default_rng(11)
+    if kind == "identity":
+        s = np.eye(n)
+    elif kind == "diagonal":
+        s = np.diag(rng.standard_normal(n))
+    elif kind == "rank_one":
+        x = rng.standard_normal(n)
+        s = np.outer(x, x)
+    elif kind == "ones":
+        s = np.ones((n, n))
+    elif kind in ("huge", "tiny"):
+        x = rng.standard_normal((n, n))
+        s = (x + x.T) * (1e150 if kind == "huge" else 1e-150)
+    elif kind == "degenerate":
+        q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+        d = np.repeat([3.0, 1.0, -2.0], [70, 70, 60])
+        s = (q * d) @ q.T
+        s = 0.5 * (s + s.T)
+    else:
+        s = np.zeros((n, n))
+    s = np.asfortranarray(s)
+    e = sk.eig_sym(s)
+    w, v = e.eigenvalues, e.eigenvectors
+    fro = max(np.linalg.norm(s), 1e-300)
+    assert np.all(np.isfinite(w)) and np.all(np.isfinite(v))
+    assert np.all(np.diff(w) <= 0)
+    assert np.max(np.abs(w - np.linalg.eigvalsh(s)[::-1])) <= 1e-13 * fro
+    assert np.linalg.norm(s @ v - v * w) <= 1e-10 * fro
+    assert np.max(np.abs(v.T @ v - np.eye(n))) <= 1e-12
+    if kind in ("identity", "diagonal", "zero"):
+        assert np.array_equal(np.abs(v) > 0, np.abs(v) == 1.0)  # a permutation: nothing was rotated
+
+
 def test_eig_errors(sk):
     with pytest.raises(errors.DimensionError):
         sk.eig_sym(np.ones((2, 3)))
