@@ -5,7 +5,8 @@ its sources):
 
     python tests/golden/make_golden.py small c1 c2mid      # minutes
     python tests/golden/make_golden.py c2 [--threads T]     # ~1 h  (full reference truncated + randomized)
-    python tests/golden/make_golden.py c4 c3 c5             # hours (c5: eig_sym(4096) ~3.4 h)
+    python tests/golden/make_golden.py c4 c3 c5             # hours (c5: eig_sym(4096) > 4 h)
+    python tests/golden/make_golden.py c5lapack             # 8 min: c5's reference Gram + LAPACK (cross-check)
 
 Inputs come from the generator shared with bench.py (paper_1906_12085_b200/
 synth.py): the GPU regenerates the same bytes, checked through `a_rows` (a few
@@ -209,7 +210,7 @@ def block_gram(ref, c_rows_iter, threads):
 
 
 def blocked(ref, name, cfg, seed, threads, sub_rows=32768, gen_rows=262144, force_vk=False,
-            materialise_max=12e9):
+            materialise_max=12e9, eig="ref"):
     m, n = cfg.m, cfg.n
     times = {"m": m, "n": n, "threads": threads, "sub_rows": sub_rows, "host": os.uname().nodename}
     t0 = time.time()
@@ -271,15 +272,21 @@ def blocked(ref, name, cfg, seed, threads, sub_rows=32768, gen_rows=262144, forc
         total = tot[0]
     log(name, f"gram done {times['block_gram_s']:.1f}s; eig_sym({n}) ...")
     t0 = time.perf_counter()
-    w, v = ref.eig_sym(g)
+    if eig == "lapack":  # labelled weaker oracle: LAPACK dsyevd on the reference's Gram (minutes instead of hours)
+        w, v = np.linalg.eigh(g)
+        w, v = w[::-1].copy(), v[:, ::-1].copy()
+    else:
+        w, v = ref.eig_sym(g)
     times["eig_sym_s"] = time.perf_counter() - t0
     lam, rank = finish_lambda(w)
     k = ref.select_components(lam, total, cfg.t) or 0
     log(name, f"eig_sym {times['eig_sym_s']:.1f}s rank={rank} K={k}")
     out.update(total=total, mean=mean, truncated_lambda=lam, truncated_k=k,
                truncated_margin=k_margin(lam, total, cfg.t, k), gram_sha256=sha(g),
-               oracle=(f"svdkit_ref::gram on {sub_rows}-row blocks summed in block order + svdkit_ref::eig_sym "
-                       f"(SURVEY 8c alternative); total: {total_note}"))
+               oracle=(f"svdkit_ref::gram on {sub_rows}-row blocks summed in block order + "
+                       + ("LAPACK dsyevd (numpy.linalg.eigh) on that Gram — NOT the reference eig_sym; a labelled "
+                          "cross-check oracle" if eig == "lapack" else "svdkit_ref::eig_sym")
+                       + f" (SURVEY 8c alternative); total: {total_note}"))
     store_basis(out, "truncated", lam, v, k, n, force_vk=force_vk)
     np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **out)
     record_times(name, times)
@@ -309,5 +316,7 @@ if __name__ == "__main__":
                  {"truncated": (0, 0, 0), "randomized": (1024, 2, synth.METHOD_SEED)}, force_vk=True)
         elif w in ("c3", "c4", "c5"):
             blocked(ref, w, C[w], synth.MATRIX_SEED, args.threads, force_vk=(w == "c4"))
+        elif w == "c5lapack":  # c5 with LAPACK on the reference's Gram: a cross-check of the c5 fixture
+            blocked(ref, "c5lapack", C["c5"], synth.MATRIX_SEED, args.threads, eig="lapack")
         else:
             raise SystemExit(f"unknown fixture {w}")

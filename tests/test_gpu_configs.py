@@ -34,6 +34,8 @@ CASES = [
     ("c3", "lanczos", 0, 0), ("c3", "truncated", 0, 0),
     ("c4", "truncated", 0, 0),
     ("c5", "truncated", 0, 0), ("c5", "randomized", 4096, 3), ("c5", "lanczos", 0, 0),
+    # the same c5 bytes against LAPACK on the reference's Gram (a labelled cross-check oracle, minutes to make)
+    ("c5lapack", "truncated", 0, 0), ("c5lapack", "randomized", 4096, 3), ("c5lapack", "lanczos", 0, 0),
 ]
 
 _state = {"name": None, "a": None}
@@ -57,14 +59,15 @@ def _fixture(name):
 
 def _matrix(eng, name, gz):
     import torch
-    if _state["name"] != name:
+    key = str(gz["cfg"]) + ":" + str(int(gz["m"]))  # fixtures of the same input share the matrix
+    if _state["name"] != key:
         _state["a"] = None
         gc.collect()
         torch.cuda.empty_cache()
         cfg = synth.CONFIGS[str(gz["cfg"])]
         _state["a"] = synth.device_matrix(eng, int(gz["m"]), int(gz["n"]), cfg.spectrum(int(gz["n"])),
                                           float(gz["sigma"]), seed=int(gz["seed"]))
-        _state["name"] = name
+        _state["name"] = key
     return _state["a"]
 
 

@@ -28,10 +28,11 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("config", nargs="?", default="c5")
     ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--fixture", default=None, help="fixture name under tests/golden (default: the config's)")
     args = ap.parse_args()
     cfg = bench.config(args.config)
     m, n, t = cfg["m"], cfg["n"], cfg["t"]
-    gz = np.load(os.path.join(ROOT, "tests", "golden", f"{args.config}.npz"))
+    gz = np.load(os.path.join(ROOT, "tests", "golden", f"{args.fixture or args.config}.npz"))
     eng = Engine(0)
     torch.cuda.set_stream(eng.stream)
     a0, _ = bench.generate(eng, cfg, 1, 0)
