@@ -6,10 +6,11 @@ import sys
 
 rows = []
 for line in open(sys.argv[1]):
-    m = re.match(r"^\.?(c\w+) (\w+) (vs reference \w+ )?(\{.*\})\s*$", line.strip())
+    m = re.match(r"^[.sFEx]*(c\w+) (\w+) (vs reference \w+ )?(\{.*\})\s*$", line.strip())
     if not m:
         continue
     cfg, method, vs, d = m.groups()
+    d = re.sub(r"np\.(?:float64|int64)\(([^()]*)\)", r"\1", d)
     try:
         p = ast.literal_eval(d)
     except Exception:  # noqa: BLE001
