@@ -77,6 +77,7 @@ struct Params {
     const long long* utab;
     const long long* cfirst;
     const long long* tfirst;
+    const long long* clist;  // CTA b runs the units clist[cfirst[b]] .. clist[cfirst[b + 1] - 1]
 };
 
 // 3-D box: (m_lo 16, k 16, m_hi 8) lands as m_lo*8 + k*128 + m_hi*2048 bytes,
@@ -274,7 +275,8 @@ __global__ void __launch_bounds__(THREADS, 1)
             const int u_begin = p.utab ? static_cast<int>(p.cfirst[blockIdx.x]) : static_cast<int>(blockIdx.x);
             const int u_end = p.utab ? static_cast<int>(p.cfirst[blockIdx.x + 1]) : p.units;
             const int u_step = p.utab ? 1 : static_cast<int>(gridDim.x);
-            for (int u = u_begin; u < u_end; u += u_step) {
+            for (int j = u_begin; j < u_end; j += u_step) {
+                const int u = p.utab ? static_cast<int>(p.clist[j]) : j;
                 const Unit w = decode(p, u);
                 for (int64_t k = w.k0; k < w.k1; k += BK) {
                     mbar_wait(&empty[stage], phase ^ 1);
@@ -335,7 +337,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int u_begin = p.utab ? static_cast<int>(p.cfirst[blockIdx.x]) : static_cast<int>(blockIdx.x);
     const int u_end = p.utab ? static_cast<int>(p.cfirst[blockIdx.x + 1]) : p.units;
     const int u_step = p.utab ? 1 : static_cast<int>(gridDim.x);
-    for (int u = u_begin; u < u_end; u += u_step) {
+    for (int j = u_begin; j < u_end; j += u_step) {
+        const int u = p.utab ? static_cast<int>(p.clist[j]) : j;
         const Unit w = decode(p, u);
 #pragma unroll
         for (int t = 0; t < 8; ++t)
@@ -598,6 +601,72 @@ std::vector<long long> build_syrk_line(int tiles, int64_t K, int ctas, int diag_
     out.insert(out.end(), utab.begin(), utab.end());
     out.insert(out.end(), cfirst.begin(), cfirst.end());
     out.insert(out.end(), tfirst.begin(), tfirst.end());
+    for (long long u = 0; u < out[0]; ++u) out.push_back(u);  // clist: every CTA's units are consecutive
+    return out;
+}
+
+// The same table format for the lockstep variant: the uniform tiles x S k-chunks grid (one unit per CTA, all
+// CTAs of a chunk walking the same k window, so a column block of A is fetched once for the tiles that share
+// it), rebalanced by handing the last fraction g of every full unit's chunk, cut into sub-tails, to the CTAs of
+// the cheaper diagonal units: 1 - g = w_d / 32 + (full / diag) g. Empty when the shape does not fit (fewer
+// than two chunks per tile in one wave, or no off-diagonal tile).
+std::vector<long long> build_syrk_lockstep(int tiles, int64_t K, int ctas, int diag_weight) {
+    const int n_tiles = tiles * (tiles + 1) / 2, n_full = tiles * (tiles - 1) / 2, n_diag = tiles;
+    const int S = ctas / n_tiles;
+    const long long ks = ceil_div(K, BK);
+    if (tiles < 2 || S < 2 || ks < 64LL * S) return {};
+    const double g = (1.0 - diag_weight / 32.0) / (1.0 + static_cast<double>(n_full) / n_diag);
+    const int h = (n_full % n_diag == 0) ? 1 : 2;  // sub-tails per full unit: (n_full h) % n_diag == 0
+    std::vector<char> is_diag(static_cast<size_t>(n_tiles), 0);
+    for (int tj = 0; tj < tiles; ++tj) is_diag[static_cast<size_t>(tj * (tj + 1) / 2 + tj)] = 1;
+    std::vector<long long> utab, tfirst(static_cast<size_t>(n_tiles) + 1);
+    // unit ids: main / diagonal piece of (tile, chunk), and the sub-tails of (tile, chunk)
+    std::vector<long long> base_unit(static_cast<size_t>(n_tiles) * S), tail_unit(static_cast<size_t>(n_tiles) * S * h, -1);
+    for (int t = 0; t < n_tiles; ++t) {
+        tfirst[static_cast<size_t>(t)] = static_cast<long long>(utab.size() / 3);
+        for (int sc = 0; sc < S; ++sc) {
+            const long long c0 = ks * sc / S, c1 = ks * (sc + 1) / S;
+            const long long tail = is_diag[static_cast<size_t>(t)] ? 0 : static_cast<long long>(g * (c1 - c0) + 0.5);
+            auto push = [&](long long a, long long b) {
+                utab.push_back(t);
+                utab.push_back(std::min<long long>(a * BK, K));
+                utab.push_back(std::min<long long>(b * BK, K));
+                return static_cast<long long>(utab.size() / 3 - 1);
+            };
+            base_unit[static_cast<size_t>(t) * S + sc] = push(c0, c1 - tail);
+            for (int i = 0; i < h && tail > 0; ++i) {
+                const long long a = c1 - tail + tail * i / h, b = c1 - tail + tail * (i + 1) / h;
+                if (b > a) tail_unit[(static_cast<size_t>(t) * S + sc) * h + i] = push(a, b);
+            }
+        }
+    }
+    tfirst[static_cast<size_t>(n_tiles)] = static_cast<long long>(utab.size() / 3);
+    // CTA (chunk sc, tile t) = sc * n_tiles + t; the sub-tails of a chunk are dealt to its diagonal CTAs
+    std::vector<std::vector<long long>> lists(static_cast<size_t>(ctas));
+    for (int sc = 0; sc < S; ++sc) {
+        std::vector<int> diag_ctas;
+        for (int t = 0; t < n_tiles; ++t) {
+            lists[static_cast<size_t>(sc) * n_tiles + t].push_back(base_unit[static_cast<size_t>(t) * S + sc]);
+            if (is_diag[static_cast<size_t>(t)]) diag_ctas.push_back(sc * n_tiles + t);
+        }
+        size_t next = 0;
+        for (int t = 0; t < n_tiles; ++t)
+            for (int i = 0; i < h; ++i) {
+                const long long u = tail_unit[(static_cast<size_t>(t) * S + sc) * h + i];
+                if (u >= 0) lists[static_cast<size_t>(diag_ctas[next++ % diag_ctas.size()])].push_back(u);
+            }
+    }
+    std::vector<long long> out, cfirst(static_cast<size_t>(ctas) + 1), clist;
+    for (int b = 0; b < ctas; ++b) {
+        cfirst[static_cast<size_t>(b)] = static_cast<long long>(clist.size());
+        clist.insert(clist.end(), lists[static_cast<size_t>(b)].begin(), lists[static_cast<size_t>(b)].end());
+    }
+    cfirst[static_cast<size_t>(ctas)] = static_cast<long long>(clist.size());
+    out.push_back(static_cast<long long>(utab.size() / 3));
+    out.insert(out.end(), utab.begin(), utab.end());
+    out.insert(out.end(), cfirst.begin(), cfirst.end());
+    out.insert(out.end(), tfirst.begin(), tfirst.end());
+    out.insert(out.end(), clist.begin(), clist.end());
     return out;
 }
 
@@ -814,7 +883,10 @@ void syrk(Ctx* c, int64_t m, int64_t n, const double* A, int64_t lda, double* G,
     if (m >= kSyrkLineMinRows && !(sk_env && std::atoi(sk_env) == 0)) {
         const char* dw_env = std::getenv("SVDK_SYRK_DIAGW");
         const int diag_w = dw_env ? std::min(32, std::max(1, std::atoi(dw_env))) : kSyrkDiagWeight;
-        std::vector<long long> host = build_syrk_line(p.tiles_m, m, c->num_sms, diag_w);
+        // SVDK_SYRK_LINE=2: the lockstep grid with the diagonal CTAs taking the full units' tails
+        std::vector<long long> host;
+        if (sk_env && std::atoi(sk_env) == 2) host = build_syrk_lockstep(p.tiles_m, m, c->num_sms, diag_w);
+        if (host.empty()) host = build_syrk_line(p.tiles_m, m, c->num_sms, diag_w);
         const size_t units = static_cast<size_t>(host[0]);
         line = DBuf(c, host.size());
         h2d(c, line.p(), reinterpret_cast<const double*>(host.data()), static_cast<int64_t>(host.size()));
@@ -822,6 +894,7 @@ void syrk(Ctx* c, int64_t m, int64_t n, const double* A, int64_t lda, double* G,
         p.utab = base + 1;
         p.cfirst = p.utab + 3 * units;
         p.tfirst = p.cfirst + c->num_sms + 1;
+        p.clist = p.tfirst + p.n_tiles + 1;
         p.units = static_cast<int>(units);
         p.splits = 2;  // partial tiles + the reduction kernel
     }
@@ -900,7 +973,10 @@ void gemm(Ctx* c, bool transa, int64_t m, int64_t n, int64_t k, const double* A,
 extern "C" long long svdk_debug_syrk_line(int tiles, long long K, int ctas, int diag_weight, long long* out,
                                           long long cap) {
     if (tiles < 1 || K < 1 || ctas < 1) return -1;
-    const std::vector<long long> t = svdk::build_syrk_line(tiles, K, ctas, diag_weight > 0 ? diag_weight : svdk::kSyrkDiagWeight);
+    // diag_weight < 0: the lockstep variant with weight -diag_weight (0 entries when the shape does not fit)
+    const std::vector<long long> t =
+        diag_weight < 0 ? svdk::build_syrk_lockstep(tiles, K, ctas, -diag_weight)
+                        : svdk::build_syrk_line(tiles, K, ctas, diag_weight > 0 ? diag_weight : svdk::kSyrkDiagWeight);
     if (out && static_cast<long long>(t.size()) <= cap) std::copy(t.begin(), t.end(), out);
     return static_cast<long long>(t.size());
 }

@@ -314,43 +314,83 @@ def test_facade_tools_host_match_reference(rt):
     assert report_text == rt.ordering_report(TOOL_RECORDS)[0]
 
 
-# --------------------------------------------------------------------------- SYRK work line (host logic)
+# --------------------------------------------------------------------------- SYRK work tables (host logic)
+def _syrk_table(tiles, rows, ctas, weight):
+    import ctypes as C
+    from paper_1906_12085_b200 import _lib
+    lib = C.CDLL(_lib.LIB_PATH)
+    lib.svdk_debug_syrk_line.restype = C.c_longlong
+    lib.svdk_debug_syrk_line.argtypes = [C.c_int, C.c_longlong, C.c_int, C.c_int, C.POINTER(C.c_longlong), C.c_longlong]
+    need = lib.svdk_debug_syrk_line(tiles, rows, ctas, weight, None, 0)
+    if need <= 0:
+        return None
+    buf = (C.c_longlong * need)()
+    assert lib.svdk_debug_syrk_line(tiles, rows, ctas, weight, buf, need) == need
+    t = list(buf)
+    units, n_tiles = t[0], tiles * (tiles + 1) // 2
+    utab = [tuple(t[1 + 3 * u:4 + 3 * u]) for u in range(units)]
+    o = 1 + 3 * units
+    cfirst, tfirst, clist = t[o:o + ctas + 1], t[o + ctas + 1:o + ctas + 1 + n_tiles + 1], t[o + ctas + n_tiles + 2:]
+    return utab, cfirst, tfirst, clist
+
+
+def _check_syrk_table(tiles, rows, ctas, table, slack_steps):
+    utab, cfirst, tfirst, clist = table
+    units, n_tiles = len(utab), tiles * (tiles + 1) // 2
+    assert len(tfirst) == n_tiles + 1 and cfirst[0] == 0 and cfirst[-1] == units and tfirst[-1] == units
+    assert sorted(clist) == list(range(units))  # every unit runs on exactly one CTA
+    assert all(a <= b for a, b in zip(cfirst, cfirst[1:]))
+    diag = {tj * (tj + 1) // 2 + tj for tj in range(tiles)}
+    for tile in range(n_tiles):  # a tile's pieces are contiguous in the table, in k order, and cover [0, K)
+        pieces = utab[tfirst[tile]:tfirst[tile + 1]]
+        assert pieces and all(p[0] == tile for p in pieces)
+        assert pieces[0][1] == 0 and pieces[-1][2] == rows
+        assert all(a[2] == b[1] and a[2] % 16 == 0 for a, b in zip(pieces, pieces[1:]))
+        assert all(p[2] > p[1] for p in pieces)
+    loads = []
+    for b in range(ctas):
+        w = 0
+        for u in clist[cfirst[b]:cfirst[b + 1]]:
+            tile, k0, k1 = utab[u]
+            w += -(-(k1 - k0) // 16) * (19 if tile in diag else 32)
+        loads.append(w)
+    busy = [w for w in loads if w]
+    mean = sum(busy) / len(busy)
+    assert max(busy) - mean <= 32 * slack_steps and mean - min(busy) <= 32 * slack_steps, (max(busy), mean, min(busy))
+    return loads
+
+
 @pytest.mark.parametrize("tiles,rows,ctas", [(8, 8388608, 148), (8, 200000, 148), (32, 65536, 148), (16, 500000, 148),
                                              (2, 32768, 148), (1, 40000, 148), (3, 33001, 148), (8, 1 << 20, 7)])
 def test_syrk_work_line_table(tiles, rows, ctas):
     """build_syrk_line (csrc/gemm_f64.cu): every upper tile's k range [0, K) is covered exactly once by
     contiguous pieces in piece order, a tile's pieces and a CTA's pieces are contiguous in the table, and the
     CTAs' weights (32 per full k-step, 19 per diagonal one) are equal to within one k-step per piece."""
-    import ctypes as C
-    from paper_1906_12085_b200 import _lib
-    lib = C.CDLL(_lib.LIB_PATH)
-    lib.svdk_debug_syrk_line.restype = C.c_longlong
-    lib.svdk_debug_syrk_line.argtypes = [C.c_int, C.c_longlong, C.c_int, C.c_int, C.POINTER(C.c_longlong), C.c_longlong]
-    need = lib.svdk_debug_syrk_line(tiles, rows, ctas, 0, None, 0)
-    buf = (C.c_longlong * need)()
-    assert lib.svdk_debug_syrk_line(tiles, rows, ctas, 0, buf, need) == need
-    t = list(buf)
-    units, n_tiles = t[0], tiles * (tiles + 1) // 2
-    utab = [tuple(t[1 + 3 * u:4 + 3 * u]) for u in range(units)]
-    cfirst = t[1 + 3 * units:1 + 3 * units + ctas + 1]
-    tfirst = t[1 + 3 * units + ctas + 1:]
-    assert len(tfirst) == n_tiles + 1 and cfirst[0] == 0 and cfirst[-1] == units and tfirst[-1] == units
-    assert all(a <= b for a, b in zip(cfirst, cfirst[1:]))
-    diag = {tj * (tj + 1) // 2 + tj for tj in range(tiles)}
-    for tile in range(n_tiles):
-        pieces = utab[tfirst[tile]:tfirst[tile + 1]]
-        assert pieces and all(p[0] == tile for p in pieces)
-        assert pieces[0][1] == 0 and pieces[-1][2] == rows
-        assert all(a[2] == b[1] and a[2] % 16 == 0 for a, b in zip(pieces, pieces[1:]))
-        assert all(p[2] > p[1] for p in pieces)
-    assert sorted(u[0] for u in utab) == [u[0] for u in utab]  # tile order
-    loads = []
-    for b in range(ctas):
-        w = 0
-        for tile, k0, k1 in utab[cfirst[b]:cfirst[b + 1]]:
-            w += -(-(k1 - k0) // 16) * (19 if tile in diag else 32)
-        loads.append(w)
-    mean = sum(loads) / ctas
+    table = _syrk_table(tiles, rows, ctas, 0)
+    utab, cfirst, tfirst, clist = table
+    assert clist == list(range(len(utab)))  # the line: consecutive units per CTA
+    assert sorted(u[0] for u in utab) == [u[0] for u in utab]
     pieces_max = max(cfirst[b + 1] - cfirst[b] for b in range(ctas))
-    assert max(loads) - mean <= 32 * (pieces_max + 1), (max(loads), mean)
-    assert mean - min(loads) <= 32 * (pieces_max + 1), (min(loads), mean)
+    _check_syrk_table(tiles, rows, ctas, table, pieces_max + 1)
+
+
+@pytest.mark.parametrize("tiles,rows,ctas", [(8, 8388608, 148), (8, 200000, 148), (8, 1 << 20, 148), (4, 65536, 148),
+                                             (7, 300000, 148)])
+def test_syrk_lockstep_table(tiles, rows, ctas):
+    """build_syrk_lockstep: the tiles x S k-chunk grid with the tails of the full units handed to the CTAs
+    of the diagonal units: full coverage, one main piece per CTA starting at its chunk's first k-step (so the
+    CTAs of a chunk walk the same k window), balanced weights; not applicable shapes return no table."""
+    table = _syrk_table(tiles, rows, ctas, -19)
+    assert table is not None
+    utab, cfirst, tfirst, clist = table
+    n_tiles = tiles * (tiles + 1) // 2
+    S = ctas // n_tiles
+    ks = -(-rows // 16)
+    starts = {16 * (ks * sc // S) for sc in range(S)}
+    for b in range(n_tiles * S):
+        first = utab[clist[cfirst[b]]]
+        assert first[1] in starts, (b, first)
+    sub_tails = 2 if (tiles * (tiles - 1) // 2) % tiles else 1
+    _check_syrk_table(tiles, rows, ctas, table, 2 * tiles * sub_tails + 4)
+    assert _syrk_table(32, 65536, 148, -19) is None and _syrk_table(1, 40000, 148, -19) is None
+    assert _syrk_table(2, 32768, 148, -19) is None  # chunks too short
