@@ -1973,7 +1973,10 @@ int run_plan(Ctx* c, JacobiPlan& P) {
 }
 
 // Largest n_pad that runs the solve-ahead chain by default (see jacobi_pair_solve_ahead).
-constexpr int64_t kAheadMaxN = 1024;
+// Measured (eig_sym ms, fused / separate kernels): n = 1024 8.9 / 10.8, 1152 10.3 / 13.4, 1280 16.1 / 15.5,
+// 1536 25.9 / 25.2, 1792 42.2 / 32.9, 2048 86.6 / 45.2 — above ~1200 the worker CTAs' task throughput
+// (one CTA per SM) falls behind the separate update kernels.
+constexpr int64_t kAheadMaxN = 1152;
 
 template <int TB>
 void build_pair_plan(Ctx* c, JacobiPlan& P) {
