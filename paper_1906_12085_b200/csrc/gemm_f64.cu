@@ -873,30 +873,39 @@ void syrk(Ctx* c, int64_t m, int64_t n, const double* A, int64_t lda, double* G,
     p.ldc = ldg;
     p.alpha = alpha;
     p.beta_one = beta_one ? 1 : 0;
-    // Tall Gram (the c2 / c4 / c5 shapes): one work line over all SMs. A diagonal
-    // tile only needs its 136 upper 8 x 8 blocks (17 / 32 of a tile's DMMAs), so
-    // the line weighs its k-steps kSyrkDiagWeight against 32 for the other tiles and every CTA
-    // gets the same weight as a contiguous piece of it (pieces may straddle two
-    // tiles); the per-piece partial tiles are summed per tile in piece order.
+    // Tall Gram (m >= kSyrkLineMinRows): a table of (tile, k0, k1) units instead of the uniform tiles x
+    // splits grid, in which a diagonal tile computes only its 136 upper 8 x 8 blocks (17 / 32 of a tile's
+    // DMMAs; diag_unit) and its k-steps weigh kSyrkDiagWeight against 32:
+    //   default   the lockstep table where the shape fits it (>= 2 k-chunks per tile in one wave: n <= ~1400;
+    //             c2 / c4): the uniform k-chunk grid — all CTAs of a chunk walk the same k window, so a
+    //             column block of A is fetched once for the tiles sharing it — with the last 9% of every
+    //             full unit's chunk handed to the CTAs of the cheaper diagonal units; else the uniform grid
+    //   =1        the work line: all k-steps of all tiles end to end, cut into equal-weight contiguous
+    //             pieces per CTA (pieces may straddle two tiles). 3-5% faster than the default on the Gram,
+    //             but the pieces sit at unrelated k offsets and A is re-fetched per tile: 7x (n = 1024) to
+    //             30x (n = 4096) the algorithmic DRAM reads
+    //   =0        always the uniform grid
+    // The per-unit partial tiles are summed per tile in unit order (fixed order, exact mirror).
     DBuf line;
     const char* sk_env = std::getenv("SVDK_SYRK_LINE");
-    if (m >= kSyrkLineMinRows && !(sk_env && std::atoi(sk_env) == 0)) {
+    const int sk_mode = sk_env ? std::atoi(sk_env) : 2;
+    if (m >= kSyrkLineMinRows && sk_mode != 0) {
         const char* dw_env = std::getenv("SVDK_SYRK_DIAGW");
         const int diag_w = dw_env ? std::min(32, std::max(1, std::atoi(dw_env))) : kSyrkDiagWeight;
-        // SVDK_SYRK_LINE=2: the lockstep grid with the diagonal CTAs taking the full units' tails
-        std::vector<long long> host;
-        if (sk_env && std::atoi(sk_env) == 2) host = build_syrk_lockstep(p.tiles_m, m, c->num_sms, diag_w);
-        if (host.empty()) host = build_syrk_line(p.tiles_m, m, c->num_sms, diag_w);
-        const size_t units = static_cast<size_t>(host[0]);
-        line = DBuf(c, host.size());
-        h2d(c, line.p(), reinterpret_cast<const double*>(host.data()), static_cast<int64_t>(host.size()));
-        const long long* base = reinterpret_cast<const long long*>(line.p());
-        p.utab = base + 1;
-        p.cfirst = p.utab + 3 * units;
-        p.tfirst = p.cfirst + c->num_sms + 1;
-        p.clist = p.tfirst + p.n_tiles + 1;
-        p.units = static_cast<int>(units);
-        p.splits = 2;  // partial tiles + the reduction kernel
+        std::vector<long long> host = sk_mode == 1 ? build_syrk_line(p.tiles_m, m, c->num_sms, diag_w)
+                                                   : build_syrk_lockstep(p.tiles_m, m, c->num_sms, diag_w);
+        if (!host.empty()) {
+            const size_t units = static_cast<size_t>(host[0]);
+            line = DBuf(c, host.size());
+            h2d(c, line.p(), reinterpret_cast<const double*>(host.data()), static_cast<int64_t>(host.size()));
+            const long long* base = reinterpret_cast<const long long*>(line.p());
+            p.utab = base + 1;
+            p.cfirst = p.utab + 3 * units;
+            p.tfirst = p.cfirst + c->num_sms + 1;
+            p.clist = p.tfirst + p.n_tiles + 1;
+            p.units = static_cast<int>(units);
+            p.splits = 2;  // partial tiles + the reduction kernel
+        }
     }
     const CUtensorMap ma = make_map(A, m, n, lda, BK, BM);
     launch(c, p, ma, ma);
