@@ -227,7 +227,8 @@ __device__ __forceinline__ void diag_unit(double (&acc)[8][4][2], const uint8_t*
     }
 }
 
-template <bool AMM>
+// TAB: the SYRK unit tables (its own instantiation, so the plain TN / NN kernels carry none of that code).
+template <bool AMM, bool TAB = false>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                 const Params p) {
@@ -272,11 +273,12 @@ __global__ void __launch_bounds__(THREADS, 1)
                          : "memory");
             int stage = 0;
             uint32_t phase = 0;
-            const int u_begin = p.utab ? static_cast<int>(p.cfirst[blockIdx.x]) : static_cast<int>(blockIdx.x);
-            const int u_end = p.utab ? static_cast<int>(p.cfirst[blockIdx.x + 1]) : p.units;
-            const int u_step = p.utab ? 1 : static_cast<int>(gridDim.x);
+            constexpr bool tab = TAB;
+            const int u_begin = tab ? static_cast<int>(p.cfirst[blockIdx.x]) : static_cast<int>(blockIdx.x);
+            const int u_end = tab ? static_cast<int>(p.cfirst[blockIdx.x + 1]) : p.units;
+            const int u_step = tab ? 1 : static_cast<int>(gridDim.x);
             for (int j = u_begin; j < u_end; j += u_step) {
-                const int u = p.utab ? static_cast<int>(p.clist[j]) : j;
+                const int u = tab ? static_cast<int>(p.clist[j]) : j;
                 const Unit w = decode(p, u);
                 for (int64_t k = w.k0; k < w.k1; k += BK) {
                     mbar_wait(&empty[stage], phase ^ 1);
@@ -334,18 +336,19 @@ __global__ void __launch_bounds__(THREADS, 1)
     double acc[8][4][2];
     int stage = 0;
     uint32_t phase = 0;
-    const int u_begin = p.utab ? static_cast<int>(p.cfirst[blockIdx.x]) : static_cast<int>(blockIdx.x);
-    const int u_end = p.utab ? static_cast<int>(p.cfirst[blockIdx.x + 1]) : p.units;
-    const int u_step = p.utab ? 1 : static_cast<int>(gridDim.x);
+    constexpr bool tab = TAB;
+    const int u_begin = tab ? static_cast<int>(p.cfirst[blockIdx.x]) : static_cast<int>(blockIdx.x);
+    const int u_end = tab ? static_cast<int>(p.cfirst[blockIdx.x + 1]) : p.units;
+    const int u_step = tab ? 1 : static_cast<int>(gridDim.x);
     for (int j = u_begin; j < u_end; j += u_step) {
-        const int u = p.utab ? static_cast<int>(p.clist[j]) : j;
+        const int u = tab ? static_cast<int>(p.clist[j]) : j;
         const Unit w = decode(p, u);
 #pragma unroll
         for (int t = 0; t < 8; ++t)
 #pragma unroll
             for (int n = 0; n < 4; ++n) acc[t][n][0] = acc[t][n][1] = 0.0;
 
-        if (!AMM && p.utab && w.diag) {
+        if (tab && w.diag) {
             // Diagonal tile of the SYRK work line: only the 136 upper 8 x 8 blocks
             // (diag_unit, one branch-free instantiation per consumer warp).
             switch (warp) {
@@ -677,6 +680,7 @@ bool tma_ok(const void* p, int64_t ld) {
 void launch(Ctx* c, Params& p, const CUtensorMap& ma, const CUtensorMap& mb) {
     ensure_smem_attr(reinterpret_cast<const void*>(gemm_kernel<false>), SMEM_BYTES);
     ensure_smem_attr(reinterpret_cast<const void*>(gemm_kernel<true>), SMEM_BYTES);
+    ensure_smem_attr(reinterpret_cast<const void*>(gemm_kernel<false, true>), SMEM_BYTES);
     DBuf partial;
     if (p.splits > 1) {
         partial = DBuf(c, static_cast<size_t>(p.units) * TILE_ELEMS);
@@ -695,6 +699,8 @@ void launch(Ctx* c, Params& p, const CUtensorMap& ma, const CUtensorMap& mb) {
                          flops, bytes);
         if (p.a_mmajor)
             gemm_kernel<true><<<grid, THREADS, SMEM_BYTES, c->stream>>>(ma, mb, p);
+        else if (p.utab)
+            gemm_kernel<false, true><<<grid, THREADS, SMEM_BYTES, c->stream>>>(ma, mb, p);
         else
             gemm_kernel<false><<<grid, THREADS, SMEM_BYTES, c->stream>>>(ma, mb, p);
         SVDK_CHECK_LAUNCH();
