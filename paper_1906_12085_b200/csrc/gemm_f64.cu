@@ -31,6 +31,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <utility>
 #include <vector>
 
 #include "svdk_internal.h"
@@ -611,20 +612,25 @@ std::vector<long long> build_syrk_line(int tiles, int64_t K, int ctas, int diag_
 // The same table format for the lockstep variant: the uniform tiles x S k-chunks grid (one unit per CTA, all
 // CTAs of a chunk walking the same k window, so a column block of A is fetched once for the tiles that share
 // it), rebalanced by handing the last fraction g of every full unit's chunk, cut into sub-tails, to the CTAs of
-// the cheaper diagonal units: 1 - g = w_d / 32 + (full / diag) g. Empty when the shape does not fit (fewer
+// the cheaper diagonal units and to the CTAs the grid leaves without a unit (c4: 144 units on 148 SMs). Empty when the shape does not fit (fewer
 // than two chunks per tile in one wave, or no off-diagonal tile).
 std::vector<long long> build_syrk_lockstep(int tiles, int64_t K, int ctas, int diag_weight) {
     const int n_tiles = tiles * (tiles + 1) / 2, n_full = tiles * (tiles - 1) / 2, n_diag = tiles;
     const int S = ctas / n_tiles;
     const long long ks = ceil_div(K, BK);
     if (tiles < 2 || S < 2 || ks < 64LL * S) return {};
-    const double g = (1.0 - diag_weight / 32.0) / (1.0 + static_cast<double>(n_full) / n_diag);
-    const int h = (n_full % n_diag == 0) ? 1 : 2;  // sub-tails per full unit: (n_full h) % n_diag == 0
+    // Helpers of the tails: the S n_diag diagonal CTAs (spare 1 - w_d / 32 of a unit each) and the
+    // ctas - S n_tiles CTAs without a unit of their own. Balanced finish at T = 1 - g of a unit:
+    //   n_full g = n_diag (T - w_d / 32) + F T,  F = free CTAs per chunk.
+    const int n_free = ctas - S * n_tiles;
+    const double wd = diag_weight / 32.0, F = static_cast<double>(n_free) / S;
+    const double g = (n_diag * (1.0 - wd) + F) / (n_full + n_diag + F);
+    constexpr int H = 16;  // sub-tails per full unit (a helper ends within half a sub-tail of the mean: ~0.4%)
     std::vector<char> is_diag(static_cast<size_t>(n_tiles), 0);
     for (int tj = 0; tj < tiles; ++tj) is_diag[static_cast<size_t>(tj * (tj + 1) / 2 + tj)] = 1;
     std::vector<long long> utab, tfirst(static_cast<size_t>(n_tiles) + 1);
-    // unit ids: main / diagonal piece of (tile, chunk), and the sub-tails of (tile, chunk)
-    std::vector<long long> base_unit(static_cast<size_t>(n_tiles) * S), tail_unit(static_cast<size_t>(n_tiles) * S * h, -1);
+    std::vector<long long> base_unit(static_cast<size_t>(n_tiles) * S);
+    std::vector<std::pair<long long, long long>> tails;  // (k-steps, unit id)
     for (int t = 0; t < n_tiles; ++t) {
         tfirst[static_cast<size_t>(t)] = static_cast<long long>(utab.size() / 3);
         for (int sc = 0; sc < S; ++sc) {
@@ -637,27 +643,39 @@ std::vector<long long> build_syrk_lockstep(int tiles, int64_t K, int ctas, int d
                 return static_cast<long long>(utab.size() / 3 - 1);
             };
             base_unit[static_cast<size_t>(t) * S + sc] = push(c0, c1 - tail);
-            for (int i = 0; i < h && tail > 0; ++i) {
-                const long long a = c1 - tail + tail * i / h, b = c1 - tail + tail * (i + 1) / h;
-                if (b > a) tail_unit[(static_cast<size_t>(t) * S + sc) * h + i] = push(a, b);
+            for (int i = 0; i < H && tail > 0; ++i) {
+                const long long a = c1 - tail + tail * i / H, b = c1 - tail + tail * (i + 1) / H;
+                if (b > a) tails.emplace_back(b - a, push(a, b));
             }
         }
     }
     tfirst[static_cast<size_t>(n_tiles)] = static_cast<long long>(utab.size() / 3);
-    // CTA (chunk sc, tile t) = sc * n_tiles + t; the sub-tails of a chunk are dealt to its diagonal CTAs
+    // CTA (chunk sc, tile t) = sc * n_tiles + t, then the free CTAs. Every sub-tail goes to the helper
+    // with the least work so far (work in full-tile k-steps; longest sub-tails first).
     std::vector<std::vector<long long>> lists(static_cast<size_t>(ctas));
-    for (int sc = 0; sc < S; ++sc) {
-        std::vector<int> diag_ctas;
+    std::vector<double> work(static_cast<size_t>(ctas), 0.0);
+    std::vector<int> helpers;
+    for (int sc = 0; sc < S; ++sc)
         for (int t = 0; t < n_tiles; ++t) {
-            lists[static_cast<size_t>(sc) * n_tiles + t].push_back(base_unit[static_cast<size_t>(t) * S + sc]);
-            if (is_diag[static_cast<size_t>(t)]) diag_ctas.push_back(sc * n_tiles + t);
-        }
-        size_t next = 0;
-        for (int t = 0; t < n_tiles; ++t)
-            for (int i = 0; i < h; ++i) {
-                const long long u = tail_unit[(static_cast<size_t>(t) * S + sc) * h + i];
-                if (u >= 0) lists[static_cast<size_t>(diag_ctas[next++ % diag_ctas.size()])].push_back(u);
+            const int b = sc * n_tiles + t;
+            const long long len = ks * (sc + 1) / S - ks * sc / S;
+            lists[static_cast<size_t>(b)].push_back(base_unit[static_cast<size_t>(t) * S + sc]);
+            if (is_diag[static_cast<size_t>(t)]) {
+                work[static_cast<size_t>(b)] = wd * static_cast<double>(len);
+                helpers.push_back(b);
             }
+        }
+    for (int b = S * n_tiles; b < ctas; ++b) helpers.push_back(b);
+    std::stable_sort(tails.begin(), tails.end(),
+                     [](const std::pair<long long, long long>& x, const std::pair<long long, long long>& y) {
+                         return x.first > y.first;
+                     });
+    for (const auto& tl : tails) {
+        int best = helpers[0];
+        for (int hb : helpers)
+            if (work[static_cast<size_t>(hb)] < work[static_cast<size_t>(best)]) best = hb;
+        lists[static_cast<size_t>(best)].push_back(tl.second);
+        work[static_cast<size_t>(best)] += static_cast<double>(tl.first);
     }
     std::vector<long long> out, cfirst(static_cast<size_t>(ctas) + 1), clist;
     for (int b = 0; b < ctas; ++b) {
