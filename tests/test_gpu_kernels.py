@@ -22,6 +22,25 @@ def test_gram_vs_numpy(sk, m, n):
     assert np.array_equal(g, g.T), "gram must be exactly symmetric (kernels.cpp:92-93)"
 
 
+@pytest.mark.parametrize("mode", ["default", "line", "uniform"])
+@pytest.mark.parametrize("m,n", [(40000, 300), (33001, 1100), (70000, 129), (32768, 128), (50000, 1500)])
+def test_gram_tall_unit_tables(sk, monkeypatch, mode, m, n):
+    """Tall Grams (m >= 32768 rows) on every unit table: the lockstep table (default where it fits: ragged
+    last tiles, odd / even tile counts, one tile), the work line, and the uniform grid — against numpy,
+    exactly symmetric, and the three tables within rounding of each other. (50000 x 1500 does not fit the
+    lockstep table and runs the uniform grid by default.)"""
+    if mode != "default":
+        monkeypatch.setenv("SVDK_SYRK_LINE", "1" if mode == "line" else "0")
+    rng = np.random.default_rng(m + n)
+    a = np.asfortranarray(rng.standard_normal((m, n)))
+    g = sk.gram(a)
+    ref = a.T @ a
+    cn = np.linalg.norm(a, axis=0)
+    # two summation orders of m products differ by ~sqrt(m) eps relative to |a_i| |a_j| (1.6e-14 seen at m = 50000)
+    assert rel_gemm_err(g, ref, cn, cn) < 5e-14
+    assert np.array_equal(g, g.T), "gram must be exactly symmetric (kernels.cpp:92-93)"
+
+
 def test_gram_vs_reference(sk, ref):
     a = np.asfortranarray(np.random.default_rng(3).standard_normal((3000, 200)))
     g, gr = sk.gram(a), ref.gram(a)
